@@ -1,0 +1,160 @@
+/*
+ * ges_b200.h -- C ABI of the B200-native GES forward renderer.
+ *
+ * The reference has no FFI: its render path is the Python function
+ * ges.forward.render (/root/reference/pkg/src/ges/forward.py:403-417) and the
+ * two passes it calls.  Each entry point below replaces one of those calls
+ * (cited per function); the Python package paper_2504_17545_b200 binds them
+ * with ctypes (INTEGRATION.md shows the binding).  All pointers are DEVICE
+ * pointers unless stated; all calls are stream-ordered and re-entrant per
+ * stream; no global mutable state except the thread-local error string.
+ * Memory is owned by the caller (scene blob, frame workspace, outputs).
+ *
+ * Return codes: 0 ok; GES_EINVAL invalid argument (Python: ValueError);
+ * GES_EDEGREE unsupported SH degree (Python: ValueError, as sh.py:24-31);
+ * GES_EWORKSPACE workspace too small; GES_ECUDA CUDA error (RuntimeError).
+ */
+#ifndef GES_B200_H
+#define GES_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GES_ABI_VERSION 1
+
+#define GES_OK 0
+#define GES_EINVAL 1
+#define GES_EDEGREE 2
+#define GES_EWORKSPACE 3
+#define GES_ECUDA 4
+
+#define GES_LAYERS_FULL 0           /* forward.py:417 */
+#define GES_LAYERS_SURFELS_ONLY 1   /* forward.py:407-410 */
+#define GES_LAYERS_GAUSSIANS_ONLY 2 /* forward.py:412-416 */
+
+/* Pinhole camera, cameras.py:17-80.  w2c is the top 3x4 of world_to_camera,
+ * row-major.  width/height are the BASE resolution; supersample=4 renders the
+ * surfel pass on the camera scaled by 2 (cameras.py:75-80, forward.py:136). */
+typedef struct ges_camera {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double w2c[12];
+} ges_camera_t;
+
+/* RenderSettings, forward.py:36-58 (dtype is always float32 on device,
+ * threads is meaningless on the GPU). */
+typedef struct ges_settings {
+    int32_t supersample;      /* 1 or 4 */
+    int32_t layers;           /* GES_LAYERS_* */
+    int32_t mip;              /* 0/1 */
+    int32_t epsilon_mode;     /* 0 adaptive, 1 constant (forward.py:212-215) */
+    float epsilon_value;
+    int32_t with_geometry;    /* 0/1 */
+    float background[3];
+} ges_settings_t;
+
+/* Source scene in the reference's storage layout (primitives.py:42-161),
+ * float64 device arrays, row-major.  g_filter3d may be NULL (all zero). */
+typedef struct ges_scene_src {
+    int64_t n_surfels, n_gaussians;
+    int32_t sh_degree;        /* 0..3 */
+    int32_t gaussian_dim;     /* 3 = GaussianKind.THREE_D, 2 = TWO_D */
+    const double *s_pos, *s_quat, *s_log_scale, *s_sh;
+    const double *g_pos, *g_raw_opacity, *g_quat, *g_log_scale, *g_sh, *g_filter3d;
+} ges_scene_src_t;
+
+/* Packed device scene (float32, 16-byte aligned SoA).  Filled by
+ * ges_scene_pack; all pointers point into the caller's scene blob. */
+typedef struct ges_scene {
+    int64_t n_surfels, n_gaussians;
+    int32_t sh_degree, gaussian_dim;
+    float *s_pos_s1;      /* n_surfels x 4: pos.xyz, exp(log_scale[0])          */
+    float *s_quat;        /* n_surfels x 4: unit (w, x, y, z)                  */
+    float *s_s2;          /* n_surfels:     exp(log_scale[1])                  */
+    float *s_sh;          /* n_surfels x K x 3                                 */
+    float *g_pos_op;      /* n_gaussians x 4: pos.xyz, eff_opacity             */
+    float *g_quat;        /* n_gaussians x 4                                   */
+    float *g_scale_eps;   /* n_gaussians x 4: eff_scale (s2=0 for 2D), epsilon */
+    float *g_sh;          /* n_gaussians x K x 3                               */
+} ges_scene_t;
+
+/* Output buffers; any may be NULL (not written).  H, W = base resolution.
+ * Layouts match SurfelBuffers / GaussianBuffers / RenderResult
+ * (forward.py:61-82): colours (H,W,3) f32, depth (H,W) f32 (+inf uncovered),
+ * normal (H,W,3) f32, winner (H,W) int32 (-1 uncovered). */
+typedef struct ges_outputs {
+    float *image;
+    float *s_color, *s_depth, *s_normal;
+    int32_t *s_winner;
+    float *g_color, *g_weight, *g_depth, *g_normal;
+} ges_outputs_t;
+
+/* Per-frame counters written by the device (read them after the frame). */
+typedef struct ges_frame_status {
+    int64_t surfel_pairs;     /* tile/surfel pairs the frame needed   */
+    int64_t gaussian_pairs;   /* tile/Gaussian pairs the frame needed */
+    int32_t overflow;         /* nonzero: a pair list exceeded capacity, outputs invalid */
+    int32_t pad;
+} ges_frame_status_t;
+
+int ges_abi_version(void);
+const char *ges_last_error(void);
+
+/* Bytes of the packed scene blob (replaces the lazy property math of
+ * primitives.py:55-56, :113-131 done once per scene instead of per render). */
+size_t ges_scene_bytes(int64_t n_surfels, int64_t n_gaussians, int32_t sh_degree);
+int ges_scene_pack(const ges_scene_src_t *src, void *blob, size_t blob_bytes,
+                   ges_scene_t *out, void *stream);
+
+/* Frame workspace: per-primitive screen records, tile counters and the two
+ * tile lists with the given pair capacities. */
+size_t ges_workspace_bytes(const ges_scene_t *scene, const ges_camera_t *cam,
+                           const ges_settings_t *st, int64_t surfel_pair_cap,
+                           int64_t gaussian_pair_cap);
+
+/* Full two-pass render: forward.py:403-417 (render). */
+int ges_render(const ges_scene_t *scene, const ges_camera_t *cam,
+               const ges_settings_t *st, const ges_outputs_t *out,
+               void *workspace, size_t ws_bytes, int64_t surfel_pair_cap,
+               int64_t gaussian_pair_cap, ges_frame_status_t *status_dev,
+               void *stream);
+
+/* Pass 1 alone: forward.py:127-209 (rasterize_surfels). */
+int ges_rasterize_surfels(const ges_scene_t *scene, const ges_camera_t *cam,
+                          const ges_settings_t *st, const ges_outputs_t *out,
+                          void *workspace, size_t ws_bytes, int64_t surfel_pair_cap,
+                          ges_frame_status_t *status_dev, void *stream);
+
+/* Pass 2 alone against a given surfel depth map (H,W) f32:
+ * forward.py:218-245 (accumulate_gaussians).  Writes g_* outputs. */
+int ges_accumulate_gaussians(const ges_scene_t *scene, const ges_camera_t *cam,
+                             const float *surfel_depth, const ges_settings_t *st,
+                             const ges_outputs_t *out, void *workspace, size_t ws_bytes,
+                             int64_t gaussian_pair_cap, ges_frame_status_t *status_dev,
+                             void *stream);
+
+/* forward.py:384-388 (composite): image = (C_s*w + C_G)/(w + W_G); n = H*W. */
+int ges_composite(const float *surfel_color, const float *g_color, const float *g_weight,
+                  float surfel_weight, float *image, int64_t n, void *stream);
+
+/* forward.py:391-400 (smooth_geometry). */
+int ges_smooth_geometry(const float *s_depth, const float *s_normal, const float *g_depth,
+                        const float *g_normal, const float *g_weight, float *depth_out,
+                        float *normal_out, int64_t n, void *stream);
+
+/* End-to-end with HOST buffers: copies cam batch in, renders each view with
+ * ges_render on device-resident scene, copies each view's image (H,W,3 f32)
+ * to host_images (pinned recommended).  Used by the e2e benchmark leg. */
+int ges_render_views_host(const ges_scene_t *scene, const ges_camera_t *host_cams,
+                          int32_t n_views, const ges_settings_t *st, float *host_images,
+                          void *workspace, size_t ws_bytes, int64_t surfel_pair_cap,
+                          int64_t gaussian_pair_cap, void *image_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GES_B200_H */

@@ -1,0 +1,265 @@
+// C-ABI entry points (include/ges_b200.h): argument validation, scene-blob and
+// frame-workspace layout, and the per-frame launch sequence
+//   memset -> K1 surfel prep(+count) -> K4 Gaussian prep(+count) -> scan -> fill -> fused tile kernel
+// Every call is stream-ordered and capturable in a CUDA graph (no host sync).
+#include <stdio.h>
+
+#include <string>
+
+#include "ges_launch.h"
+
+using namespace ges;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return GES_ECUDA;
+}
+
+inline size_t al(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct Carve {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t n) {
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += al(n * sizeof(T));
+        return p;
+    }
+};
+
+int check_settings(const ges_settings_t* st) {
+    if (!st) return fail(GES_EINVAL, "settings is NULL");
+    if (st->supersample != 1 && st->supersample != 4) return fail(GES_EINVAL, "supersample must be 1 or 4");
+    if (st->layers < 0 || st->layers > 2) return fail(GES_EINVAL, "unknown layer mode");
+    if (st->epsilon_mode != 0 && st->epsilon_mode != 1) return fail(GES_EINVAL, "unknown epsilon mode");
+    return GES_OK;
+}
+
+int check_scene(const ges_scene_t* sc) {
+    if (!sc) return fail(GES_EINVAL, "scene is NULL");
+    if (sc->sh_degree < 0 || sc->sh_degree > 3) return fail(GES_EDEGREE, "SH degree must be in [0, 3]");
+    if (sc->gaussian_dim != 2 && sc->gaussian_dim != 3) return fail(GES_EINVAL, "gaussian_dim must be 2 or 3");
+    if (sc->n_surfels < 0 || sc->n_gaussians < 0) return fail(GES_EINVAL, "negative primitive count");
+    if (sc->n_surfels >= (1ll << 31) || sc->n_gaussians >= (1ll << 31))
+        return fail(GES_EINVAL, "primitive count exceeds 2^31");
+    return GES_OK;
+}
+
+int check_cam(const ges_camera_t* c) {
+    if (!c) return fail(GES_EINVAL, "camera is NULL");
+    if (!(c->fx > 0) || !(c->fy > 0)) return fail(GES_EINVAL, "focal lengths must be positive");
+    if (c->width <= 0 || c->height <= 0 || c->width > 32767 || c->height > 32767)
+        return fail(GES_EINVAL, "image size out of range");
+    return GES_OK;
+}
+
+// Frame workspace layout; base == nullptr only measures.
+struct Frame {
+    SurfRec* srec;
+    float4 *s_rgb, *s_nrm;
+    void* grec;
+    float4* g_nrm;
+    uint32_t *cnt_s, *off_s, *cur_s, *cnt_g, *off_g, *cur_g;
+    uint32_t *list_s, *list_g;
+    ges_frame_status_t* status;
+    size_t bytes;
+    int ntx, nty, ntiles;
+};
+
+Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, int64_t cap_s, int64_t cap_g) {
+    Frame f{};
+    Carve c{static_cast<char*>(base)};
+    f.ntx = (cam->width + TILE - 1) / TILE;
+    f.nty = (cam->height + TILE - 1) / TILE;
+    f.ntiles = f.ntx * f.nty;
+    size_t ns = (size_t)sc->n_surfels, ng = (size_t)sc->n_gaussians;
+    f.status = c.take<ges_frame_status_t>(1);
+    f.cnt_s = c.take<uint32_t>(2 * (size_t)(f.ntiles + 1));   // counts for both passes: one memset
+    f.cnt_g = f.cnt_s ? f.cnt_s + (f.ntiles + 1) : nullptr;
+    f.off_s = c.take<uint32_t>(f.ntiles + 1);
+    f.cur_s = c.take<uint32_t>(f.ntiles + 1);
+    f.off_g = c.take<uint32_t>(f.ntiles + 1);
+    f.cur_g = c.take<uint32_t>(f.ntiles + 1);
+    f.srec = c.take<SurfRec>(ns);
+    f.s_rgb = c.take<float4>(ns);
+    f.s_nrm = c.take<float4>(ns);
+    f.grec = c.take<char>(ng * (sc->gaussian_dim == 2 ? sizeof(Gauss2Rec) : sizeof(GaussRec)));
+    f.g_nrm = c.take<float4>(ng);
+    f.list_s = c.take<uint32_t>((size_t)cap_s);
+    f.list_g = c.take<uint32_t>((size_t)cap_g);
+    f.bytes = c.off;
+    return f;
+}
+
+// mode: 1 surfel pass, 2 Gaussian pass against ds_in, 3 both.
+int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st, const ges_outputs_t* out,
+              const float* ds_in, int mode, void* ws, size_t ws_bytes, int64_t cap_s, int64_t cap_g,
+              ges_frame_status_t* status_dev, cudaStream_t s) {
+    int rc;
+    if ((rc = check_scene(sc)) || (rc = check_cam(cam)) || (rc = check_settings(st))) return rc;
+    if (!out) return fail(GES_EINVAL, "outputs is NULL");
+    if (cap_s < 0 || cap_g < 0 || cap_s >= (1ll << 32) || cap_g >= (1ll << 32))
+        return fail(GES_EINVAL, "pair capacity out of range");
+    Frame f = layout(ws, sc, cam, cap_s, cap_g);
+    if (!ws || ws_bytes < f.bytes) return fail(GES_EWORKSPACE, "workspace too small (see ges_workspace_bytes)");
+    ges_frame_status_t* status = status_dev ? status_dev : f.status;
+    const int grid = st->supersample == 4 ? 2 : 1;
+    const bool do_s = mode & 1;
+    const bool do_g = (mode & 2) && st->layers != GES_LAYERS_SURFELS_ONLY;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(f.cnt_s, 0, 2 * sizeof(uint32_t) * (f.ntiles + 1), s)) != cudaSuccess)
+        return cuda_fail(e, "memset counts");
+    if ((e = cudaMemsetAsync(status, 0, sizeof(ges_frame_status_t), s)) != cudaSuccess)
+        return cuda_fail(e, "memset status");
+    CamK cs = make_cam(*cam, grid), cg = make_cam(*cam, 1);
+    Grid gs{cs.W, cs.H, TILE * grid, f.ntx, f.nty}, gg{cg.W, cg.H, TILE, f.ntx, f.nty};
+    ges_scene_t scs = *sc;
+    if (!do_s) scs.n_surfels = 0;
+    if (!do_g) scs.n_gaussians = 0;
+    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, f.s_rgb, f.s_nrm, f.cnt_s}, s)))
+        return cuda_fail(e, "surfel preprocess");
+    if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))
+        return cuda_fail(e, "gaussian preprocess");
+    if ((e = launch_scan(f.cnt_s, f.off_s, f.cur_s, f.ntiles, f.cnt_g, f.off_g, f.cur_g, f.ntiles, cap_s, cap_g,
+                         status, s)))
+        return cuda_fail(e, "tile scan");
+    if ((e = launch_fill(f.srec, scs.n_surfels, f.cur_s, f.list_s, cap_s, TILE * grid, f.ntx, f.grec,
+                         scs.n_gaussians, sc->gaussian_dim, f.cur_g, f.list_g, cap_g, f.ntx, s)))
+        return cuda_fail(e, "tile fill");
+    TileArgs a{};
+    a.W = cam->width; a.H = cam->height; a.ntx = f.ntx; a.nty = f.nty;
+    a.layers = st->layers;
+    for (int i = 0; i < 3; ++i) a.bg[i] = st->background[i];
+    a.rfx = cs.fx; a.rfy = cs.fy; a.rcx = cs.cx; a.rcy = cs.cy;
+    a.srec = f.srec; a.s_rgb = f.s_rgb; a.s_nrm = f.s_nrm; a.s_list = f.list_s; a.s_off = f.off_s;
+    a.gfx = cg.fx; a.gfy = cg.fy; a.gcx = cg.cx; a.gcy = cg.cy;
+    a.grec = f.grec; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.g_off = f.off_g;
+    a.ds_in = ds_in;
+    a.out = *out;
+    a.status = status;
+    int tmode = (do_s ? 1 : 0) | (do_g ? 2 : 0);
+    if (tmode == 0) tmode = 1;   // surfels_only + pass-2-only entry never happens; keep a valid mode
+    if (mode == 2 && !do_g) {
+        // accumulate_gaussians with layers=surfels_only still accumulates (forward.py:218-245
+        // ignores layers); force the Gaussian pass.
+        tmode = 2;
+    }
+    if ((e = launch_tile(a, st->supersample, tmode, sc->gaussian_dim, st->with_geometry != 0, s)))
+        return cuda_fail(e, "tile kernel");
+    return GES_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ges_abi_version(void) { return GES_ABI_VERSION; }
+
+const char* ges_last_error(void) { return g_err.c_str(); }
+
+size_t ges_scene_bytes(int64_t ns, int64_t ng, int32_t deg) {
+    if (deg < 0 || deg > 3 || ns < 0 || ng < 0) return 0;
+    size_t K = (size_t)(deg + 1) * (deg + 1);
+    return al(ns * 16) + al(ns * 16) + al(ns * 4) + al(ns * K * 12) + al(ng * 16) * 3 + al(ng * K * 12);
+}
+
+int ges_scene_pack(const ges_scene_src_t* src, void* blob, size_t blob_bytes, ges_scene_t* out, void* stream) {
+    if (!src || !out) return fail(GES_EINVAL, "NULL argument");
+    if (src->sh_degree < 0 || src->sh_degree > 3) return fail(GES_EDEGREE, "SH degree must be in [0, 3]");
+    if (src->gaussian_dim != 2 && src->gaussian_dim != 3) return fail(GES_EINVAL, "gaussian_dim must be 2 or 3");
+    if (src->n_surfels < 0 || src->n_gaussians < 0) return fail(GES_EINVAL, "negative primitive count");
+    size_t need = ges_scene_bytes(src->n_surfels, src->n_gaussians, src->sh_degree);
+    if (blob_bytes < need || (need && !blob)) return fail(GES_EWORKSPACE, "scene blob too small");
+    size_t ns = src->n_surfels, ng = src->n_gaussians, K = (size_t)(src->sh_degree + 1) * (src->sh_degree + 1);
+    Carve c{static_cast<char*>(blob)};
+    ges_scene_t sc{};
+    sc.n_surfels = src->n_surfels; sc.n_gaussians = src->n_gaussians;
+    sc.sh_degree = src->sh_degree; sc.gaussian_dim = src->gaussian_dim;
+    sc.s_pos_s1 = c.take<float>(ns * 4);
+    sc.s_quat = c.take<float>(ns * 4);
+    sc.s_s2 = c.take<float>(ns);
+    sc.s_sh = c.take<float>(ns * K * 3);
+    sc.g_pos_op = c.take<float>(ng * 4);
+    sc.g_quat = c.take<float>(ng * 4);
+    sc.g_scale_eps = c.take<float>(ng * 4);
+    sc.g_sh = c.take<float>(ng * K * 3);
+    cudaError_t e = launch_pack(*src, sc, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "scene pack");
+    *out = sc;
+    return GES_OK;
+}
+
+size_t ges_workspace_bytes(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st,
+                           int64_t cap_s, int64_t cap_g) {
+    if (check_scene(sc) || check_cam(cam) || check_settings(st) || cap_s < 0 || cap_g < 0) return 0;
+    return layout(nullptr, sc, cam, cap_s, cap_g).bytes;
+}
+
+int ges_render(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st, const ges_outputs_t* out,
+               void* ws, size_t ws_bytes, int64_t cap_s, int64_t cap_g, ges_frame_status_t* status_dev,
+               void* stream) {
+    return run_frame(sc, cam, st, out, nullptr, 3, ws, ws_bytes, cap_s, cap_g, status_dev, (cudaStream_t)stream);
+}
+
+int ges_rasterize_surfels(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st,
+                          const ges_outputs_t* out, void* ws, size_t ws_bytes, int64_t cap_s,
+                          ges_frame_status_t* status_dev, void* stream) {
+    return run_frame(sc, cam, st, out, nullptr, 1, ws, ws_bytes, cap_s, 0, status_dev, (cudaStream_t)stream);
+}
+
+int ges_accumulate_gaussians(const ges_scene_t* sc, const ges_camera_t* cam, const float* surfel_depth,
+                             const ges_settings_t* st, const ges_outputs_t* out, void* ws, size_t ws_bytes,
+                             int64_t cap_g, ges_frame_status_t* status_dev, void* stream) {
+    if (!surfel_depth) return fail(GES_EINVAL, "surfel_depth is NULL");
+    ges_settings_t s2 = st ? *st : ges_settings_t{};
+    s2.supersample = 1;   // the Gaussian pass always runs at base resolution (forward.py:411)
+    if (st && s2.layers == GES_LAYERS_SURFELS_ONLY) s2.layers = GES_LAYERS_FULL;
+    return run_frame(sc, cam, st ? &s2 : nullptr, out, surfel_depth, 2, ws, ws_bytes, 0, cap_g, status_dev,
+                     (cudaStream_t)stream);
+}
+
+int ges_composite(const float* sc, const float* gc, const float* gw, float sw, float* img, int64_t n, void* stream) {
+    if (n < 0 || (n && (!sc || !gc || !gw || !img))) return fail(GES_EINVAL, "bad composite arguments");
+    cudaError_t e = launch_composite(sc, gc, gw, sw, img, n, (cudaStream_t)stream);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "composite");
+}
+
+int ges_smooth_geometry(const float* sd, const float* sn, const float* gd, const float* gn, const float* gw,
+                        float* d_out, float* n_out, int64_t n, void* stream) {
+    if (n < 0 || (n && (!sd || !sn || !gd || !gn || !gw || !d_out || !n_out)))
+        return fail(GES_EINVAL, "bad smooth_geometry arguments");
+    cudaError_t e = launch_smooth(sd, sn, gd, gn, gw, d_out, n_out, n, (cudaStream_t)stream);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "smooth_geometry");
+}
+
+int ges_render_views_host(const ges_scene_t* sc, const ges_camera_t* host_cams, int32_t n_views,
+                          const ges_settings_t* st, float* host_images, void* ws, size_t ws_bytes, int64_t cap_s,
+                          int64_t cap_g, void* image_dev, void* stream) {
+    if (!host_cams || !host_images || !image_dev || n_views < 0) return fail(GES_EINVAL, "bad view batch arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t off = 0;
+    for (int v = 0; v < n_views; ++v) {
+        ges_outputs_t out{};
+        out.image = static_cast<float*>(image_dev);
+        int rc = ges_render(sc, &host_cams[v], st, &out, ws, ws_bytes, cap_s, cap_g, nullptr, stream);
+        if (rc) return rc;
+        size_t bytes = (size_t)host_cams[v].width * host_cams[v].height * 3 * sizeof(float);
+        cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(host_images) + off, image_dev, bytes,
+                                        cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_fail(e, "image copy");
+        off += bytes;
+    }
+    return GES_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Shared device definitions for the GES sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ges_b200.h"
+
+namespace ges {
+
+constexpr int TILE = 16;                 // base-resolution tile (forward.py:27)
+constexpr int TILE_PX = TILE * TILE;     // one thread per base pixel
+constexpr int NWARP = TILE_PX / 32;      // 8 warps, each an 8x4 pixel patch
+constexpr double R_OPAQUE = 3.3290429691304455;   // sqrt(2 ln 255), filters.py:28-30
+constexpr float R2_F = 11.082527f;                // fp32 R^2 (NEP-50 weak scalar)
+constexpr double NEAR = 0.01;                     // cameras.py:14
+constexpr float NEAR_F = 0.01f;
+constexpr float PARALLEL_EPS_F = 1e-8f;           // geometry.py:15
+constexpr double SCREEN_VAR = 0.3;                // filters.py:21
+constexpr float ALPHA_CUTOFF_F = 1.0f / 255.0f;   // forward.py:26
+
+// Camera in the form the kernels use (double for per-primitive math).
+struct CamK {
+    double fx, fy, cx, cy;
+    double R[9];
+    double t[3];
+    double pos[3];      // world-space camera centre -R^T t (cameras.py:38)
+    int W, H;           // resolution of THIS pass (hi-res for ss=4 surfels)
+};
+
+// Per-surfel screen record written by the surfel preprocess (64 B).
+//   r0 = (D0, Dx, Dy, nq)   den(x,y) = n.d = D0 + Dx*(x-xr) + Dy*(y-yr)
+//   r1 = (U0, Ux, Uy, xr)   U = ((n.q) a1 - (a1.q) n).d / s1, u = U/den
+//   r2 = (V0, Vx, Vy, yr)   V likewise with a2, s2
+//   r3 = (zmin, rect_x, rect_y, 0)  rect packed lo | hi << 16 (pixel ranges)
+struct __align__(16) SurfRec {
+    float4 r0, r1, r2, r3;
+};
+
+// Per-Gaussian screen record (3D EWA), 64 B.
+//   r0 = (mx_int, mx_frac, my_int, my_frac)       mean2d split for precision
+//   r1 = (pa, pb, pc, sigma)  power = pa dx^2 + pb dx dy + pc dy^2
+//   r2 = (depth, eps, pmin, rect_x)  pmin: power below which alpha < 1/255
+//   r3 = (rect_y, r, g, b)
+struct __align__(16) GaussRec {
+    float4 r0, r1, r2, r3;
+};
+
+// Per-2D-Gaussian record, 80 B: ray-plane homography like SurfRec plus
+//   r3 = (sigma, eps, rect_x, rect_y), r4 = (r, g, b, zmin)
+struct __align__(16) Gauss2Rec {
+    float4 r0, r1, r2, r3, r4;
+};
+
+__device__ __forceinline__ uint32_t pack_span(int lo, int hi) {
+    return (uint32_t)lo | ((uint32_t)hi << 16);
+}
+__device__ __forceinline__ int span_lo(uint32_t s) { return (int)(s & 0xffffu); }
+__device__ __forceinline__ int span_hi(uint32_t s) { return (int)(s >> 16); }
+
+}  // namespace ges

@@ -1,0 +1,392 @@
+// K0 scene pack, K1 surfel preprocess, K4 Gaussian preprocess (3D EWA and
+// planar 2D).  One thread per primitive; per-primitive geometry in float64
+// (as the reference does before casting to dtype, forward.py:148-163), the
+// per-pixel coefficients it emits in float32.  Each kernel also counts its
+// primitive into the tiles its pixel range overlaps (count pass of the
+// sort-free count -> prefix-sum -> fill binning).
+#include <math.h>
+
+#include "ges_launch.h"
+#include "ges_sh.cuh"
+
+namespace ges {
+
+CamK make_cam(const ges_camera_t& c, int scale) {
+    CamK k{};
+    k.fx = c.fx * scale; k.fy = c.fy * scale; k.cx = c.cx * scale; k.cy = c.cy * scale;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) k.R[3 * i + j] = c.w2c[4 * i + j];
+        k.t[i] = c.w2c[4 * i + 3];
+    }
+    for (int j = 0; j < 3; ++j)   // -R^T t
+        k.pos[j] = -(k.R[j] * k.t[0] + k.R[3 + j] * k.t[1] + k.R[6 + j] * k.t[2]);
+    k.W = c.width * scale; k.H = c.height * scale;
+    return k;
+}
+
+// ---------------------------------------------------------------- helpers
+struct d3 { double x, y, z; };
+__device__ __forceinline__ d3 mk(double x, double y, double z) { return {x, y, z}; }
+__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ d3 scl(d3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ d3 sub(d3 a, d3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ d3 rot(const CamK& c, d3 v) {   // W v
+    return {c.R[0] * v.x + c.R[1] * v.y + c.R[2] * v.z, c.R[3] * v.x + c.R[4] * v.y + c.R[5] * v.z,
+            c.R[6] * v.x + c.R[7] * v.y + c.R[8] * v.z};
+}
+
+// Columns of the rotation of quaternion (w,x,y,z), renormalised (geometry.py:18-36).
+__device__ __forceinline__ void quat_cols(float4 qf, d3& c0, d3& c1, d3& c2) {
+    double w = qf.x, x = qf.y, y = qf.z, z = qf.w;
+    double inv = 1.0 / sqrt(w * w + x * x + y * y + z * z);
+    w *= inv; x *= inv; y *= inv; z *= inv;
+    c0 = mk(1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y));
+    c1 = mk(2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x));
+    c2 = mk(2 * (x * z + w * y), 2 * (y * z - w * x), 1 - 2 * (x * x + y * y));
+}
+
+// Exact screen AABB of the projected disc {a m1 + b m2 : a^2+b^2<=1}
+// (geometry.py:273-302) -> inclusive pixel ranges with 0.5 px padding
+// (forward.py:85-96).  Returns false if the range is empty.
+__device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1, int& y0, int& y1) {
+    double B0 = m1.z, B1 = m2.z, B2 = q.z;
+    double c2 = B2 * B2 - (B0 * B0 + B1 * B1);
+    bool whole = c2 <= 0.0;
+    double c2s = whole ? 1.0 : c2;
+    double lo[2], hi[2];
+    for (int ax = 0; ax < 2; ++ax) {
+        double f = ax ? c.fy : c.fx, cc = ax ? c.cy : c.cx;
+        double m1a = ax ? m1.y : m1.x, m2a = ax ? m2.y : m2.x, qa = ax ? q.y : q.x;
+        double A0 = f * m1a + cc * m1.z, A1 = f * m2a + cc * m2.z, A2 = f * qa + cc * q.z;
+        double c1 = -2.0 * (A2 * B2 - (A0 * B0 + A1 * B1));
+        double c0 = A2 * A2 - (A0 * A0 + A1 * A1);
+        double root = sqrt(fmax(c1 * c1 - 4.0 * c2s * c0, 0.0));
+        lo[ax] = (-c1 - root) / (2.0 * c2s);
+        hi[ax] = (-c1 + root) / (2.0 * c2s);
+    }
+    auto clampi = [](double v, int n) -> int {
+        if (!(v >= 0.0)) return 0;          // also NaN -> 0 like np.clip of NaN cast (never alive)
+        if (v > n - 1.0) return n - 1;
+        return (int)v;
+    };
+    if (whole) {
+        x0 = 0; x1 = c.W - 1; y0 = 0; y1 = c.H - 1;
+    } else {
+        x0 = clampi(ceil(lo[0] - 0.5 - 0.5), c.W);
+        x1 = clampi(floor(hi[0] + 0.5 - 0.5), c.W);
+        y0 = clampi(ceil(lo[1] - 0.5 - 0.5), c.H);
+        y1 = clampi(floor(hi[1] + 0.5 - 0.5), c.H);
+    }
+    return x1 >= x0 && y1 >= y0;
+}
+
+__device__ __forceinline__ void count_tiles(uint32_t* cnt, const Grid& g, int x0, int x1, int y0, int y1) {
+    int tx0 = x0 / g.tile_px, tx1 = x1 / g.tile_px, ty0 = y0 / g.tile_px, ty1 = y1 / g.tile_px;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(cnt + ty * g.ntx + tx, 1u);
+}
+
+// Ray-plane homography of a planar primitive relative to pixel (xr, yr):
+// n.d, U and V as affine functions of the pixel offset (see SurfRec).
+__device__ __forceinline__ float4 affine_of(d3 v, const CamK& c, int xr, int yr, float last) {
+    double cx = v.x / c.fx, cy = v.y / c.fy;
+    double c0 = cx * (xr + 0.5 - c.cx) + cy * (yr + 0.5 - c.cy) + v.z;
+    return make_float4((float)c0, (float)cx, (float)cy, last);
+}
+
+__device__ __forceinline__ void planar_coeffs(d3 q, d3 a1, d3 a2, d3 n, double s1, double s2,
+                                              const CamK& c, int x0, int x1, int y0, int y1,
+                                              float4& r0, float4& r1, float4& r2) {
+    double nq = dot(n, q);
+    d3 cu = scl(sub(scl(a1, nq), scl(n, dot(a1, q))), 1.0 / s1);
+    d3 cv = scl(sub(scl(a2, nq), scl(n, dot(a2, q))), 1.0 / s2);
+    int xr = x0, yr = y0;
+    if (q.z > 0.0) {
+        double mx = c.fx * q.x / q.z + c.cx, my = c.fy * q.y / q.z + c.cy;
+        xr = (int)fmin(fmax(floor(mx), (double)x0), (double)x1);
+        yr = (int)fmin(fmax(floor(my), (double)y0), (double)y1);
+    }
+    r0 = affine_of(n, c, xr, yr, (float)nq);
+    r1 = affine_of(cu, c, xr, yr, (float)xr);
+    r2 = affine_of(cv, c, xr, yr, (float)yr);
+}
+
+// ---------------------------------------------------------------- K0 pack
+__global__ void k_pack_prims(ges_scene_src_t src, ges_scene_t dst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < src.n_surfels) {
+        const double* p = src.s_pos + 3 * i;
+        const double* q = src.s_quat + 4 * i;
+        const double* l = src.s_log_scale + 2 * i;
+        double nrm = 1.0 / sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+        reinterpret_cast<float4*>(dst.s_pos_s1)[i] = make_float4(p[0], p[1], p[2], exp(l[0]));
+        reinterpret_cast<float4*>(dst.s_quat)[i] =
+            make_float4(q[0] * nrm, q[1] * nrm, q[2] * nrm, q[3] * nrm);
+        dst.s_s2[i] = (float)exp(l[1]);
+    }
+    if (i < src.n_gaussians) {
+        // primitives.py:113-131: eff_scale = sqrt(s^2 + f3), eff_opacity =
+        // sigma * prod(s / eff_s), epsilon = (5/D) sum eff_s.
+        int D = src.gaussian_dim;
+        const double* p = src.g_pos + 3 * i;
+        const double* q = src.g_quat + 4 * i;
+        const double* l = src.g_log_scale + D * i;
+        double f3 = src.g_filter3d ? src.g_filter3d[i] : 0.0;
+        double sig = 1.0 / (1.0 + exp(-src.g_raw_opacity[i]));
+        double es[3] = {0.0, 0.0, 0.0}, esum = 0.0;
+        for (int k = 0; k < D; ++k) {
+            double s = exp(l[k]);
+            es[k] = sqrt(s * s + f3);
+            sig *= s / es[k];
+            esum += es[k];
+        }
+        double nrm = 1.0 / sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+        reinterpret_cast<float4*>(dst.g_pos_op)[i] = make_float4(p[0], p[1], p[2], sig);
+        reinterpret_cast<float4*>(dst.g_quat)[i] =
+            make_float4(q[0] * nrm, q[1] * nrm, q[2] * nrm, q[3] * nrm);
+        reinterpret_cast<float4*>(dst.g_scale_eps)[i] =
+            make_float4(es[0], es[1], es[2], (5.0 / D) * esum);
+    }
+}
+
+__global__ void k_pack_sh(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (float)a[i];
+}
+
+cudaError_t launch_pack(const ges_scene_src_t& src, const ges_scene_t& dst, cudaStream_t s) {
+    int64_t n = src.n_surfels > src.n_gaussians ? src.n_surfels : src.n_gaussians;
+    if (n > 0) k_pack_prims<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, dst);
+    int K = (src.sh_degree + 1) * (src.sh_degree + 1);
+    if (src.n_surfels) k_pack_sh<<<1184, 256, 0, s>>>(src.s_sh, dst.s_sh, src.n_surfels * K * 3);
+    if (src.n_gaussians) k_pack_sh<<<1184, 256, 0, s>>>(src.g_sh, dst.g_sh, src.n_gaussians * K * 3);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K1 surfels
+// forward.py:148-158 (frames, colour, n_vis, cull, bounds, ranges) for one surfel.
+template <int DEG>
+__global__ void __launch_bounds__(256) k_surfel_prep(ges_scene_t sc, CamK cam, Grid g, PrepOut o) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= sc.n_surfels) return;
+    float4 ps = __ldg(reinterpret_cast<const float4*>(sc.s_pos_s1) + i);
+    float4 qf = __ldg(reinterpret_cast<const float4*>(sc.s_quat) + i);
+    double s1 = ps.w, s2 = __ldg(sc.s_s2 + i);
+    d3 r0, r1, r2;
+    quat_cols(qf, r0, r1, r2);
+    d3 p = mk(ps.x, ps.y, ps.z);
+    d3 q = rot(cam, p);
+    q.x += cam.t[0]; q.y += cam.t[1]; q.z += cam.t[2];
+    d3 a1 = rot(cam, r0), a2 = rot(cam, r1), n = rot(cam, r2);
+    SurfRec rec;
+    int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+    bool alive = q.z > NEAR;
+    if (alive) alive = disc_ranges(q, scl(a1, s1 * R_OPAQUE), scl(a2, s2 * R_OPAQUE), cam, x0, x1, y0, y1);
+    if (alive) {
+        planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
+        double zmin = q.z - R_OPAQUE * sqrt(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z);
+        rec.r3 = make_float4((float)zmin, __uint_as_float(pack_span(x0, x1)),
+                             __uint_as_float(pack_span(y0, y1)), 0.f);
+        count_tiles(o.tile_count, g, x0, x1, y0, y1);
+        // view colour: SH at the centre-to-camera direction (forward.py:99-103)
+        d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
+        double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
+        float3 col = sh_color<DEG>(sc.s_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
+                                   (float)(dv.y * inv), (float)(dv.z * inv));
+        o.rgb[i] = make_float4(col.x, col.y, col.z, 0.f);
+        double sgn = dot(n, q) < 0.0 ? 1.0 : -1.0;   // forward.py:152
+        o.nrm[i] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);
+    } else {
+        rec.r0 = rec.r1 = rec.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        rec.r3 = make_float4(0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)), 0.f);
+    }
+    reinterpret_cast<SurfRec*>(o.rec)[i] = rec;
+}
+
+cudaError_t launch_surfel_prep(const ges_scene_t& sc, const CamK& cam, const Grid& g, const PrepOut& o,
+                               cudaStream_t s) {
+    if (sc.n_surfels == 0) return cudaSuccess;
+    unsigned nb = (unsigned)((sc.n_surfels + 255) / 256);
+    switch (sc.sh_degree) {
+        case 0: k_surfel_prep<0><<<nb, 256, 0, s>>>(sc, cam, g, o); break;
+        case 1: k_surfel_prep<1><<<nb, 256, 0, s>>>(sc, cam, g, o); break;
+        case 2: k_surfel_prep<2><<<nb, 256, 0, s>>>(sc, cam, g, o); break;
+        default: k_surfel_prep<3><<<nb, 256, 0, s>>>(sc, cam, g, o); break;
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K4 Gaussians
+struct GaussCfg {
+    int mip, eps_const, geom;
+    float eps_value;
+};
+
+// 3D EWA: geometry.py:114-132 + forward.py:252-290.
+template <int DEG>
+__global__ void __launch_bounds__(256) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+                                                     PrepOut o) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= sc.n_gaussians) return;
+    float4 po = __ldg(reinterpret_cast<const float4*>(sc.g_pos_op) + i);
+    float4 qf = __ldg(reinterpret_cast<const float4*>(sc.g_quat) + i);
+    float4 se = __ldg(reinterpret_cast<const float4*>(sc.g_scale_eps) + i);
+    d3 p = mk(po.x, po.y, po.z);
+    d3 t = rot(cam, p);
+    t.x += cam.t[0]; t.y += cam.t[1]; t.z += cam.t[2];
+    bool valid = t.z > NEAR;
+    d3 ts = valid ? t : mk(0.0, 0.0, 1.0);
+    d3 r0, r1, r2;
+    quat_cols(qf, r0, r1, r2);
+    // camera-space axes scaled: M = sum_k s_k^2 (W r_k)(W r_k)^T
+    d3 w0 = scl(rot(cam, r0), se.x), w1 = scl(rot(cam, r1), se.y), w2 = scl(rot(cam, r2), se.z);
+    double iz = 1.0 / ts.z;
+    // J rows: j0 = (fx/z, 0, -fx x/z^2), j1 = (0, fy/z, -fy y/z^2); cov = sum_k (J w_k)(J w_k)^T
+    double jx[3], jy[3];
+    const d3 ws[3] = {w0, w1, w2};
+    for (int k = 0; k < 3; ++k) {
+        jx[k] = cam.fx * iz * ws[k].x - cam.fx * ts.x * iz * iz * ws[k].z;
+        jy[k] = cam.fy * iz * ws[k].y - cam.fy * ts.y * iz * iz * ws[k].z;
+    }
+    double cv00 = jx[0] * jx[0] + jx[1] * jx[1] + jx[2] * jx[2];
+    double cv11 = jy[0] * jy[0] + jy[1] * jy[1] + jy[2] * jy[2];
+    double cv01 = jx[0] * jy[0] + jx[1] * jy[1] + jx[2] * jy[2];
+    double raw_det = cv00 * cv11 - cv01 * cv01;
+    double c00 = cv00 + SCREEN_VAR, c11 = cv11 + SCREEN_VAR, c01 = cv01;
+    double det = c00 * c11 - c01 * c01;
+    double sig = po.w;
+    if (cfg.mip) sig *= sqrt(fmax(raw_det, 0.0) / det);
+    valid = valid && det > 0.0;
+    double la = c11 / det, lb = -c01 / det, lc = c00 / det;
+    double m2max = 2.0 * log(fmax(255.0 * sig, 1e-12));
+    valid = valid && m2max > 0.0;
+    double rx = sqrt(fmax(m2max * c00, 0.0)), ry = sqrt(fmax(m2max * c11, 0.0));
+    double mx = cam.fx * ts.x / ts.z + cam.cx, my = cam.fy * ts.y / ts.z + cam.cy;
+    GaussRec rec;
+    int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+    if (valid) {
+        auto clampi = [](double v, int n) -> int {
+            if (!(v >= 0.0)) return 0;
+            if (v > n - 1.0) return n - 1;
+            return (int)v;
+        };
+        x0 = clampi(ceil(mx - rx - 0.5 - 0.5), cam.W);
+        x1 = clampi(floor(mx + rx + 0.5 - 0.5), cam.W);
+        y0 = clampi(ceil(my - ry - 0.5 - 0.5), cam.H);
+        y1 = clampi(floor(my + ry + 0.5 - 0.5), cam.H);
+        valid = x1 >= x0 && y1 >= y0;
+    }
+    if (valid) {
+        double mxi = floor(mx), myi = floor(my);
+        rec.r0 = make_float4((float)mxi, (float)(mx - mxi), (float)myi, (float)(my - myi));
+        rec.r1 = make_float4((float)(-0.5 * la), (float)(-lb), (float)(-0.5 * lc), (float)sig);
+        float eps = cfg.eps_const ? cfg.eps_value : se.w;
+        rec.r2 = make_float4((float)t.z, eps, (float)(-0.5 * m2max) - 1e-4f,
+                             __uint_as_float(pack_span(x0, x1)));
+        d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
+        double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
+        float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
+                                   (float)(dv.y * inv), (float)(dv.z * inv));
+        rec.r3 = make_float4(__uint_as_float(pack_span(y0, y1)), col.x, col.y, col.z);
+        count_tiles(o.tile_count, g, x0, x1, y0, y1);
+        if (cfg.geom) {   // forward.py:277-284: shortest eff_scale axis, camera-facing
+            int k = 0;
+            double smin = se.x;
+            if (se.y < smin) { k = 1; smin = se.y; }
+            if (se.z < smin) { k = 2; }
+            d3 nv = rot(cam, k == 0 ? r0 : (k == 1 ? r1 : r2));
+            double sgn = dot(nv, t) < 0.0 ? 1.0 : -1.0;
+            o.nrm[i] = make_float4((float)(nv.x * sgn), (float)(nv.y * sgn), (float)(nv.z * sgn), 0.f);
+        }
+    } else {
+        rec.r0 = rec.r1 = make_float4(0.f, 0.f, 0.f, 0.f);
+        rec.r2 = make_float4(0.f, 0.f, 0.f, __uint_as_float(pack_span(1, 0)));
+        rec.r3 = make_float4(__uint_as_float(pack_span(1, 0)), 0.f, 0.f, 0.f);
+    }
+    reinterpret_cast<GaussRec*>(o.rec)[i] = rec;
+}
+
+// Planar 2D Gaussians: forward.py:324-351 (+ filters.py:84-109 when mip).
+template <int DEG>
+__global__ void __launch_bounds__(256) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+                                                     PrepOut o) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= sc.n_gaussians) return;
+    float4 po = __ldg(reinterpret_cast<const float4*>(sc.g_pos_op) + i);
+    float4 qf = __ldg(reinterpret_cast<const float4*>(sc.g_quat) + i);
+    float4 se = __ldg(reinterpret_cast<const float4*>(sc.g_scale_eps) + i);
+    d3 r0, r1, r2;
+    quat_cols(qf, r0, r1, r2);
+    d3 p = mk(po.x, po.y, po.z);
+    d3 q = rot(cam, p);
+    q.x += cam.t[0]; q.y += cam.t[1]; q.z += cam.t[2];
+    d3 a1 = rot(cam, r0), a2 = rot(cam, r1), n = rot(cam, r2);
+    double s1 = se.x, s2 = se.y, sig = po.w;
+    bool fvalid = true;
+    if (cfg.mip) {   // object_space_filter_2d with r = 0.3 (filters.py:84-109, geometry.py:305-319)
+        double z = q.z;
+        d3 m1 = scl(a1, s1), m2 = scl(a2, s2);
+        double J00 = cam.fx * (m1.x * z - q.x * m1.z) / (z * z);
+        double J01 = cam.fx * (m2.x * z - q.x * m2.z) / (z * z);
+        double J10 = cam.fy * (m1.y * z - q.y * m1.z) / (z * z);
+        double J11 = cam.fy * (m2.y * z - q.y * m2.z) / (z * z);
+        double det = J00 * J11 - J01 * J10;
+        fvalid = fabs(det) > 1e-12 && z > NEAR;
+        double dets = fvalid ? det : 1.0;
+        double i00 = J11 / dets, i01 = -J01 / dets, i10 = -J10 / dets, i11 = J00 / dets;
+        double sm0 = sqrt(1.0 + SCREEN_VAR * (i00 * i00 + i01 * i01));
+        double sm1 = sqrt(1.0 + SCREEN_VAR * (i10 * i10 + i11 * i11));
+        s1 *= sm0; s2 *= sm1;
+        sig *= 1.0 / (sm0 * sm1);
+    }
+    double m2max = 2.0 * log(fmax(255.0 * sig, 1e-12));
+    bool valid = fvalid && q.z > NEAR && m2max > 0.0;
+    double rmax = sqrt(fmax(m2max, 0.0));
+    int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+    if (valid) valid = disc_ranges(q, scl(a1, s1 * rmax), scl(a2, s2 * rmax), cam, x0, x1, y0, y1);
+    Gauss2Rec rec;
+    if (valid) {
+        planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
+        float eps = cfg.eps_const ? cfg.eps_value : se.w;
+        rec.r3 = make_float4((float)sig, eps, __uint_as_float(pack_span(x0, x1)),
+                             __uint_as_float(pack_span(y0, y1)));
+        d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
+        double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
+        float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
+                                   (float)(dv.y * inv), (float)(dv.z * inv));
+        rec.r4 = make_float4(col.x, col.y, col.z, (float)m2max * 1.0001f + 1e-4f);
+        count_tiles(o.tile_count, g, x0, x1, y0, y1);
+        if (cfg.geom) {
+            double sgn = dot(n, q) < 0.0 ? 1.0 : -1.0;   // forward.py:337
+            o.nrm[i] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);
+        }
+    } else {
+        rec.r0 = rec.r1 = rec.r2 = rec.r4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        rec.r3 = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
+    }
+    reinterpret_cast<Gauss2Rec*>(o.rec)[i] = rec;
+}
+
+cudaError_t launch_gauss_prep(const ges_scene_t& sc, const CamK& cam, const Grid& g,
+                              const ges_settings_t& st, const PrepOut& o, cudaStream_t s) {
+    if (sc.n_gaussians == 0) return cudaSuccess;
+    GaussCfg cfg{st.mip, st.epsilon_mode == 1, st.with_geometry, st.epsilon_value};
+    unsigned nb = (unsigned)((sc.n_gaussians + 255) / 256);
+#define GES_G(KER)                                                          \
+    switch (sc.sh_degree) {                                                 \
+        case 0: KER<0><<<nb, 256, 0, s>>>(sc, cam, g, cfg, o); break;      \
+        case 1: KER<1><<<nb, 256, 0, s>>>(sc, cam, g, cfg, o); break;      \
+        case 2: KER<2><<<nb, 256, 0, s>>>(sc, cam, g, cfg, o); break;      \
+        default: KER<3><<<nb, 256, 0, s>>>(sc, cam, g, cfg, o); break;     \
+    }
+    if (sc.gaussian_dim == 2) {
+        GES_G(k_gauss2_prep)
+    } else {
+        GES_G(k_gauss3_prep)
+    }
+#undef GES_G
+    return cudaGetLastError();
+}
+
+}  // namespace ges

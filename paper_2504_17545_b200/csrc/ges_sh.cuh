@@ -1,0 +1,69 @@
+// Real spherical harmonics to degree 3, graphics sign convention
+// (reference sh.py:13-64, :117-133): rgb = clamp(0.5 + sum_k Y_k(dir) c_k, 0, 1).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace ges {
+
+// sh: K x 3 floats, coefficient-major (DC first), for ONE primitive.
+template <int DEG>
+__device__ __forceinline__ float3 sh_color(const float* __restrict__ sh, float x, float y, float z) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    float c[K * 3];
+    if constexpr ((K * 3) % 4 == 0) {
+        const float4* s4 = reinterpret_cast<const float4*>(sh);
+#pragma unroll
+        for (int j = 0; j < K * 3 / 4; ++j) {
+            float4 v = __ldg(s4 + j);
+            c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < K * 3; ++j) c[j] = __ldg(sh + j);
+    }
+    float b[K];
+    b[0] = 0.28209479177387814f;
+    if constexpr (DEG >= 1) {
+        const float C1 = 0.4886025119029199f;
+        b[1] = -C1 * y; b[2] = C1 * z; b[3] = -C1 * x;
+    }
+    if constexpr (DEG >= 2) {
+        float xx = x * x, yy = y * y, zz = z * z;
+        b[4] = 1.0925484305920792f * x * y;
+        b[5] = -1.0925484305920792f * y * z;
+        b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+        b[7] = -1.0925484305920792f * x * z;
+        b[8] = 0.5462742152960396f * (xx - yy);
+        if constexpr (DEG >= 3) {
+            b[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+            b[10] = 2.890611442640554f * x * y * z;
+            b[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+            b[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            b[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+            b[14] = 1.445305721320277f * z * (xx - yy);
+            b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+        }
+    }
+    float r = 0.f, g = 0.f, bl = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        r = fmaf(b[k], c[3 * k], r);
+        g = fmaf(b[k], c[3 * k + 1], g);
+        bl = fmaf(b[k], c[3 * k + 2], bl);
+    }
+    return make_float3(fminf(fmaxf(0.5f + r, 0.f), 1.f), fminf(fmaxf(0.5f + g, 0.f), 1.f),
+                       fminf(fmaxf(0.5f + bl, 0.f), 1.f));
+}
+
+__device__ __forceinline__ float3 sh_color_dyn(int deg, const float* __restrict__ sh, float x, float y,
+                                               float z) {
+    switch (deg) {
+        case 0: return sh_color<0>(sh, x, y, z);
+        case 1: return sh_color<1>(sh, x, y, z);
+        case 2: return sh_color<2>(sh, x, y, z);
+        default: return sh_color<3>(sh, x, y, z);
+    }
+}
+
+}  // namespace ges

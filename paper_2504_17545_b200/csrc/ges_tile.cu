@@ -1,0 +1,410 @@
+// K3 + K6 fused: one CTA per 16x16 base-resolution tile, one thread per pixel.
+//
+// Pass 1 (forward.py:127-209): every thread keeps, per (sub)sample, the packed
+// key (float_bits(t) << 32 | surfel_id) of the nearest covering surfel in
+// registers; min over keys == argmin over hit depth with ties to the lowest
+// index, exactly np.argmin over the ascending candidate list (forward.py:187).
+// No atomics: the z-buffer is private per pixel.
+//
+// Pass 2 (forward.py:248-381): order-independent, depth-gated accumulation of
+// Gaussian alpha and alpha*colour in registers against the pass-1 depth that
+// never leaves the register file, fused with the composite write
+// (forward.py:384-417).
+//
+// Both passes stream the tile's primitive list through shared memory in
+// batches of 256 (one primitive per thread, transformed to tile-relative
+// coefficients once), then build per-warp work lists: a primitive is handed
+// to the warps whose 8x4 pixel patch its pixel range overlaps (and, for
+// Gaussians, whose nearest surfel depth can pass the gate), so warps only
+// test primitives that can touch them.
+#include <math.h>
+
+#include "ges_launch.h"
+
+namespace ges {
+
+constexpr int NB = TILE_PX;     // batch = one primitive per thread
+
+struct __align__(16) TileSmem {
+    float4 st[5][NB];           // staged per-primitive coefficients
+    uint8_t wl[NWARP][NB];      // per-warp work lists (batch indices)
+    int cnt[NWARP][NWARP];      // cnt[src warp][dst warp]
+    int pre[NWARP][NWARP];      // exclusive prefix over src warps
+    int tot[NWARP];
+    float wmax[NWARP];          // per-warp max surfel depth (Gaussian culling)
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Distribute the batch to per-warp lists (deterministic, batch order kept).
+__device__ __forceinline__ void build_lists(TileSmem& sm, uint32_t mask, int warp, int lane) {
+    uint32_t bal[NWARP];
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) bal[w] = __ballot_sync(0xffffffffu, (mask >> w) & 1u);
+    if (lane == 0) {
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) sm.cnt[warp][w] = __popc(bal[w]);
+    }
+    __syncthreads();
+    if (threadIdx.x < NWARP) {
+        int w = threadIdx.x, acc = 0;
+#pragma unroll
+        for (int s = 0; s < NWARP; ++s) {
+            sm.pre[s][w] = acc;
+            acc += sm.cnt[s][w];
+        }
+        sm.tot[w] = acc;
+    }
+    __syncthreads();
+    uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w)
+        if ((mask >> w) & 1u) sm.wl[w][sm.pre[warp][w] + __popc(bal[w] & lt)] = (uint8_t)threadIdx.x;
+    __syncthreads();
+}
+
+// Bitmask of warp patches (8x4 base px each, 2 columns x 4 rows) that the
+// local inclusive range [x0,x1]x[y0,y1] (in units of `ss` subpixels) overlaps.
+template <int SS>
+__device__ __forceinline__ uint32_t patch_mask(int x0, int x1, int y0, int y1) {
+    uint32_t mx = 0, my = 0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+        if (x0 <= SS * (c * 8 + 8) - 1 && x1 >= SS * c * 8) mx |= 1u << c;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (y0 <= SS * (r * 4 + 4) - 1 && y1 >= SS * r * 4) my |= 1u << r;
+    uint32_t m = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if ((my >> r) & 1u) m |= mx << (2 * r);
+    return m;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int SS, int MODE, int GK, bool GEOM>
+__global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
+    __shared__ TileSmem sm;
+    if (a.status->overflow) return;   // pair lists incomplete: host re-renders
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x;
+    const int tx = tile % a.ntx, ty = tile / a.ntx;
+    const int plx = (warp & 1) * 8 + (lane & 7), ply = (warp >> 1) * 4 + (lane >> 3);
+    const int x = tx * TILE + plx, y = ty * TILE + ply;
+    const bool inside = x < a.W && y < a.H;
+    const int64_t pix = (int64_t)y * a.W + x;
+
+    float ds = INFINITY;             // surfel depth of this pixel (sub-sample 0)
+    float3 cs = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+
+    // ------------------------------------------------------------ pass 1
+    if constexpr (MODE & 1) {
+        constexpr int NS = SS * SS;
+        unsigned long long best[NS];
+        float lxf[SS], lyf[SS], pe[NS];
+#pragma unroll
+        for (int s = 0; s < SS; ++s) {
+            lxf[s] = (float)(SS * plx + s);
+            lyf[s] = (float)(SS * ply + s);
+        }
+#pragma unroll
+        for (int sy = 0; sy < SS; ++sy)
+#pragma unroll
+            for (int sx = 0; sx < SS; ++sx) {
+                int X = SS * x + sx, Y = SS * y + sy;
+                float dxn = (float)((X + 0.5 - a.rcx) / a.rfx), dyn = (float)((Y + 0.5 - a.rcy) / a.rfy);
+                pe[sy * SS + sx] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
+                best[sy * SS + sx] = ~0ull;
+            }
+        const int ox = tx * TILE * SS, oy = ty * TILE * SS;
+        const uint32_t beg = a.s_off[tile], end = a.s_off[tile + 1];
+        for (uint32_t base = beg; base < end; base += NB) {
+            const int nb = min((uint32_t)NB, end - base);
+            uint32_t mask = 0;
+            if ((int)threadIdx.x < nb) {
+                const uint32_t id = a.s_list[base + threadIdx.x];
+                const SurfRec* r = a.srec + id;
+                float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3);
+                float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
+                float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
+                float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
+                float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
+                uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
+                mask = patch_mask<SS>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
+                                      span_hi(syr) - oy);
+                sm.st[0][threadIdx.x] = make_float4(d0, r0.y, r0.z, r0.w);
+                sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
+                sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, __uint_as_float(id), r3.x);
+            }
+            build_lists(sm, mask, warp, lane);
+            const int L = sm.tot[warp];
+            for (int k = 0; k < L; ++k) {
+                const int j = sm.wl[warp][k];
+                const float4 A = sm.st[0][j], B = sm.st[1][j], C = sm.st[2][j];
+                const unsigned long long idk = __float_as_uint(C.z);
+#pragma unroll
+                for (int sy = 0; sy < SS; ++sy)
+#pragma unroll
+                    for (int sx = 0; sx < SS; ++sx) {
+                        const float lx = lxf[sx], ly = lyf[sy];
+                        const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
+                        const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
+                        const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
+                        const float r2 = fmaf(U, U, V * V);
+                        if (r2 <= R2_F * den * den && fabsf(den) > pe[sy * SS + sx]) {
+                            const float t = __fdividef(A.w, den);
+                            if (t > NEAR_F) {
+                                unsigned long long key =
+                                    ((unsigned long long)__float_as_uint(t) << 32) | idk;
+                                best[sy * SS + sx] = key < best[sy * SS + sx] ? key : best[sy * SS + sx];
+                            }
+                        }
+                    }
+            }
+            __syncthreads();
+        }
+        // resolve: depth/normal/winner from sub-sample 0, colour = box mean
+        float3 acc = make_float3(0.f, 0.f, 0.f);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            float3 c = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+            if (best[s] != ~0ull) {
+                float4 v = __ldg(a.s_rgb + (uint32_t)best[s]);
+                c = make_float3(v.x, v.y, v.z);
+            }
+            acc.x += c.x; acc.y += c.y; acc.z += c.z;
+        }
+        if (NS > 1) {
+            acc.x /= (float)NS; acc.y /= (float)NS; acc.z /= (float)NS;
+        }
+        cs = acc;
+        const bool cov = best[0] != ~0ull;
+        ds = cov ? __uint_as_float((uint32_t)(best[0] >> 32)) : INFINITY;
+        if (inside) {
+            if (a.out.s_depth) a.out.s_depth[pix] = ds;
+            if (a.out.s_winner) a.out.s_winner[pix] = cov ? (int32_t)(uint32_t)best[0] : -1;
+            if (a.out.s_color) {
+                a.out.s_color[3 * pix] = cs.x; a.out.s_color[3 * pix + 1] = cs.y;
+                a.out.s_color[3 * pix + 2] = cs.z;
+            }
+            if (a.out.s_normal) {
+                float4 n = cov ? __ldg(a.s_nrm + (uint32_t)best[0]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                a.out.s_normal[3 * pix] = n.x; a.out.s_normal[3 * pix + 1] = n.y;
+                a.out.s_normal[3 * pix + 2] = n.z;
+            }
+        }
+    } else {
+        if (inside && a.ds_in) ds = a.ds_in[pix];
+    }
+
+    // ------------------------------------------------------------ pass 2
+    if constexpr (MODE & 2) {
+        float wsum = 0.f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
+        const float wm = warp_max(inside ? ds : -INFINITY);
+        if (lane == 0) sm.wmax[warp] = wm;
+        __syncthreads();
+        const float lx = (float)plx, ly = (float)ply;
+        float pe = 0.f;
+        if constexpr (GK == 2) {
+            float dxn = (float)((x + 0.5 - a.gcx) / a.gfx), dyn = (float)((y + 0.5 - a.gcy) / a.gfy);
+            pe = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
+        }
+        const int ox = tx * TILE, oy = ty * TILE;
+        const uint32_t beg = a.g_off[tile], end = a.g_off[tile + 1];
+        for (uint32_t base = beg; base < end; base += NB) {
+            const int nb = min((uint32_t)NB, end - base);
+            uint32_t mask = 0;
+            if ((int)threadIdx.x < nb) {
+                const uint32_t id = a.g_list[base + threadIdx.x];
+                if constexpr (GK == 3) {
+                    const GaussRec* r = reinterpret_cast<const GaussRec*>(a.grec) + id;
+                    float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3);
+                    float mxt = (r0.x - (float)ox) + (r0.y - 0.5f);
+                    float myt = (r0.z - (float)oy) + (r0.w - 0.5f);
+                    uint32_t sxr = __float_as_uint(r2.w), syr = __float_as_uint(r3.x);
+                    mask = patch_mask<1>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
+                                         span_hi(syr) - oy);
+                    // exact conservative cull: d < fl(max_ds + eps) is necessary for the gate
+#pragma unroll
+                    for (int w = 0; w < NWARP; ++w)
+                        if (!(r2.x < sm.wmax[w] + r2.y)) mask &= ~(1u << w);
+                    sm.st[0][threadIdx.x] = make_float4(mxt, myt, r1.x, r1.y);
+                    sm.st[1][threadIdx.x] = make_float4(r1.z, r1.w, r2.x, r2.y);
+                    sm.st[2][threadIdx.x] = make_float4(r3.y, r3.z, r3.w, r2.z);
+                } else {
+                    const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + id;
+                    float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3),
+                           r4 = __ldg(&r->r4);
+                    float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
+                    float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
+                    float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
+                    float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
+                    uint32_t sxr = __float_as_uint(r3.z), syr = __float_as_uint(r3.w);
+                    mask = patch_mask<1>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
+                                         span_hi(syr) - oy);
+                    sm.st[0][threadIdx.x] = make_float4(d0, r0.y, r0.z, r0.w);
+                    sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
+                    sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.x, r3.y);
+                    sm.st[3][threadIdx.x] = r4;
+                }
+                if constexpr (GEOM) sm.st[4][threadIdx.x] = __ldg(a.g_nrm + id);
+            }
+            build_lists(sm, mask, warp, lane);
+            const int L = sm.tot[warp];
+            for (int k = 0; k < L; ++k) {
+                const int j = sm.wl[warp][k];
+                const float4 A = sm.st[0][j], B = sm.st[1][j], C = sm.st[2][j];
+                if constexpr (GK == 3) {
+                    // forward.py:301-311
+                    const float dx = lx - A.x, dy = ly - A.y;
+                    const float p = fmaf(A.z * dx, dx, fmaf(B.x * dy, dy, A.w * dx * dy));
+                    if (p >= C.w) {
+                        const float al = B.y * __expf(p);
+                        if (al >= ALPHA_CUTOFF_F && B.z < ds + B.w) {
+                            wsum += al;
+                            cr = fmaf(al, C.x, cr); cg = fmaf(al, C.y, cg); cb = fmaf(al, C.z, cb);
+                            if constexpr (GEOM) {
+                                const float4 N = sm.st[4][j];
+                                dsum = fmaf(al, B.z, dsum);
+                                nx = fmaf(al, N.x, nx); ny = fmaf(al, N.y, ny); nz = fmaf(al, N.z, nz);
+                            }
+                        }
+                    }
+                } else {
+                    // forward.py:361-379
+                    const float4 E = sm.st[3][j];
+                    const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
+                    const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
+                    const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
+                    const float r2u = fmaf(U, U, V * V);
+                    if (r2u <= E.w * den * den && fabsf(den) > pe) {
+                        const float inv = __fdividef(1.0f, den);
+                        const float t = A.w * inv;
+                        const float q2 = r2u * inv * inv;
+                        const float al = C.z * __expf(-0.5f * q2);
+                        if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds + C.w) {
+                            wsum += al;
+                            cr = fmaf(al, E.x, cr); cg = fmaf(al, E.y, cg); cb = fmaf(al, E.z, cb);
+                            if constexpr (GEOM) {
+                                const float4 N = sm.st[4][j];
+                                dsum = fmaf(al, t, dsum);
+                                nx = fmaf(al, N.x, nx); ny = fmaf(al, N.y, ny); nz = fmaf(al, N.z, nz);
+                            }
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (inside) {
+            if (a.out.g_weight) a.out.g_weight[pix] = wsum;
+            if (a.out.g_color) {
+                a.out.g_color[3 * pix] = cr; a.out.g_color[3 * pix + 1] = cg; a.out.g_color[3 * pix + 2] = cb;
+            }
+            if constexpr (GEOM) {
+                if (a.out.g_depth) a.out.g_depth[pix] = dsum;
+                if (a.out.g_normal) {
+                    a.out.g_normal[3 * pix] = nx; a.out.g_normal[3 * pix + 1] = ny;
+                    a.out.g_normal[3 * pix + 2] = nz;
+                }
+            }
+            if (a.out.image) {
+                float3 im;
+                if (a.layers == GES_LAYERS_GAUSSIANS_ONLY) {   // forward.py:412-416
+                    if (wsum > 0.f) {
+                        float dn = fmaxf(wsum, 1e-12f);
+                        im = make_float3(cr / dn, cg / dn, cb / dn);
+                    } else {
+                        im = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+                    }
+                } else {                                       // composite, forward.py:384-388
+                    float dn = 1.0f + wsum;
+                    im = make_float3((cs.x + cr) / dn, (cs.y + cg) / dn, (cs.z + cb) / dn);
+                }
+                a.out.image[3 * pix] = im.x; a.out.image[3 * pix + 1] = im.y; a.out.image[3 * pix + 2] = im.z;
+            }
+        }
+    } else if (inside) {   // surfels_only (forward.py:407-410): empty Gaussian buffers
+        if (a.out.image) {
+            a.out.image[3 * pix] = cs.x; a.out.image[3 * pix + 1] = cs.y; a.out.image[3 * pix + 2] = cs.z;
+        }
+        if (a.out.g_weight) a.out.g_weight[pix] = 0.f;
+        if (a.out.g_color) {
+            a.out.g_color[3 * pix] = 0.f; a.out.g_color[3 * pix + 1] = 0.f; a.out.g_color[3 * pix + 2] = 0.f;
+        }
+    }
+}
+
+template <int SS, int MODE>
+static void launch_kind(const TileArgs& a, int g_kind, bool geom, cudaStream_t s) {
+    unsigned nt = (unsigned)(a.ntx * a.nty);
+    if (g_kind == 2) {
+        if (geom) k_tile<SS, MODE, 2, true><<<nt, NB, 0, s>>>(a);
+        else k_tile<SS, MODE, 2, false><<<nt, NB, 0, s>>>(a);
+    } else {
+        if (geom) k_tile<SS, MODE, 3, true><<<nt, NB, 0, s>>>(a);
+        else k_tile<SS, MODE, 3, false><<<nt, NB, 0, s>>>(a);
+    }
+}
+
+cudaError_t launch_tile(const TileArgs& a, int ss, int mode, int g_kind, bool geom, cudaStream_t s) {
+    if (a.ntx * a.nty == 0) return cudaSuccess;
+    if (mode == 2) {
+        launch_kind<1, 2>(a, g_kind, geom, s);
+    } else if (ss == 4) {
+        if (mode == 1) launch_kind<2, 1>(a, 3, false, s);
+        else launch_kind<2, 3>(a, g_kind, geom, s);
+    } else {
+        if (mode == 1) launch_kind<1, 1>(a, 3, false, s);
+        else launch_kind<1, 3>(a, g_kind, geom, s);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- composite / smooth_geometry
+__global__ void k_composite(const float* __restrict__ sc, const float* __restrict__ gc,
+                            const float* __restrict__ gw, float sw, float* __restrict__ img, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float dn = sw + gw[i];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) img[3 * i + c] = (sc[3 * i + c] * sw + gc[3 * i + c]) / dn;
+    }
+}
+
+__global__ void k_smooth(const float* __restrict__ sd, const float* __restrict__ sn, const float* __restrict__ gd,
+                         const float* __restrict__ gn, const float* __restrict__ gw, float* __restrict__ dout,
+                         float* __restrict__ nout, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float dn = 1.0f + gw[i];
+        dout[i] = (sd[i] + gd[i]) / dn;
+        float v0 = (sn[3 * i] + gn[3 * i]) / dn, v1 = (sn[3 * i + 1] + gn[3 * i + 1]) / dn,
+              v2 = (sn[3 * i + 2] + gn[3 * i + 2]) / dn;
+        float nr = sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
+        bool ok = nr > 1e-12f;
+        float inv = ok ? 1.0f / fmaxf(nr, 1e-12f) : 0.f;
+        nout[3 * i] = v0 * inv; nout[3 * i + 1] = v1 * inv; nout[3 * i + 2] = v2 * inv;
+    }
+}
+
+cudaError_t launch_composite(const float* sc, const float* gc, const float* gw, float sw, float* img, int64_t n,
+                             cudaStream_t s) {
+    if (n > 0) k_composite<<<1184, 256, 0, s>>>(sc, gc, gw, sw, img, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_smooth(const float* sd, const float* sn, const float* gd, const float* gn, const float* gw,
+                          float* d_out, float* n_out, int64_t n, cudaStream_t s) {
+    if (n > 0) k_smooth<<<1184, 256, 0, s>>>(sd, sn, gd, gn, gw, d_out, n_out, n);
+    return cudaGetLastError();
+}
+
+}  // namespace ges

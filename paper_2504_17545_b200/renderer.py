@@ -1,0 +1,283 @@
+"""Device-native render engine: packed device scenes, frame workspaces and
+the C-ABI calls, all on torch-managed CUDA memory and the current stream.
+
+``Renderer.render`` returns device tensors and never synchronises unless
+asked to (``check=True``); the drop-in NumPy API in :mod:`.forward` is a thin
+layer over it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+STATUS_WORDS = 3   # ges_frame_status_t = {i64, i64, i32, i32}
+
+
+def _kind_dim(g) -> int:
+    v = getattr(getattr(g, "kind", None), "value", getattr(g, "kind", None))
+    if v in ("2d", "TWO_D", 2):
+        return 2
+    if v in ("3d", "THREE_D", 3, None):
+        return int(np.asarray(g.log_scale).shape[1]) if v is None else 3
+    raise ValueError(f"unknown Gaussian kind {v!r}")
+
+
+def _degree(sh) -> int:
+    K = int(np.asarray(sh).shape[1])
+    d = int(round(math.sqrt(K))) - 1
+    if (d + 1) ** 2 != K:
+        raise ValueError(f"coefficient count {K} is not a square")
+    if not 0 <= d <= 3:
+        raise ValueError(f"SH degree must be in [0, 3], got {d}")   # sh.py:24-31
+    return d
+
+
+def camera_struct(cam) -> _lib.Camera:
+    m = np.asarray(cam.world_to_camera, dtype=np.float64)
+    c = _lib.Camera()
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.w2c[:] = [float(v) for v in m[:3, :4].reshape(-1)]
+    return c
+
+
+def settings_struct(st) -> _lib.Settings:
+    s = _lib.Settings()
+    s.supersample = int(st.supersample)
+    s.layers = _lib.LAYERS[st.layers]
+    s.mip = int(bool(st.mip))
+    s.epsilon_mode = 1 if st.epsilon_mode == "constant" else 0
+    s.epsilon_value = float(st.epsilon_value)
+    s.with_geometry = int(bool(st.with_geometry))
+    s.background[:] = [float(v) for v in st.background]
+    return s
+
+
+class DeviceScene:
+    """A scene packed once into float32 SoA on the device (kernel K0).
+
+    Built from any object with the reference's ``Scene`` fields; the source
+    float64 arrays are uploaded, packed by ``ges_scene_pack`` and dropped.
+    """
+
+    def __init__(self, scene, device=None):
+        self.device = torch.device(device or "cuda")
+        s, g = scene.surfels, scene.gaussians
+        ns, ng = int(np.asarray(s.pos).shape[0]), int(np.asarray(g.pos).shape[0])
+        ds = _degree(s.sh) if ns else None
+        dg = _degree(g.sh) if ng else None
+        if ds is not None and dg is not None and ds != dg:
+            raise NotImplementedError("surfels and Gaussians with different SH degrees")
+        deg = ds if ds is not None else (dg if dg is not None else int(getattr(scene, "sh_degree", 0)))
+        dim = _kind_dim(g)
+        self.n_surfels, self.n_gaussians, self.sh_degree, self.dim = ns, ng, deg, dim
+        dev = self.device
+
+        def up(a, shape):
+            t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)).reshape(shape))
+            return t.to(dev, non_blocking=False)
+
+        K = (deg + 1) ** 2
+        keep = []
+        src = _lib.SceneSrc()
+        src.n_surfels, src.n_gaussians, src.sh_degree, src.gaussian_dim = ns, ng, deg, dim
+        if ns:
+            for name, a, shp in (("s_pos", s.pos, (ns, 3)), ("s_quat", s.quat, (ns, 4)),
+                                 ("s_log_scale", s.log_scale, (ns, 2)), ("s_sh", s.sh, (ns, K, 3))):
+                t = up(a, shp)
+                keep.append(t)
+                setattr(src, name, t.data_ptr())
+        if ng:
+            f3 = getattr(g, "filter3d", None)
+            f3 = np.zeros(ng) if f3 is None else f3
+            for name, a, shp in (("g_pos", g.pos, (ng, 3)), ("g_raw_opacity", g.raw_opacity, (ng,)),
+                                 ("g_quat", g.quat, (ng, 4)), ("g_log_scale", g.log_scale, (ng, dim)),
+                                 ("g_sh", g.sh, (ng, K, 3)), ("g_filter3d", f3, (ng,))):
+                t = up(a, shp)
+                keep.append(t)
+                setattr(src, name, t.data_ptr())
+        L = _lib.lib()
+        nbytes = L.ges_scene_bytes(ns, ng, deg)
+        self.blob = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
+        self.c = _lib.Scene()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(L.ges_scene_pack(C.byref(src), C.c_void_p(self.blob.data_ptr()), nbytes,
+                                    C.byref(self.c), C.c_void_p(stream)), "ges_scene_pack")
+        self._src = keep   # freed by the caching allocator in stream order
+        torch.cuda.current_stream(dev).synchronize()
+        self._src = None
+
+    @property
+    def nbytes(self) -> int:
+        return self.blob.numel()
+
+
+class _SceneCache:
+    """LRU of packed scenes keyed by the identity of the source arrays."""
+
+    def __init__(self, size=4):
+        self.size = size
+        self.d: OrderedDict = OrderedDict()
+
+    @staticmethod
+    def _key(scene, device):
+        s, g = scene.surfels, scene.gaussians
+        arrs = (s.pos, s.quat, s.log_scale, s.sh, g.pos, g.raw_opacity, g.quat, g.log_scale, g.sh,
+                getattr(g, "filter3d", None))
+        parts = []
+        for a in arrs:
+            if a is None:
+                parts.append(None)
+            else:
+                parts.append((id(a), np.asarray(a).__array_interface__["data"][0], np.asarray(a).shape))
+        return (str(device), _kind_dim(g), tuple(parts)), arrs
+
+    def get(self, scene, device):
+        key, arrs = self._key(scene, device)
+        hit = self.d.get(key)
+        if hit is not None:
+            self.d.move_to_end(key)
+            return hit[0]
+        ds = DeviceScene(scene, device)
+        self.d[key] = (ds, arrs)   # holding arrs pins the ids
+        while len(self.d) > self.size:
+            self.d.popitem(last=False)
+        return ds
+
+    def clear(self):
+        self.d.clear()
+
+
+SCENE_CACHE = _SceneCache()
+
+
+@dataclass
+class Frame:
+    """Device outputs of one render call (any field may be None)."""
+    image: torch.Tensor = None
+    s_color: torch.Tensor = None
+    s_depth: torch.Tensor = None
+    s_normal: torch.Tensor = None
+    s_winner: torch.Tensor = None
+    g_color: torch.Tensor = None
+    g_weight: torch.Tensor = None
+    g_depth: torch.Tensor = None
+    g_normal: torch.Tensor = None
+    status: torch.Tensor = None
+
+    def pairs(self):
+        st = self.status.cpu()
+        return int(st[0]), int(st[1]), int(st[2] & 0xFFFFFFFF)
+
+
+_ALL = ("image", "s_color", "s_depth", "s_normal", "s_winner", "g_color", "g_weight", "g_depth",
+        "g_normal")
+
+
+class Renderer:
+    """Owns a frame workspace on one device and renders packed scenes.
+
+    Tile-pair lists are sized by a capacity (pairs) that grows on overflow:
+    the device reports the pairs a frame needed in its status word, and
+    ``check=True`` re-renders a frame whose lists overflowed.
+    """
+
+    def __init__(self, device=None):
+        self.device = torch.device(device or "cuda")
+        self.cap_s = 0
+        self.cap_g = 0
+        self._ws = None
+
+    def _caps(self, ds: DeviceScene, ss: int):
+        self.cap_s = max(self.cap_s, 1 << 20, 8 * ds.n_surfels * (4 if ss == 4 else 1))
+        self.cap_g = max(self.cap_g, 1 << 20, 8 * ds.n_gaussians)
+
+    def workspace(self, ds, cam_c, st_c):
+        need = _lib.lib().ges_workspace_bytes(C.byref(ds.c), C.byref(cam_c), C.byref(st_c),
+                                               self.cap_s, self.cap_g)
+        if need == 0:
+            _lib.check(_lib.GES_EINVAL, "ges_workspace_bytes")
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws, need
+
+    def alloc(self, cam, settings, want=_ALL) -> Frame:
+        H, W = int(cam.height), int(cam.width)
+        f32 = dict(dtype=torch.float32, device=self.device)
+        fr = Frame(status=torch.zeros(STATUS_WORDS, dtype=torch.int64, device=self.device))
+        shapes = dict(image=(H, W, 3), s_color=(H, W, 3), s_depth=(H, W), s_normal=(H, W, 3),
+                      g_color=(H, W, 3), g_weight=(H, W), g_depth=(H, W), g_normal=(H, W, 3))
+        for k in want:
+            if k == "s_winner":
+                fr.s_winner = torch.empty((H, W), dtype=torch.int32, device=self.device)
+            elif k in ("g_depth", "g_normal") and not settings.with_geometry:
+                continue
+            else:
+                setattr(fr, k, torch.empty(shapes[k], **f32))
+        return fr
+
+    @staticmethod
+    def _outputs(fr: Frame) -> _lib.Outputs:
+        o = _lib.Outputs()
+        for k in _ALL:
+            t = getattr(fr, k)
+            setattr(o, k, t.data_ptr() if t is not None else None)
+        return o
+
+    def render(self, ds: DeviceScene, cam, settings, *, frame: Frame = None, mode: int = 3,
+               surfel_depth: torch.Tensor = None, check: bool = True, want=_ALL) -> Frame:
+        """mode 3: full render; 1: surfel pass only; 2: Gaussian pass against
+        ``surfel_depth`` (H, W) float32 on the device."""
+        cam_c = camera_struct(cam)
+        st_c = settings_struct(settings)
+        fr = frame if frame is not None else self.alloc(cam, settings, want)
+        out_c = self._outputs(fr)
+        L = _lib.lib()
+        for attempt in range(3):
+            self._caps(ds, settings.supersample)
+            ws, nbytes = self.workspace(ds, cam_c, st_c)
+            stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+            args_ws = (C.c_void_p(ws.data_ptr()), nbytes)
+            st_ptr = C.c_void_p(fr.status.data_ptr())
+            if mode == 3:
+                rc = L.ges_render(C.byref(ds.c), C.byref(cam_c), C.byref(st_c), C.byref(out_c), *args_ws,
+                                  self.cap_s, self.cap_g, st_ptr, stream)
+            elif mode == 1:
+                rc = L.ges_rasterize_surfels(C.byref(ds.c), C.byref(cam_c), C.byref(st_c), C.byref(out_c),
+                                             *args_ws, self.cap_s, st_ptr, stream)
+            else:
+                dep = surfel_depth.contiguous()
+                rc = L.ges_accumulate_gaussians(C.byref(ds.c), C.byref(cam_c), C.c_void_p(dep.data_ptr()),
+                                                C.byref(st_c), C.byref(out_c), *args_ws, self.cap_g,
+                                                st_ptr, stream)
+            _lib.check(rc, "render")
+            if not check:
+                return fr
+            sp, gp, ovf = fr.pairs()
+            if not ovf:
+                return fr
+            self.cap_s = max(self.cap_s, int(sp * 1.25) + 1024)
+            self.cap_g = max(self.cap_g, int(gp * 1.25) + 1024)
+        raise RuntimeError("tile pair lists overflowed repeatedly")
+
+
+_RENDERERS: dict = {}
+
+
+def default_renderer(device=None) -> Renderer:
+    dev = torch.device(device or "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    r = _RENDERERS.get(dev)
+    if r is None:
+        r = _RENDERERS[dev] = Renderer(dev)
+    return r

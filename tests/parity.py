@@ -1,0 +1,61 @@
+"""Parity comparator: GPU float32 outputs vs the float64 oracle.
+
+Rule (north_star): the surfel-ID map must be bit-exact except
+on pixels the oracle flags as ties (float64 decision margin below the TIE_*
+thresholds in oracle/ges_oracle.py); depth relative error <= DEPTH_REL and
+RGB max-abs error <= RGB_TOL on the remaining pixels; PSNR >= 60 dB over all
+pixels.  The report counts the excluded pixels.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+RGB_TOL = 1e-4
+DEPTH_REL = 1e-5
+PSNR_MIN = 60.0
+
+
+def psnr(a, b):
+    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return float("inf") if mse == 0 else 10.0 * np.log10(1.0 / mse)
+
+
+def compare(gpu, ora, tie, *, region=None):
+    """gpu / ora: dicts with image, s_winner, s_depth (+ optional s_color,
+    g_weight, g_color ...).  tie: (H, W) bool.  region: optional (H, W) bool
+    mask restricting the comparison (tile-sampled oracle)."""
+    H, W = tie.shape
+    region = np.ones((H, W), bool) if region is None else region
+    keep = region & ~tie
+    rep = dict(pixels=int(region.sum()), excluded=int((region & tie).sum()))
+    gw, ow = gpu["s_winner"], ora["s_winner"]
+    rep["winner_mismatch"] = int(((gw != ow) & keep).sum())
+    rep["winner_mismatch_incl_ties"] = int(((gw != ow) & region).sum())
+    gd, od = gpu["s_depth"].astype(np.float64), ora["s_depth"]
+    both = keep & np.isfinite(od) & (gw == ow)
+    rep["coverage_mismatch"] = int((np.isfinite(gd) != np.isfinite(od))[keep].sum())
+    rep["depth_rel_max"] = float(np.max(np.abs(gd[both] - od[both]) / np.abs(od[both]))) if both.any() else 0.0
+    for k in ("image", "s_color", "s_normal", "g_color", "g_weight", "g_depth", "g_normal"):
+        if k in gpu and k in ora and gpu[k] is not None and ora[k] is not None:
+            diff = np.abs(gpu[k].astype(np.float64) - ora[k])
+            if diff.ndim == 3:
+                diff = diff.max(axis=-1)
+            rep[f"{k}_maxabs"] = float(diff[keep].max()) if keep.any() else 0.0
+    r = region
+    rep["psnr"] = psnr(gpu["image"][r], ora["image"][r])
+    return rep
+
+
+def assert_parity(rep, *, rgb_tol=RGB_TOL, depth_rel=DEPTH_REL, psnr_min=PSNR_MIN,
+                  weight_tol=None):
+    assert rep["winner_mismatch"] == 0, rep
+    assert rep["coverage_mismatch"] == 0, rep
+    assert rep["depth_rel_max"] <= depth_rel, rep
+    assert rep["image_maxabs"] <= rgb_tol, rep
+    if "s_color_maxabs" in rep:
+        assert rep["s_color_maxabs"] <= rgb_tol, rep
+    if "g_color_maxabs" in rep and weight_tol is not None:
+        assert rep["g_weight_maxabs"] <= weight_tol, rep
+        assert rep["g_color_maxabs"] <= weight_tol, rep
+    assert rep["psnr"] >= psnr_min, rep

@@ -1,0 +1,254 @@
+"""GPU parity: the sm_100a kernels (through the C ABI via the drop-in API)
+against the float64 oracle and the reference golden vectors.  Mirrors the
+reference's own hot-path tests (pkg/tests/test_forward.py) with the float32
+parity rule of tests/parity.py."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2504_17545_b200 as G  # noqa: E402
+from paper_2504_17545_b200 import scenes as S  # noqa: E402
+from paper_2504_17545_b200.types import (Camera, GaussianKind, GaussianSet, Scene, Stage,  # noqa: E402
+                                         SurfelSet)
+from golden_io import load, names, settings_ns  # noqa: E402
+from oracle import ges_oracle as O  # noqa: E402
+from parity import assert_parity, compare  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def gpu_dict(out):
+    d = dict(image=out.image, s_winner=out.surfels.winner, s_depth=out.surfels.depth,
+             s_color=out.surfels.color, s_normal=out.surfels.normal,
+             g_color=out.gaussians.color, g_weight=out.gaussians.weight)
+    if out.gaussians.depth is not None:
+        d.update(g_depth=out.gaussians.depth, g_normal=out.gaussians.normal)
+    return d
+
+
+def ora_dict(out):
+    d = dict(image=out.image, s_winner=out.surfels.winner, s_depth=out.surfels.depth,
+             s_color=out.surfels.color, s_normal=out.surfels.normal,
+             g_color=out.gaussians.color, g_weight=out.gaussians.weight)
+    if out.gaussians.depth is not None:
+        d.update(g_depth=out.gaussians.depth, g_normal=out.gaussians.normal)
+    return d
+
+
+def settings32(st):
+    kw = {k: (tuple(v) if isinstance(v, list) else v) for k, v in st.items()}
+    return G.RenderSettings(dtype=np.float32, **kw)
+
+
+@pytest.mark.parametrize("name", names())
+def test_golden_parity(name):
+    """GPU vs the reference's own float64 output, ties from the oracle."""
+    scene, cam, st, gold, _ = load(name)
+    out = G.render(scene, cam, settings32(st))
+    ora = O.render(scene, cam, settings_ns(st), ties=True)
+    ref = dict(image=gold["image"], s_winner=gold["s_winner"], s_depth=gold["s_depth"],
+               s_color=gold["s_color"], s_normal=gold["s_normal"], g_color=gold["g_color"],
+               g_weight=gold["g_weight"])
+    if "g_depth" in gold:
+        ref.update(g_depth=gold["g_depth"], g_normal=gold["g_normal"])
+    rep = compare(gpu_dict(out), ref, ora.tie)
+    assert_parity(rep, weight_tol=5e-4)
+    if "g_depth_maxabs" in rep:
+        assert rep["g_depth_maxabs"] < 5e-4 and rep["g_normal_maxabs"] < 5e-4, rep
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_random_scene_480x270(seed):
+    """Denser stress scene (the survey's fp32-vs-fp64 noise-floor setup, scaled)."""
+    r = np.random.default_rng(seed)
+    sc = Scene(S.random_surfels(r, 20000, 3, scale_range=(0.005, 0.02)),
+               S.random_gaussians(r, 6000, 3, scale_range=(0.004, 0.025), extent=1.2), 3, Stage.FROZEN)
+    cam = S.make_camera(480, 270)
+    out = G.render(sc, cam)
+    ora = O.render(sc, cam, settings_ns({}), ties=True)
+    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie)
+    assert_parity(rep)
+
+
+def test_config2_tile_sample():
+    """Full-size config 2 (1M surfels + 300k Gaussians, 1080p): GPU frame vs
+    the oracle on a sample of tiles including the densest ones."""
+    sc = S.config_scene(2)
+    cam = S.config_cameras(2)[0]
+    out = G.render(sc, cam)
+    ntx = (cam.width + 15) // 16
+    nt = ntx * ((cam.height + 15) // 16)
+    rng = np.random.default_rng(5)
+    tiles = sorted(set(rng.choice(nt, 12, replace=False).tolist() + [nt // 2 + ntx // 2, nt // 2]))
+    ora = O.render(sc, cam, settings_ns({}, np.float64), tiles=tiles, ties=True)
+    region = np.zeros((cam.height, cam.width), bool)
+    for ti in tiles:
+        ty0, ty1, tx0, tx1 = O.tile_list(cam.height, cam.width)[ti]
+        region[ty0:ty1, tx0:tx1] = True
+    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie, region=region)
+    assert_parity(rep)
+    assert rep["pixels"] >= 12 * 256
+
+
+# ---- known-answer tests (test_forward.py:79-145) --------------------------------
+def frontal(color=0.2, depth=3.0, scale=1.0):
+    sh = np.zeros((1, 1, 3))
+    sh[0, 0] = (color - 0.5) / 0.28209479177387814
+    s = SurfelSet(np.array([[0.0, 0.0, depth]]), np.array([[1.0, 0, 0, 0]]),
+                  np.log(np.full((1, 2), scale)), sh, np.array([255.0]))
+    return Scene(s, GaussianSet.empty(0), 0, Stage.FROZEN)
+
+
+def ident(w=32, h=32, f=40.0):
+    return Camera(f, f, w / 2, h / 2, w, h, np.eye(4))
+
+
+def test_single_surfel_centre():
+    b = G.rasterize_surfels(frontal(0.8, 3.0), ident())
+    assert b.coverage[16, 16]
+    assert np.allclose(b.color[16, 16], 0.8, atol=1e-6)
+    assert np.isclose(b.depth[16, 16], 3.0, rtol=1e-6)
+    assert np.allclose(b.normal[16, 16], [0, 0, -1])
+    assert b.winner[16, 16] == 0
+
+
+def test_zbuffer_nearest_and_background():
+    near, far = frontal(0.9, 2.0), frontal(0.1, 5.0)
+    sc = Scene(SurfelSet(*(np.concatenate([getattr(far.surfels, k), getattr(near.surfels, k)])
+                           for k in ("pos", "quat", "log_scale", "sh", "w"))),
+               GaussianSet.empty(0), 0, Stage.FROZEN)
+    b = G.rasterize_surfels(sc, ident(), G.RenderSettings(background=(0.25, 0.5, 0.75)))
+    assert b.winner[16, 16] == 1 and np.allclose(b.color[16, 16], 0.9, atol=1e-6)
+    small = G.rasterize_surfels(frontal(scale=0.1), ident(), G.RenderSettings(background=(0.25, 0.5, 0.75)))
+    assert not small.coverage[0, 0] and np.isinf(small.depth[0, 0]) and small.winner[0, 0] == -1
+    assert np.allclose(small.color[0, 0], [0.25, 0.5, 0.75])
+
+
+def test_empty_scene_background():
+    sc = Scene(SurfelSet.empty(0), GaussianSet.empty(0), 0, Stage.FROZEN)
+    out = G.render(sc, ident(), G.RenderSettings(background=(0.1, 0.2, 0.3)))
+    assert np.allclose(out.image, [0.1, 0.2, 0.3])
+
+
+def test_footprint_boundary_radius():
+    R = O.R_OPAQUE
+    b = G.rasterize_surfels(frontal(1.0, 4.0, 1.0), ident(512, 512, 256.0))
+    ys, xs = np.nonzero(b.coverage)
+    rad = np.hypot(xs + 0.5 - 256.0, ys + 0.5 - 256.0) * 4.0 / 256.0
+    assert rad.max() <= R + 1e-5
+    xx, yy = np.meshgrid(np.arange(512) + 0.5, np.arange(512) + 0.5)
+    inside = np.hypot(xx - 256.0, yy - 256.0) * 4.0 / 256.0 <= R - 0.01
+    assert np.all(b.coverage[inside])
+
+
+def test_centered_gaussian_weight():
+    sh = np.zeros((1, 1, 3))
+    sh[0, 0] = (0.9 - 0.5) / 0.28209479177387814
+    g = GaussianSet(np.array([[0.0, 0.0, 2.0]]), np.log(np.array([0.8]) / 0.2), np.array([[1.0, 0, 0, 0]]),
+                    np.log(np.full((1, 3), 0.3)), sh)
+    sc = Scene(SurfelSet.empty(0), g, 0, Stage.FROZEN)
+    gb = G.accumulate_gaussians(sc, ident(), np.full((32, 32), np.inf))
+    d = np.array([0.5, 0.5])
+    cov = (40.0 * 0.3 / 2.0) ** 2 * np.eye(2) + 0.3 * np.eye(2)
+    expect = 0.8 * np.exp(-0.5 * d @ np.linalg.inv(cov) @ d)
+    assert np.isclose(gb.weight[16, 16], expect, rtol=1e-5)
+    assert np.allclose(gb.color[16, 16], expect * 0.9, rtol=1e-5)
+
+
+def test_depth_gate():
+    r = np.random.default_rng(1234)
+    g = S.random_gaussians(r, 1, degree=0)
+    g.pos[0] = [0.0, 0.0, 5.0]
+    sc = Scene(SurfelSet.empty(0), g, 0, Stage.FROZEN)
+    eps = O.gaussian_eff(g)[2][0]
+    assert np.all(G.accumulate_gaussians(sc, ident(), np.full((32, 32), 5.0 - 2 * eps)).weight == 0)
+    assert G.accumulate_gaussians(sc, ident(), np.full((32, 32), 5.0 + eps)).weight.max() > 0
+
+
+def test_epsilon_monotonicity_and_pass_separation():
+    r = np.random.default_rng(3)
+    sc = S.random_scene(r, 10, 30)
+    cam = S.make_camera()
+    base = G.render(sc, cam)
+    big = G.accumulate_gaussians(sc, cam, base.surfels.depth,
+                                 G.RenderSettings(epsilon_mode="constant", epsilon_value=1e9))
+    assert np.all(big.weight >= base.gaussians.weight - 1e-6)
+    only = G.render(sc, cam, G.RenderSettings(layers="surfels_only"))
+    gb = G.accumulate_gaussians(sc, cam, only.surfels.depth)
+    re = G.composite(only.surfels.color, gb)
+    assert np.max(np.abs(re - base.image)) <= 1e-6
+
+
+def test_order_independence_permutation():
+    r = np.random.default_rng(9)
+    sc = S.random_scene(r, 10, 60)
+    cam = S.make_camera()
+    a = G.render(sc, cam)
+    perm = r.permutation(60)
+    sc2 = Scene(sc.surfels, sc.gaussians.select(perm), sc.sh_degree, sc.stage)
+    b = G.render(sc2, cam)
+    assert np.max(np.abs(a.image - b.image)) <= 1e-4
+    sp = r.permutation(10)
+    sc3 = Scene(sc.surfels.select(sp), sc.gaussians, sc.sh_degree, sc.stage)
+    c = G.render(sc3, cam)
+    inv = np.argsort(sp)
+    mapped = np.where(c.surfels.winner >= 0, sp[np.maximum(c.surfels.winner, 0)], -1)
+    assert np.array_equal(mapped, a.surfels.winner)
+
+
+def test_run_to_run_deterministic_surfels():
+    sc = S.config_scene(1)
+    cam = S.config_cameras(1)[0]
+    a = G.render(sc, cam)
+    b = G.render(sc, cam)
+    assert np.array_equal(a.surfels.winner, b.surfels.winner)
+    assert np.array_equal(a.surfels.depth, b.surfels.depth)
+    assert np.max(np.abs(a.image - b.image)) <= 1e-6
+
+
+def test_near_plane_crossing_surfel():
+    """A surfel spanning the focal plane gets whole-screen bounds
+    (geometry.py:295-297) and still matches the oracle."""
+    r = np.random.default_rng(4)
+    s = S.random_surfels(r, 40, 1, scale_range=(0.1, 0.5))
+    s.pos[0] = S.make_camera().position * 0.98
+    s.log_scale[0] = np.log([2.0, 2.0])
+    sc = Scene(s, S.random_gaussians(r, 30, 1), 1, Stage.FROZEN)
+    cam = S.make_camera(64, 64)
+    out = G.render(sc, cam)
+    ora = O.render(sc, cam, settings_ns({}), ties=True)
+    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+
+
+def test_settings_validation():
+    with pytest.raises(ValueError):
+        G.RenderSettings(supersample=2)
+    with pytest.raises(ValueError):
+        G.RenderSettings(layers="nope")
+    with pytest.raises(ValueError):
+        G.RenderSettings(epsilon_mode="x")
+    sc = S.random_scene(np.random.default_rng(0), 3, 3)
+    with pytest.raises(NotImplementedError):
+        G.render(sc, S.make_camera(), G.RenderSettings(dtype=np.float64))
+    bad = Scene(S.random_surfels(np.random.default_rng(0), 3, 1), GaussianSet.empty(1), 1, Stage.FROZEN)
+    bad.surfels.sh = np.zeros((3, 5, 3))
+    with pytest.raises(ValueError):
+        G.render(bad, S.make_camera())
+
+
+def test_smooth_geometry_identity():
+    sc = S.random_scene(np.random.default_rng(2), 10, 0)
+    out = G.render(sc, S.make_camera(), G.RenderSettings(with_geometry=True))
+    d, n = G.smooth_geometry(out.surfels, out.gaussians)
+    assert np.array_equal(d, out.surfels.depth)
+    cov = out.surfels.coverage
+    assert np.allclose(n[cov], out.surfels.normal[cov], atol=1e-6)
+    with pytest.raises(ValueError):
+        G.smooth_geometry(out.surfels, G.GaussianBuffers(out.gaussians.color, out.gaussians.weight))
