@@ -1,0 +1,418 @@
+"""Benchmark of the GES forward render path on B200 (contract: one JSON line).
+
+Default workload = BASELINE config 2: 1M surfels + 300k Gaussians, SH degree
+3, 1920x1080, float32, seeded synthetic scene.  One step = one
+batch of ``--views`` views per rank (azimuths around the 8(d) pose, same
+distance/elevation); value = frames/s over all ranks (weak scaling: fixed
+views per GPU).  For N > 1 each step ends with the frame exchange: the RGBA8
+frames are gathered to rank 0 over NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--views 8]
+  python bench.py --impl reference ...   # the reference algorithm on host cores
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ges", choices=["ges", "reference"])
+    p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--views", type=int, default=None, help="views per rank per step")
+    p.add_argument("--ss", type=int, default=1, choices=[1, 4])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    p.add_argument("--cpu-tiles", type=int, default=48, help="tiles in the CPU sample")
+    p.add_argument("--profile-only", action="store_true", help="render a few frames, no JSON (for ncu)")
+    return p.parse_args()
+
+
+ARGS = parse()
+if ARGS.impl == "reference":
+    # the reference's CPU tile threads; keep BLAS single-threaded per tile thread
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+from paper_2504_17545_b200 import scenes as S  # noqa: E402
+
+METRIC = "frames/sec at 1080p (1M surfels+300k Gaussians) per B200, views/s at 1/2/4/8 GPUs"
+WORKLOADS = {
+    1: "config1: 10k surfels + 2k Gaussians, SH0, 128x128",
+    2: "config2: 1M surfels + 300k Gaussians, SH3, 1920x1080",
+    3: "config3 (Speedy): 1M surfels + 60k Gaussians, SH3, 1920x1080",
+    4: "config4 (Mip): 1M surfels + 300k filtered Gaussians, SH3, 3840x2160, mip=True",
+    5: "config5: 3M surfels + 1M Gaussians, SH3, 3840x2160 orbit views",
+}
+DEFAULT_VIEWS = {1: 32, 2: 8, 3: 8, 4: 4, 5: 4}
+
+
+def views_for(cfg, rank, world, per_rank):
+    """Cameras of this rank's views."""
+    total = per_rank * world
+    ks = range(rank * per_rank, (rank + 1) * per_rank)
+    if cfg == 5:
+        cams = S.orbit_cameras((0, 0, 0), 4.0, max(total, 1), height=1.0, fov_deg=50.0,
+                               width=3840, height_px=2160)
+        return [cams[k] for k in ks]
+    w, h = S.CONFIGS[cfg]["res"]
+    return [S.make_camera(w, h, azim=0.3 + 2.0 * math.pi * k / total) for k in ks]
+
+
+def b_alg(cfg, W, H):
+    """Algorithmic bytes per frame: scene read once + 20 B/px."""
+    c = S.CONFIGS[cfg]
+    K = (c["deg"] + 1) ** 2
+    ng = c["ng"]
+    return c["ns"] * (36 + 12 * K) + ng * (44 + 12 * K) + W * H * 20
+
+
+def base_config(cfg, per_rank, world, ss):
+    w, h = S.CONFIGS[cfg]["res"]
+    return {"workload": WORKLOADS[cfg], "views_per_rank_per_step": per_rank,
+            "resolution": [w, h], "supersample": ss, "parallelism": f"views x{world}",
+            "scene": "seeded synthetic (SURVEY 8(d), seed 0)",
+            "l2": "inputs larger than L2 (packed scene > 126 MB; no flush needed)"}
+
+
+# ----------------------------------------------------------------------------- CPU
+def cpu_sample(cfg, scene, cam, n_tiles, threads, ss=1):
+    """Time the reference algorithm (oracle/ges_oracle.py, float32 like the
+    reference default) on a bounded sample: full per-frame preprocessing plus
+    ``n_tiles`` of the frame's tiles, extrapolated to the whole frame."""
+    from oracle import ges_oracle as O
+    from types import SimpleNamespace
+    st = SimpleNamespace(supersample=ss, background=(0.0, 0.0, 0.0), layers="full", mip=cfg == 4,
+                         epsilon_mode="adaptive", epsilon_value=0.0, dtype=np.float32,
+                         threads=threads, with_geometry=False)
+    nt = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    rng = np.random.default_rng(7)
+    tiles = sorted(rng.choice(nt, min(n_tiles, nt), replace=False).tolist())
+    t0 = time.perf_counter()
+    O.render(scene, cam, st, tiles=[])            # per-frame preprocessing only
+    t1 = time.perf_counter()
+    O.render(scene, cam, st, tiles=tiles)         # preprocessing + sampled tiles
+    t2 = time.perf_counter()
+    pre = t1 - t0
+    per_tile = max((t2 - t1) - pre, 0.0) / len(tiles)
+    frame_s = pre + per_tile * nt
+    return frame_s, t2 - t0, len(tiles), nt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on this box's host cores."""
+    if rank != 0:
+        return
+    cfg = args.config
+    scene = S.config_scene(cfg)
+    cam = views_for(cfg, 0, 1, 1)[0]
+    threads = os.cpu_count() or 1
+    per_rank = args.views or DEFAULT_VIEWS[cfg]
+    n_tiles = 8
+    times = []
+    wall = 0.0
+    for i in range(args.warmup + args.steps):
+        fs, w, nt, tot = cpu_sample(cfg, scene, cam, n_tiles, threads, args.ss)
+        if i >= args.warmup:
+            times.append(fs)
+            wall += w
+    frame_s = statistics.median(times)
+    fps = 1.0 / frame_s
+    sample = (f"per step: full per-frame preprocessing + {nt} of {tot} tiles of one "
+              f"{cam.width}x{cam.height} view, extrapolated to the frame; float32; "
+              f"{threads} tile threads, OPENBLAS_NUM_THREADS=1")
+    line = {"metric": METRIC, "value": fps, "unit": "frames/s", "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": frame_s * per_rank * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": base_config(cfg, per_rank, world, args.ss),
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
+                             "sample": sample, "measured_wall_s": wall},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- GPU
+def run_gpu(args, rank, world, local_rank):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_17545_b200 as G
+    from paper_2504_17545_b200 import _lib
+    from paper_2504_17545_b200.multiview import ViewBatchRenderer, gather_frames
+    from paper_2504_17545_b200.renderer import camera_struct, settings_struct
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = args.config
+    per_rank = args.views or DEFAULT_VIEWS[cfg]
+    scene = S.config_scene(cfg)
+    cams = views_for(cfg, rank, world, per_rank)
+    settings = G.RenderSettings(supersample=args.ss, mip=(cfg == 4))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ds = G.DeviceScene(scene, dev)
+    torch.cuda.synchronize()
+    upload_ms = (time.perf_counter() - t0) * 1e3
+    rend = G.Renderer(dev)
+    # B_alg outputs (image fp32, depth, winner) + the RGBA8 send buffer for the gather
+    vb = ViewBatchRenderer(rend, ds, cams, settings, want=("image", "s_depth", "s_winner", "image_rgba8"))
+    # size the pair lists from a checked first frame of every view
+    for c, fr in zip(vb.cams, vb.frames):
+        rend.render(ds, c, settings, frame=fr, check=True)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        vb.render(check=False)
+        if world > 1:
+            gather_frames(vb.rgba, dst=0)
+
+    if args.profile_only:
+        for _ in range(max(args.warmup, 1) + args.steps):
+            step()
+        torch.cuda.synchronize()
+        return
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    phys = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+    smi_index = phys[local_rank] if len(phys) > local_rank and phys[local_rank] else local_rank
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(smi_index) as clk:
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    if vb.overflowed():
+        raise RuntimeError("tile pair lists overflowed inside the timed region")
+    frames = per_rank * world * args.steps
+    fps = frames / elapsed
+    ms_step = elapsed * 1e3 / args.steps
+    s_pairs, g_pairs, _ = vb.frames[0].pairs()
+
+    # ---- per-phase breakdown (separate pass, events on the launching stream)
+    L = _lib.lib()
+    n_prof = max(4, min(3 * per_rank, 24))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(n_prof)]
+    for row in evs:
+        for e in row:
+            e.record(stream)
+    torch.cuda.synchronize()
+    st_c = settings_struct(settings)
+    for i in range(n_prof):
+        c = vb.cams[i % per_rank]
+        fr = vb.frames[i % per_rank]
+        cam_c = camera_struct(c)
+        ws, nbytes = rend.workspace(ds, cam_c, st_c)
+        arr = (C.c_void_p * 6)(*[e.cuda_event for e in evs[i]])
+        _lib.check(L.ges_render_profiled(C.byref(ds.c), C.byref(cam_c), C.byref(st_c),
+                                         C.byref(rend._outputs(fr)), C.c_void_p(ws.data_ptr()), nbytes,
+                                         rend.cap_s, rend.cap_g, C.c_void_p(fr.status.data_ptr()),
+                                         C.c_void_p(stream.cuda_stream), arr), "profiled render")
+    torch.cuda.synchronize()
+    names = ["memset+surfel_prep", "gauss_prep", "tile_scan", "tile_fill", "tile_render"]
+    phase = {n: statistics.mean(row[k].elapsed_time(row[k + 1]) for row in evs) for k, n in enumerate(names)}
+    frame_ms = statistics.mean(row[0].elapsed_time(row[5]) for row in evs)
+
+    # ---- end-to-end through the C ABI with host buffers (ges_render_views_host)
+    e2e = None
+    if not args.no_e2e:
+        W, H = cams[0].width, cams[0].height
+        host = torch.empty((per_rank, H, W, 3), dtype=torch.float32, pin_memory=True)
+        cams_c = (_lib.Camera * per_rank)(*[camera_struct(c) for c in cams])
+        cam_pin = torch.empty(C.sizeof(cams_c), dtype=torch.uint8, pin_memory=True)
+        C.memmove(cam_pin.data_ptr(), cams_c, C.sizeof(cams_c))
+        cams_pinned = C.cast(C.c_void_p(cam_pin.data_ptr()), C.POINTER(_lib.Camera))
+        imgdev = torch.empty((2, H, W, 3), dtype=torch.float32, device=dev)
+        statuses = torch.zeros((per_rank, 3), dtype=torch.int64, device=dev)
+        copy_stream = torch.cuda.Stream(dev)
+        ws, nbytes = rend.workspace(ds, camera_struct(cams[0]), st_c)
+
+        def e2e_step():
+            _lib.check(L.ges_render_views_host(C.byref(ds.c), cams_pinned, per_rank, C.byref(st_c),
+                                               C.c_void_p(host.data_ptr()), C.c_void_p(ws.data_ptr()), nbytes,
+                                               rend.cap_s, rend.cap_g, C.c_void_p(imgdev.data_ptr()),
+                                               C.c_void_p(statuses.data_ptr()), C.c_void_p(stream.cuda_stream),
+                                               C.c_void_p(copy_stream.cuda_stream)), "views_host")
+
+        for _ in range(args.warmup):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        copy_stream.synchronize()
+        stream.synchronize()
+        e_el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e_el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_el = float(t.item())
+        ref_img = vb.frames[0].image.cpu().numpy()
+        assert np.allclose(host[0].numpy(), ref_img, atol=1e-6), "e2e image differs from device render"
+        e2e = {"value": per_rank * world * args.steps / e_el, "unit": "frames/s",
+               "h2d_bytes_per_step": per_rank * C.sizeof(_lib.Camera),
+               "d2h_bytes_per_step": per_rank * W * H * 3 * 4,
+               "path": "ges_render_views_host (C ABI): host camera structs in, pinned fp32 RGB frames out, "
+                       "copy of view v overlapped with render of view v+1"}
+
+    # ---- CPU baseline sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        fs, wall, nt, tot = cpu_sample(cfg, scene, cams[0], args.cpu_tiles, threads, args.ss)
+        cpu = {"value": 1.0 / fs, "unit": "frames/s", "cores": threads, "kind": "port",
+               "sample": f"oracle/ges_oracle.py (reference algorithm, float32), full per-frame "
+                         f"preprocessing + {nt} of {tot} tiles of one view, extrapolated; "
+                         f"{threads} tile threads; {wall:.1f} s of CPU work",
+               "frame_s": fs}
+
+    if rank != 0:
+        return
+    W, H = cams[0].width, cams[0].height
+    balg = b_alg(cfg, W, H)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = balg / (frame_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_config{cfg}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_frame")
+    line = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": base_config(cfg, per_rank, world, args.ss),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "unit_of_work": "one frame (ges_render: 5 kernels)",
+                     "b_alg_bytes_per_frame": balg, "frame_ms": frame_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                     "phase_ms": phase, "dominant": max(phase, key=phase.get)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": frames * (5 if ds.n_gaussians else 4),
+        "clocks": clk.summary(),
+        "scene_upload_ms": upload_ms,
+        "pairs_per_frame": {"surfel": s_pairs, "gaussian": g_pairs},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = ARGS
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -91,6 +91,7 @@ typedef struct ges_outputs {
     float *s_color, *s_depth, *s_normal;
     int32_t *s_winner;
     float *g_color, *g_weight, *g_depth, *g_normal;
+    uint8_t *image_rgba8;     /* (H,W,4) clip(image*255+0.5) as datasets.py:54-56, alpha 255 */
 } ges_outputs_t;
 
 /* Per-frame counters written by the device (read them after the frame). */
@@ -123,6 +124,16 @@ int ges_render(const ges_scene_t *scene, const ges_camera_t *cam,
                int64_t gaussian_pair_cap, ges_frame_status_t *status_dev,
                void *stream);
 
+/* ges_render that also records 6 CUDA events (cudaEvent_t, may be NULL) on
+ * `stream` at the phase boundaries: [0] frame start, [1] after surfel
+ * preprocess, [2] after Gaussian preprocess, [3] after the tile scan,
+ * [4] after the tile fill, [5] after the fused tile kernel. */
+int ges_render_profiled(const ges_scene_t *scene, const ges_camera_t *cam,
+                        const ges_settings_t *st, const ges_outputs_t *out,
+                        void *workspace, size_t ws_bytes, int64_t surfel_pair_cap,
+                        int64_t gaussian_pair_cap, ges_frame_status_t *status_dev,
+                        void *stream, void *const *events);
+
 /* Pass 1 alone: forward.py:127-209 (rasterize_surfels). */
 int ges_rasterize_surfels(const ges_scene_t *scene, const ges_camera_t *cam,
                           const ges_settings_t *st, const ges_outputs_t *out,
@@ -146,13 +157,19 @@ int ges_smooth_geometry(const float *s_depth, const float *s_normal, const float
                         const float *g_normal, const float *g_weight, float *depth_out,
                         float *normal_out, int64_t n, void *stream);
 
-/* End-to-end with HOST buffers: copies cam batch in, renders each view with
- * ges_render on device-resident scene, copies each view's image (H,W,3 f32)
- * to host_images (pinned recommended).  Used by the e2e benchmark leg. */
+/* End-to-end view batch with HOST buffers (the multi-view caller loop of
+ * metrics.py:60-66 / cli.py:165-168): for each host camera, render on the
+ * device-resident scene and copy the (H,W,3) f32 image into host_images
+ * (pinned memory recommended; all views must share one resolution).
+ * image_dev holds TWO device image buffers (2*H*W*3 floats) so the copy of
+ * view v on copy_stream overlaps the render of view v+1 on stream.  Returns
+ * after enqueueing; synchronise copy_stream before reading host_images.
+ * status_dev: n_views ges_frame_status_t (device) or NULL. */
 int ges_render_views_host(const ges_scene_t *scene, const ges_camera_t *host_cams,
                           int32_t n_views, const ges_settings_t *st, float *host_images,
                           void *workspace, size_t ws_bytes, int64_t surfel_pair_cap,
-                          int64_t gaussian_pair_cap, void *image_dev, void *stream);
+                          int64_t gaussian_pair_cap, void *image_dev,
+                          ges_frame_status_t *status_dev, void *stream, void *copy_stream);
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,7 @@ LAYERS = {"full": 0, "surfels_only": 1, "gaussians_only": 2}
 
 # Every symbol include/ges_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = ("ges_abi_version", "ges_last_error", "ges_scene_bytes", "ges_scene_pack",
-           "ges_workspace_bytes", "ges_render", "ges_rasterize_surfels",
+           "ges_workspace_bytes", "ges_render", "ges_render_profiled", "ges_rasterize_surfels",
            "ges_accumulate_gaussians", "ges_composite", "ges_smooth_geometry",
            "ges_render_views_host")
 
@@ -50,7 +50,8 @@ class Scene(C.Structure):
 
 class Outputs(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("image", "s_color", "s_depth", "s_normal", "s_winner",
-                                          "g_color", "g_weight", "g_depth", "g_normal")]
+                                          "g_color", "g_weight", "g_depth", "g_normal",
+                                          "image_rgba8")]
 
 
 class FrameStatus(C.Structure):
@@ -79,6 +80,9 @@ def lib():
         "ges_workspace_bytes": (C.c_size_t, [P(Scene), P(Camera), P(Settings), C.c_int64, C.c_int64]),
         "ges_render": (C.c_int, [P(Scene), P(Camera), P(Settings), P(Outputs), C.c_void_p, C.c_size_t,
                                  C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
+        "ges_render_profiled": (C.c_int, [P(Scene), P(Camera), P(Settings), P(Outputs), C.c_void_p,
+                                          C.c_size_t, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]),
         "ges_rasterize_surfels": (C.c_int, [P(Scene), P(Camera), P(Settings), P(Outputs), C.c_void_p,
                                             C.c_size_t, C.c_int64, C.c_void_p, C.c_void_p]),
         "ges_accumulate_gaussians": (C.c_int, [P(Scene), P(Camera), C.c_void_p, P(Settings), P(Outputs),
@@ -88,7 +92,7 @@ def lib():
         "ges_smooth_geometry": (C.c_int, [C.c_void_p] * 7 + [C.c_int64, C.c_void_p]),
         "ges_render_views_host": (C.c_int, [P(Scene), P(Camera), C.c_int32, P(Settings), C.c_void_p,
                                             C.c_void_p, C.c_size_t, C.c_int64, C.c_int64, C.c_void_p,
-                                            C.c_void_p]),
+                                            C.c_void_p, C.c_void_p, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -104,7 +104,7 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, int64_t
 // mode: 1 surfel pass, 2 Gaussian pass against ds_in, 3 both.
 int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st, const ges_outputs_t* out,
               const float* ds_in, int mode, void* ws, size_t ws_bytes, int64_t cap_s, int64_t cap_g,
-              ges_frame_status_t* status_dev, cudaStream_t s) {
+              ges_frame_status_t* status_dev, cudaStream_t s, void* const* ev = nullptr) {
     int rc;
     if ((rc = check_scene(sc)) || (rc = check_cam(cam)) || (rc = check_settings(st))) return rc;
     if (!out) return fail(GES_EINVAL, "outputs is NULL");
@@ -117,6 +117,10 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     const bool do_s = mode & 1;
     const bool do_g = (mode & 2) && st->layers != GES_LAYERS_SURFELS_ONLY;
     cudaError_t e;
+    auto mark = [&](int k) {
+        if (ev && ev[k]) cudaEventRecord((cudaEvent_t)ev[k], s);
+    };
+    mark(0);
     if ((e = cudaMemsetAsync(f.cnt_s, 0, 2 * sizeof(uint32_t) * (f.ntiles + 1), s)) != cudaSuccess)
         return cuda_fail(e, "memset counts");
     if ((e = cudaMemsetAsync(status, 0, sizeof(ges_frame_status_t), s)) != cudaSuccess)
@@ -128,14 +132,18 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     if (!do_g) scs.n_gaussians = 0;
     if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, f.s_rgb, f.s_nrm, f.cnt_s}, s)))
         return cuda_fail(e, "surfel preprocess");
+    mark(1);
     if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))
         return cuda_fail(e, "gaussian preprocess");
+    mark(2);
     if ((e = launch_scan(f.cnt_s, f.off_s, f.cur_s, f.ntiles, f.cnt_g, f.off_g, f.cur_g, f.ntiles, cap_s, cap_g,
                          status, s)))
         return cuda_fail(e, "tile scan");
+    mark(3);
     if ((e = launch_fill(f.srec, scs.n_surfels, f.cur_s, f.list_s, cap_s, TILE * grid, f.ntx, f.grec,
                          scs.n_gaussians, sc->gaussian_dim, f.cur_g, f.list_g, cap_g, f.ntx, s)))
         return cuda_fail(e, "tile fill");
+    mark(4);
     TileArgs a{};
     a.W = cam->width; a.H = cam->height; a.ntx = f.ntx; a.nty = f.nty;
     a.layers = st->layers;
@@ -156,6 +164,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     }
     if ((e = launch_tile(a, st->supersample, tmode, sc->gaussian_dim, st->with_geometry != 0, s)))
         return cuda_fail(e, "tile kernel");
+    mark(5);
     return GES_OK;
 }
 
@@ -211,6 +220,13 @@ int ges_render(const ges_scene_t* sc, const ges_camera_t* cam, const ges_setting
     return run_frame(sc, cam, st, out, nullptr, 3, ws, ws_bytes, cap_s, cap_g, status_dev, (cudaStream_t)stream);
 }
 
+int ges_render_profiled(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st,
+                        const ges_outputs_t* out, void* ws, size_t ws_bytes, int64_t cap_s, int64_t cap_g,
+                        ges_frame_status_t* status_dev, void* stream, void* const* events) {
+    return run_frame(sc, cam, st, out, nullptr, 3, ws, ws_bytes, cap_s, cap_g, status_dev, (cudaStream_t)stream,
+                     events);
+}
+
 int ges_rasterize_surfels(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st,
                           const ges_outputs_t* out, void* ws, size_t ws_bytes, int64_t cap_s,
                           ges_frame_status_t* status_dev, void* stream) {
@@ -244,22 +260,46 @@ int ges_smooth_geometry(const float* sd, const float* sn, const float* gd, const
 
 int ges_render_views_host(const ges_scene_t* sc, const ges_camera_t* host_cams, int32_t n_views,
                           const ges_settings_t* st, float* host_images, void* ws, size_t ws_bytes, int64_t cap_s,
-                          int64_t cap_g, void* image_dev, void* stream) {
-    if (!host_cams || !host_images || !image_dev || n_views < 0) return fail(GES_EINVAL, "bad view batch arguments");
-    cudaStream_t s = (cudaStream_t)stream;
-    size_t off = 0;
-    for (int v = 0; v < n_views; ++v) {
-        ges_outputs_t out{};
-        out.image = static_cast<float*>(image_dev);
-        int rc = ges_render(sc, &host_cams[v], st, &out, ws, ws_bytes, cap_s, cap_g, nullptr, stream);
-        if (rc) return rc;
-        size_t bytes = (size_t)host_cams[v].width * host_cams[v].height * 3 * sizeof(float);
-        cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(host_images) + off, image_dev, bytes,
-                                        cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) return cuda_fail(e, "image copy");
-        off += bytes;
+                          int64_t cap_g, void* image_dev, ges_frame_status_t* status_dev, void* stream,
+                          void* copy_stream) {
+    if (!host_cams || !host_images || !image_dev || n_views < 0 || !copy_stream)
+        return fail(GES_EINVAL, "bad view batch arguments");
+    if (n_views == 0) return GES_OK;
+    for (int v = 1; v < n_views; ++v)
+        if (host_cams[v].width != host_cams[0].width || host_cams[v].height != host_cams[0].height)
+            return fail(GES_EINVAL, "all views of a batch must share one resolution");
+    cudaStream_t s = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
+    const size_t px = (size_t)host_cams[0].width * host_cams[0].height;
+    const size_t bytes = px * 3 * sizeof(float);
+    cudaEvent_t rendered[2], copied[2];
+    for (int k = 0; k < 2; ++k) {
+        cudaEventCreateWithFlags(&rendered[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
     }
-    return GES_OK;
+    int rc = GES_OK;
+    for (int v = 0; v < n_views && rc == GES_OK; ++v) {
+        const int b = v & 1;
+        float* buf = static_cast<float*>(image_dev) + b * px * 3;
+        if (v >= 2) cudaStreamWaitEvent(s, copied[b], 0);   // buffer b free again
+        ges_outputs_t out{};
+        out.image = buf;
+        rc = ges_render(sc, &host_cams[v], st, &out, ws, ws_bytes, cap_s, cap_g,
+                        status_dev ? status_dev + v : nullptr, stream);
+        if (rc) break;
+        cudaEventRecord(rendered[b], s);
+        cudaStreamWaitEvent(cs, rendered[b], 0);
+        cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(host_images) + v * bytes, buf, bytes,
+                                        cudaMemcpyDeviceToHost, cs);
+        if (e != cudaSuccess) rc = cuda_fail(e, "image copy");
+        cudaEventRecord(copied[b], cs);
+    }
+    cudaStreamWaitEvent(s, copied[0], 0);   // later work on `stream` may reuse image_dev
+    cudaStreamWaitEvent(s, copied[1], 0);
+    for (int k = 0; k < 2; ++k) {           // destroy is deferred by the driver until complete
+        cudaEventDestroy(rendered[k]);
+        cudaEventDestroy(copied[k]);
+    }
+    return rc;
 }
 
 }  // extern "C"

@@ -91,6 +91,25 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// Layer-selected final colour (forward.py:384-388, :412-417).
+__device__ __forceinline__ float3 im_of(const TileArgs& a, float3 cs, float w, float cr, float cg, float cb) {
+    if (a.layers == GES_LAYERS_GAUSSIANS_ONLY) {
+        if (w > 0.f) {
+            float dn = fmaxf(w, 1e-12f);
+            return make_float3(cr / dn, cg / dn, cb / dn);
+        }
+        return make_float3(a.bg[0], a.bg[1], a.bg[2]);
+    }
+    float dn = 1.0f + w;
+    return make_float3((cs.x + cr) / dn, (cs.y + cg) / dn, (cs.z + cb) / dn);
+}
+
+// Display/send-buffer form, datasets.py:54-56: clip(x*255+0.5, 0, 255) -> u8.
+__device__ __forceinline__ void store_rgba8(uint8_t* dst, int64_t pix, float3 c) {
+    auto q = [](float v) -> uint32_t { return (uint32_t)fminf(fmaxf(v * 255.0f + 0.5f, 0.f), 255.f); };
+    reinterpret_cast<uint32_t*>(dst)[pix] = q(c.x) | (q(c.y) << 8) | (q(c.z) << 16) | (255u << 24);
+}
+
 template <int SS, int MODE, int GK, bool GEOM>
 __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
     __shared__ TileSmem sm;
@@ -318,22 +337,13 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                 }
             }
             if (a.out.image) {
-                float3 im;
-                if (a.layers == GES_LAYERS_GAUSSIANS_ONLY) {   // forward.py:412-416
-                    if (wsum > 0.f) {
-                        float dn = fmaxf(wsum, 1e-12f);
-                        im = make_float3(cr / dn, cg / dn, cb / dn);
-                    } else {
-                        im = make_float3(a.bg[0], a.bg[1], a.bg[2]);
-                    }
-                } else {                                       // composite, forward.py:384-388
-                    float dn = 1.0f + wsum;
-                    im = make_float3((cs.x + cr) / dn, (cs.y + cg) / dn, (cs.z + cb) / dn);
-                }
+                const float3 im = im_of(a, cs, wsum, cr, cg, cb);
                 a.out.image[3 * pix] = im.x; a.out.image[3 * pix + 1] = im.y; a.out.image[3 * pix + 2] = im.z;
             }
+            if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, im_of(a, cs, wsum, cr, cg, cb));
         }
     } else if (inside) {   // surfels_only (forward.py:407-410): empty Gaussian buffers
+        if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, cs);
         if (a.out.image) {
             a.out.image[3 * pix] = cs.x; a.out.image[3 * pix + 1] = cs.y; a.out.image[3 * pix + 2] = cs.z;
         }

@@ -1,0 +1,69 @@
+"""Multi-view batches and their distribution over GPUs.
+
+Views are independent units (``render`` is a pure function of scene and
+camera, forward.py:403); the reference's multi-view callers loop over them
+(metrics.py:60-66, cli.py:165-168).  Here each rank holds a full scene
+replica, renders a contiguous block of views, and the only inter-GPU
+traffic is one frame gather to the destination rank over NCCL (NVLink),
+of RGBA8 frames the tile kernel writes straight into the send buffer.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+
+def shard(n_views: int, rank: int, world: int) -> range:
+    """Contiguous block of ceil(n/world) views for ``rank``."""
+    per = math.ceil(n_views / world) if world else 0
+    lo = min(n_views, rank * per)
+    return range(lo, min(n_views, lo + per))
+
+
+def gather_frames(local: torch.Tensor, dst: int = 0, group=None):
+    """Gather equally-shaped per-rank frame batches (V, H, W, C) to ``dst``.
+    Returns the (world*V, H, W, C) batch on ``dst`` and None elsewhere."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return local
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if rank == dst:
+        out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+        dist.gather(local.contiguous(), gather_list=list(out.unbind(0)), dst=dst, group=group)
+        return out.reshape((world * local.shape[0],) + tuple(local.shape[1:]))
+    dist.gather(local.contiguous(), gather_list=None, dst=dst, group=group)
+    return None
+
+
+class ViewBatchRenderer:
+    """Renders a batch of same-resolution views of one packed scene into a
+    preallocated (V, H, W, 4) RGBA8 send buffer (plus optional fp32 images,
+    depth and winner maps), asynchronously on the current stream."""
+
+    def __init__(self, renderer, scene, cams, settings, *, want=("image_rgba8",)):
+        self.r = renderer
+        self.scene = scene
+        self.cams = list(cams)
+        self.settings = settings
+        H, W = int(self.cams[0].height), int(self.cams[0].width)
+        if any((int(c.height), int(c.width)) != (H, W) for c in self.cams):
+            raise ValueError("a view batch must share one resolution")
+        dev = renderer.device
+        self.rgba = torch.empty((len(self.cams), H, W, 4), dtype=torch.uint8, device=dev)
+        self.frames = []
+        for v, c in enumerate(self.cams):
+            fr = renderer.alloc(c, settings, want=[k for k in want if k != "image_rgba8"])
+            fr.image_rgba8 = self.rgba[v]
+            self.frames.append(fr)
+
+    def render(self, check: bool = False):
+        for c, fr in zip(self.cams, self.frames):
+            self.r.render(self.scene, c, self.settings, frame=fr, check=check)
+        return self.rgba
+
+    def overflowed(self) -> bool:
+        st = torch.stack([f.status for f in self.frames]).cpu()
+        return bool(((st[:, 2] & 0xFFFFFFFF) != 0).any())

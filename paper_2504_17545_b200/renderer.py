@@ -171,6 +171,7 @@ class Frame:
     g_weight: torch.Tensor = None
     g_depth: torch.Tensor = None
     g_normal: torch.Tensor = None
+    image_rgba8: torch.Tensor = None
     status: torch.Tensor = None
 
     def pairs(self):
@@ -180,6 +181,7 @@ class Frame:
 
 _ALL = ("image", "s_color", "s_depth", "s_normal", "s_winner", "g_color", "g_weight", "g_depth",
         "g_normal")
+_OUT_FIELDS = _ALL + ("image_rgba8",)
 
 
 class Renderer:
@@ -219,6 +221,8 @@ class Renderer:
         for k in want:
             if k == "s_winner":
                 fr.s_winner = torch.empty((H, W), dtype=torch.int32, device=self.device)
+            elif k == "image_rgba8":
+                fr.image_rgba8 = torch.empty((H, W, 4), dtype=torch.uint8, device=self.device)
             elif k in ("g_depth", "g_normal") and not settings.with_geometry:
                 continue
             else:
@@ -228,7 +232,7 @@ class Renderer:
     @staticmethod
     def _outputs(fr: Frame) -> _lib.Outputs:
         o = _lib.Outputs()
-        for k in _ALL:
+        for k in _OUT_FIELDS:
             t = getattr(fr, k)
             setattr(o, k, t.data_ptr() if t is not None else None)
         return o
