@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ges", choices=["ges", "reference"])
     p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])

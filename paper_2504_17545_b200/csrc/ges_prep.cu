@@ -185,7 +185,10 @@ __global__ void __launch_bounds__(256) k_surfel_prep(ges_scene_t sc, CamK cam, G
     if (alive) alive = disc_ranges(q, scl(a1, s1 * R_OPAQUE), scl(a2, s2 * R_OPAQUE), cam, x0, x1, y0, y1);
     if (alive) {
         planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
+        // nearest camera depth of the disc, made conservative against the float32
+        // evaluation of the per-pixel hit depth (used only to skip surfels)
         double zmin = q.z - R_OPAQUE * sqrt(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z);
+        zmin -= 1e-5 * fabs(zmin) + 1e-6;
         rec.r3 = make_float4((float)zmin, __uint_as_float(pack_span(x0, x1)),
                              __uint_as_float(pack_span(y0, y1)), 0.f);
         count_tiles(o.tile_count, g, x0, x1, y0, y1);

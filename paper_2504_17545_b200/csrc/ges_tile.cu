@@ -128,8 +128,10 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
     // ------------------------------------------------------------ pass 1
     if constexpr (MODE & 1) {
         constexpr int NS = SS * SS;
+        // best[s]: packed (t_bits << 32 | id) of the nearest hit so far; tb[s]: its t
+        // (pixels outside the image start at 0 so they never take work or block culling)
         unsigned long long best[NS];
-        float lxf[SS], lyf[SS], pe[NS];
+        float tb[NS], lxf[SS], lyf[SS], pe[NS];
 #pragma unroll
         for (int s = 0; s < SS; ++s) {
             lxf[s] = (float)(SS * plx + s);
@@ -143,7 +145,17 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                 float dxn = (float)((X + 0.5 - a.rcx) / a.rfx), dyn = (float)((Y + 0.5 - a.rcy) / a.rfy);
                 pe[sy * SS + sx] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
                 best[sy * SS + sx] = ~0ull;
+                tb[sy * SS + sx] = inside ? INFINITY : 0.f;
             }
+        auto patch_depth = [&]() {
+            float m = tb[0];
+#pragma unroll
+            for (int s = 1; s < NS; ++s) m = fmaxf(m, tb[s]);
+            return warp_max(m);
+        };
+        float wmx = INFINITY;          // max over this warp's (sub)pixels of the best depth
+        if (lane == 0) sm.wmax[warp] = INFINITY;
+        __syncthreads();
         const int ox = tx * TILE * SS, oy = ty * TILE * SS;
         const uint32_t beg = a.s_off[tile], end = a.s_off[tile + 1];
         for (uint32_t base = beg; base < end; base += NB) {
@@ -160,35 +172,51 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                 uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
                 mask = patch_mask<SS>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
                                       span_hi(syr) - oy);
-                sm.st[0][threadIdx.x] = make_float4(d0, r0.y, r0.z, r0.w);
+                // hit depth t = nq / den: orient den so that t > 0 <=> den > 0
+                float nq = r0.w, dx_ = r0.y, dy_ = r0.z;
+                if (nq < 0.f) { nq = -nq; d0 = -d0; dx_ = -dx_; dy_ = -dy_; }
+                if (!(nq > 0.f)) mask = 0;
+#pragma unroll
+                for (int w = 0; w < NWARP; ++w)   // already hidden behind warp w's surface
+                    if (r3.x > sm.wmax[w]) mask &= ~(1u << w);
+                sm.st[0][threadIdx.x] = make_float4(d0, dx_, dy_, nq);
                 sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
                 sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, __uint_as_float(id), r3.x);
             }
             build_lists(sm, mask, warp, lane);
             const int L = sm.tot[warp];
             for (int k = 0; k < L; ++k) {
+                if ((k & 7) == 0) wmx = patch_depth();
                 const int j = sm.wl[warp][k];
-                const float4 A = sm.st[0][j], B = sm.st[1][j], C = sm.st[2][j];
-                const unsigned long long idk = __float_as_uint(C.z);
+                const float4 C = sm.st[2][j];
+                if (C.w > wmx) continue;   // disc entirely behind every pixel's current hit
+                const float4 A = sm.st[0][j], B = sm.st[1][j];
 #pragma unroll
                 for (int sy = 0; sy < SS; ++sy)
 #pragma unroll
                     for (int sx = 0; sx < SS; ++sx) {
+                        const int s = sy * SS + sx;
                         const float lx = lxf[sx], ly = lyf[sy];
                         const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
                         const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
                         const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
                         const float r2 = fmaf(U, U, V * V);
-                        if (r2 <= R2_F * den * den && fabsf(den) > pe[sy * SS + sx]) {
-                            const float t = __fdividef(A.w, den);
-                            if (t > NEAR_F) {
-                                unsigned long long key =
-                                    ((unsigned long long)__float_as_uint(t) << 32) | idk;
-                                best[sy * SS + sx] = key < best[sy * SS + sx] ? key : best[sy * SS + sx];
+                        // coverage u^2+v^2 <= R^2, |n.d| > eps|d|, t > 0.01, and t no
+                        // later than the current best (multiplied out; exact key below)
+                        if (den > pe[s] && r2 <= R2_F * den * den && A.w > NEAR_F * den &&
+                            A.w <= tb[s] * 1.00001f * den) {
+                            const float t = A.w / den;
+                            const unsigned long long key =
+                                ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
+                            if (t > NEAR_F && key < best[s]) {
+                                best[s] = key;
+                                tb[s] = t;
                             }
                         }
                     }
             }
+            wmx = patch_depth();
+            if (lane == 0) sm.wmax[warp] = wmx;
             __syncthreads();
         }
         // resolve: depth/normal/winner from sub-sample 0, colour = box mean
