@@ -58,13 +58,23 @@ typedef struct ges_settings {
 } ges_settings_t;
 
 /* Source scene in the reference's storage layout (primitives.py:42-161),
- * float64 device arrays, row-major.  g_filter3d may be NULL (all zero). */
+ * float64 device arrays, row-major.  g_filter3d may be NULL (all zero).
+ * s_order / g_order (int32, may be NULL = identity) give the storage order of
+ * the packed scene: packed primitive i is source primitive order[i].  A
+ * spatially coherent order (the package uses a 3D Morton order) makes the
+ * per-frame binning atomics aggregate per warp; results do not depend on it
+ * (surfel ids reported and used for z-buffer tie-breaks are SOURCE ids). */
 typedef struct ges_scene_src {
     int64_t n_surfels, n_gaussians;
     int32_t sh_degree;        /* 0..3 */
     int32_t gaussian_dim;     /* 3 = GaussianKind.THREE_D, 2 = TWO_D */
     const double *s_pos, *s_quat, *s_log_scale, *s_sh;
     const double *g_pos, *g_raw_opacity, *g_quat, *g_log_scale, *g_sh, *g_filter3d;
+    const int32_t *s_order, *g_order;
+    /* Bounding box of all primitive centres (xmin, ymin, zmin, xmax, ymax,
+     * zmax) and the largest primitive radius; only sets the per-view depth
+     * range of the binning slabs (all zero: one slab, still exact). */
+    double bounds[7];
 } ges_scene_src_t;
 
 /* Packed device scene (float32, 16-byte aligned SoA).  Filled by
@@ -76,10 +86,12 @@ typedef struct ges_scene {
     float *s_quat;        /* n_surfels x 4: unit (w, x, y, z)                  */
     float *s_s2;          /* n_surfels:     exp(log_scale[1])                  */
     float *s_sh;          /* n_surfels x K x 3                                 */
+    int32_t *s_id;        /* n_surfels: source index of packed surfel i        */
     float *g_pos_op;      /* n_gaussians x 4: pos.xyz, eff_opacity             */
     float *g_quat;        /* n_gaussians x 4                                   */
     float *g_scale_eps;   /* n_gaussians x 4: eff_scale (s2=0 for 2D), epsilon */
     float *g_sh;          /* n_gaussians x K x 3                               */
+    double bounds[7];     /* copied from ges_scene_src_t::bounds               */
 } ges_scene_t;
 
 /* Output buffers; any may be NULL (not written).  H, W = base resolution.

@@ -38,14 +38,15 @@ class SceneSrc(C.Structure):
     _fields_ = [("n_surfels", C.c_int64), ("n_gaussians", C.c_int64), ("sh_degree", C.c_int32),
                 ("gaussian_dim", C.c_int32)] + [
         (n, C.c_void_p) for n in ("s_pos", "s_quat", "s_log_scale", "s_sh", "g_pos",
-                                  "g_raw_opacity", "g_quat", "g_log_scale", "g_sh", "g_filter3d")]
+                                  "g_raw_opacity", "g_quat", "g_log_scale", "g_sh", "g_filter3d",
+                                  "s_order", "g_order")] + [("bounds", C.c_double * 7)]
 
 
 class Scene(C.Structure):
     _fields_ = [("n_surfels", C.c_int64), ("n_gaussians", C.c_int64), ("sh_degree", C.c_int32),
                 ("gaussian_dim", C.c_int32)] + [
-        (n, C.c_void_p) for n in ("s_pos_s1", "s_quat", "s_s2", "s_sh", "g_pos_op", "g_quat",
-                                  "g_scale_eps", "g_sh")]
+        (n, C.c_void_p) for n in ("s_pos_s1", "s_quat", "s_s2", "s_sh", "s_id", "g_pos_op", "g_quat",
+                                  "g_scale_eps", "g_sh")] + [("bounds", C.c_double * 7)]
 
 
 class Outputs(C.Structure):

@@ -69,7 +69,8 @@ struct Frame {
     float4 *s_rgb, *s_nrm;
     void* grec;
     float4* g_nrm;
-    uint32_t *cnt_s, *off_s, *cur_s, *cnt_g, *off_g, *cur_g;
+    uint32_t *cnt_s, *off_s, *cnt_g, *off_g, *chunk_s, *chunk_g, *tickets;
+    size_t zero_bytes;   // counters + tickets, cleared by one memset per frame
     uint32_t *list_s, *list_g;
     ges_frame_status_t* status;
     size_t bytes;
@@ -84,12 +85,16 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, int64_t
     f.ntiles = f.ntx * f.nty;
     size_t ns = (size_t)sc->n_surfels, ng = (size_t)sc->n_gaussians;
     f.status = c.take<ges_frame_status_t>(1);
-    f.cnt_s = c.take<uint32_t>(2 * (size_t)(f.ntiles + 1));   // counts for both passes: one memset
-    f.cnt_g = f.cnt_s ? f.cnt_s + (f.ntiles + 1) : nullptr;
-    f.off_s = c.take<uint32_t>(f.ntiles + 1);
-    f.cur_s = c.take<uint32_t>(f.ntiles + 1);
-    f.off_g = c.take<uint32_t>(f.ntiles + 1);
-    f.cur_g = c.take<uint32_t>(f.ntiles + 1);
+    const size_t nbins = (size_t)f.ntiles * NSLAB;   // both passes' counters + tickets: one memset
+    f.cnt_s = c.take<uint32_t>(2 * nbins + 64);
+    f.cnt_g = f.cnt_s ? f.cnt_s + nbins : nullptr;
+    f.tickets = f.cnt_s ? f.cnt_s + 2 * nbins : nullptr;
+    f.zero_bytes = (2 * nbins + 64) * sizeof(uint32_t);
+    const size_t nchunk = (size_t)(f.ntiles + 255) / 256 + 1;
+    f.off_s = c.take<uint32_t>(f.ntiles);
+    f.off_g = c.take<uint32_t>(f.ntiles);
+    f.chunk_s = c.take<uint32_t>(nchunk);
+    f.chunk_g = c.take<uint32_t>(nchunk);
     f.srec = c.take<SurfRec>(ns);
     f.s_rgb = c.take<float4>(ns);
     f.s_nrm = c.take<float4>(ns);
@@ -99,6 +104,31 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, int64_t
     f.list_g = c.take<uint32_t>((size_t)cap_g);
     f.bytes = c.off;
     return f;
+}
+
+// Depth range of the binning slabs for one view: camera z of the scene's
+// bounding-box corners widened by the largest primitive radius.
+SlabMap slab_map(const ges_scene_t& sc, const CamK& c) {
+    const double* b = sc.bounds;
+    double zlo = 1e300, zhi = -1e300;
+    for (int k = 0; k < 8; ++k) {
+        double p[3] = {b[(k & 1) ? 3 : 0], b[(k & 2) ? 4 : 1], b[(k & 4) ? 5 : 2]};
+        double z = c.R[6] * p[0] + c.R[7] * p[1] + c.R[8] * p[2] + c.t[2];
+        zlo = z < zlo ? z : zlo;
+        zhi = z > zhi ? z : zhi;
+    }
+    zlo = zlo - b[6];
+    zhi = zhi + b[6];
+    if (zlo < NEAR) zlo = NEAR;
+    SlabMap m;
+    if (!(zhi > zlo + 1e-9)) {   // degenerate or missing bounds: everything in slab 0
+        m.zlo = 0.f;
+        m.inv_dz = 0.f;
+    } else {
+        m.zlo = (float)zlo;
+        m.inv_dz = (float)(NSLAB / (zhi - zlo));
+    }
+    return m;
 }
 
 // mode: 1 surfel pass, 2 Gaussian pass against ds_in, 3 both.
@@ -121,27 +151,27 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
         if (ev && ev[k]) cudaEventRecord((cudaEvent_t)ev[k], s);
     };
     mark(0);
-    if ((e = cudaMemsetAsync(f.cnt_s, 0, 2 * sizeof(uint32_t) * (f.ntiles + 1), s)) != cudaSuccess)
-        return cuda_fail(e, "memset counts");
+    if ((e = cudaMemsetAsync(f.cnt_s, 0, f.zero_bytes, s)) != cudaSuccess) return cuda_fail(e, "memset counts");
     if ((e = cudaMemsetAsync(status, 0, sizeof(ges_frame_status_t), s)) != cudaSuccess)
         return cuda_fail(e, "memset status");
     CamK cs = make_cam(*cam, grid), cg = make_cam(*cam, 1);
-    Grid gs{cs.W, cs.H, TILE * grid, f.ntx, f.nty}, gg{cg.W, cg.H, TILE, f.ntx, f.nty};
+    const SlabMap slabs = slab_map(*sc, cs);
+    Grid gs{cs.W, cs.H, TILE * grid, f.ntx, f.nty, slabs}, gg{cg.W, cg.H, TILE, f.ntx, f.nty, slabs};
     ges_scene_t scs = *sc;
     if (!do_s) scs.n_surfels = 0;
     if (!do_g) scs.n_gaussians = 0;
+    const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, TILE * grid};
+    const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE};
     if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, f.s_rgb, f.s_nrm, f.cnt_s}, s)))
         return cuda_fail(e, "surfel preprocess");
     mark(1);
     if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))
         return cuda_fail(e, "gaussian preprocess");
     mark(2);
-    if ((e = launch_scan(f.cnt_s, f.off_s, f.cur_s, f.ntiles, f.cnt_g, f.off_g, f.cur_g, f.ntiles, cap_s, cap_g,
-                         status, s)))
+    if ((e = launch_scan(bs, bg, status, s)))
         return cuda_fail(e, "tile scan");
     mark(3);
-    if ((e = launch_fill(f.srec, scs.n_surfels, f.cur_s, f.list_s, cap_s, TILE * grid, f.ntx, f.grec,
-                         scs.n_gaussians, sc->gaussian_dim, f.cur_g, f.list_g, cap_g, f.ntx, s)))
+    if ((e = launch_fill(f.srec, scs.n_surfels, bs, f.grec, scs.n_gaussians, sc->gaussian_dim, bg, slabs, s)))
         return cuda_fail(e, "tile fill");
     mark(4);
     TileArgs a{};
@@ -149,9 +179,10 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     a.layers = st->layers;
     for (int i = 0; i < 3; ++i) a.bg[i] = st->background[i];
     a.rfx = cs.fx; a.rfy = cs.fy; a.rcx = cs.cx; a.rcy = cs.cy;
-    a.srec = f.srec; a.s_rgb = f.s_rgb; a.s_nrm = f.s_nrm; a.s_list = f.list_s; a.s_off = f.off_s;
+    a.srec = f.srec; a.s_rgb = f.s_rgb; a.s_nrm = f.s_nrm; a.s_list = f.list_s; a.sbin = bs;
+    a.slabs = slabs;
     a.gfx = cg.fx; a.gfy = cg.fy; a.gcx = cg.cx; a.gcy = cg.cy;
-    a.grec = f.grec; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.g_off = f.off_g;
+    a.grec = f.grec; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg;
     a.ds_in = ds_in;
     a.out = *out;
     a.status = status;
@@ -179,7 +210,8 @@ const char* ges_last_error(void) { return g_err.c_str(); }
 size_t ges_scene_bytes(int64_t ns, int64_t ng, int32_t deg) {
     if (deg < 0 || deg > 3 || ns < 0 || ng < 0) return 0;
     size_t K = (size_t)(deg + 1) * (deg + 1);
-    return al(ns * 16) + al(ns * 16) + al(ns * 4) + al(ns * K * 12) + al(ng * 16) * 3 + al(ng * K * 12);
+    return al(ns * 16) + al(ns * 16) + al(ns * 4) + al(ns * K * 12) + al(ns * 4) + al(ng * 16) * 3 +
+           al(ng * K * 12);
 }
 
 int ges_scene_pack(const ges_scene_src_t* src, void* blob, size_t blob_bytes, ges_scene_t* out, void* stream) {
@@ -198,6 +230,8 @@ int ges_scene_pack(const ges_scene_src_t* src, void* blob, size_t blob_bytes, ge
     sc.s_quat = c.take<float>(ns * 4);
     sc.s_s2 = c.take<float>(ns);
     sc.s_sh = c.take<float>(ns * K * 3);
+    sc.s_id = c.take<int32_t>(ns);
+    for (int k = 0; k < 7; ++k) sc.bounds[k] = src->bounds[k];
     sc.g_pos_op = c.take<float>(ng * 4);
     sc.g_quat = c.take<float>(ng * 4);
     sc.g_scale_eps = c.take<float>(ng * 4);

@@ -1,101 +1,159 @@
 // Sort-free tile binning, steps 2 and 3 (step 1, the count, is fused into the
-// preprocess kernels): exclusive prefix sum over the per-tile counts, then a
-// fill pass that appends each primitive id to every tile its pixel range
-// overlaps.  Replaces the per-tile O(N) selection scan of the reference
-// (forward.py:168-169, :294-295) -- the reference's dominant CPU cost.
+// preprocess kernels).  Replaces the per-tile O(N) selection scan of the
+// reference (forward.py:168-169, :294-295) -- the reference's dominant CPU cost.
+//
+// Bins are (tile, depth slab) pairs: every primitive is counted into the
+// NSLAB slab of its conservative depth key in each tile it overlaps.  Within a
+// tile the slabs are laid out near to far, so the tile kernel meets near
+// primitives first (its depth culling then rejects most of the rest) and can
+// stop at the first slab that lies behind everything already drawn.  Results
+// never depend on the order (min over packed keys / order-independent sums).
+//
+//   count (prep) -> k_scan: per-tile slab prefix + prefix sum over tiles
+//                -> k_fill: append ids, one atomic per (warp, bin) group
 #include <cub/block/block_scan.cuh>
 
 #include "ges_launch.h"
 
 namespace ges {
 
-constexpr int SCAN_T = 1024;
+constexpr int SCAN_T = 256;   // tiles per scan block (one thread per tile)
 
-// Block b of the grid scans array b (0 = surfel tiles, 1 = Gaussian tiles).
-__global__ void __launch_bounds__(SCAN_T) k_scan(uint32_t* cnt_s, uint32_t* off_s, uint32_t* cur_s, int n_s,
-                                                 uint32_t* cnt_g, uint32_t* off_g, uint32_t* cur_g, int n_g,
-                                                 int64_t cap_s, int64_t cap_g, ges_frame_status_t* st) {
+// Grid (nchunks, 2): y selects the pass (0 = surfels, 1 = Gaussians).  Each
+// block turns its tiles' slab counts into slab prefixes (the fill cursors)
+// and writes the block-local exclusive prefix of the tile totals; the last
+// block of a pass to finish scans the chunk totals into chunk bases, so
+// tile_off(t) = chunk_base[t / SCAN_T] + local_off[t].  One launch, no host
+// sync; the ticket is reset with the per-frame counter memset.
+__global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_frame_status_t* st) {
     using Scan = cub::BlockScan<uint32_t, SCAN_T>;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ uint32_t carry;
-    uint32_t* cnt = blockIdx.x ? cnt_g : cnt_s;
-    uint32_t* off = blockIdx.x ? off_g : off_s;
-    uint32_t* cur = blockIdx.x ? cur_g : cur_s;
-    int n = blockIdx.x ? n_g : n_s;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < n; base += SCAN_T) {
-        int i = base + threadIdx.x;
-        uint32_t v = i < n ? cnt[i] : 0u, ex, tot;
-        Scan(tmp).ExclusiveSum(v, ex, tot);
-        uint32_t c = carry;
-        if (i < n) {
-            off[i] = c + ex;
-            cur[i] = c + ex;
+    __shared__ bool last;
+    const BinPass& p = blockIdx.y ? p1 : p0;
+    const int n = p.ntiles;
+    const int t = blockIdx.x * SCAN_T + threadIdx.x;
+    uint32_t tot = 0;
+    if (t < n) {
+        uint4* c = reinterpret_cast<uint4*>(p.cnt + (size_t)t * NSLAB);
+        const uint4 a = c[0], b = c[1];
+        uint32_t v[NSLAB] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int s = 0; s < NSLAB; ++s) {
+            const uint32_t x = v[s];
+            v[s] = tot;
+            tot += x;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) carry = c + tot;
-        __syncthreads();
+        c[0] = make_uint4(v[0], v[1], v[2], v[3]);
+        c[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    }
+    uint32_t ex, blk;
+    Scan(tmp).ExclusiveSum(tot, ex, blk);
+    if (t < n) p.off[t] = ex;
+    if (threadIdx.x == 0) {
+        p.chunk[blockIdx.x] = blk;
+        __threadfence();
+        last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // last block: exclusive scan of the chunk totals (<= SCAN_T * 8 chunks)
+    const int nc = gridDim.x;
+    const int per = (nc + SCAN_T - 1) / SCAN_T;
+    uint32_t run = 0;
+    uint32_t vals[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x * per + k;
+        vals[k] = (k < per && i < nc) ? *((volatile uint32_t*)p.chunk + i) : 0u;
+        run += vals[k];
+    }
+    uint32_t base, total;
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(run, base, total);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x * per + k;
+        if (k < per && i < nc) {
+            p.chunk[i] = base;
+            base += vals[k];
+        }
     }
     if (threadIdx.x == 0) {
-        off[n] = carry;
-        int64_t cap = blockIdx.x ? cap_g : cap_s;
-        if (blockIdx.x) st->gaussian_pairs = carry; else st->surfel_pairs = carry;
-        if ((int64_t)carry > cap) atomicOr(&st->overflow, 1);
+        p.chunk[nc] = total;
+        if (blockIdx.y) st->gaussian_pairs = total; else st->surfel_pairs = total;
+        if ((int64_t)total > p.cap) atomicOr(&st->overflow, 1);
     }
 }
 
-cudaError_t launch_scan(uint32_t* counts_s, uint32_t* off_s, uint32_t* cur_s, int ntiles_s,
-                        uint32_t* counts_g, uint32_t* off_g, uint32_t* cur_g, int ntiles_g,
-                        int64_t cap_s, int64_t cap_g, ges_frame_status_t* status, cudaStream_t s) {
-    k_scan<<<2, SCAN_T, 0, s>>>(counts_s, off_s, cur_s, ntiles_s, counts_g, off_g, cur_g, ntiles_g, cap_s,
-                                cap_g, status);
+cudaError_t launch_scan(const BinPass& s, const BinPass& g, ges_frame_status_t* status, cudaStream_t st) {
+    const int nc = (s.ntiles + SCAN_T - 1) / SCAN_T;
+    if (nc > SCAN_T * 8) return cudaErrorInvalidValue;   // > 524288 tiles
+    k_scan<<<dim3(nc, 2), SCAN_T, 0, st>>>(s, g, status);
     return cudaGetLastError();
 }
 
-__device__ __forceinline__ void fill_one(uint32_t id, uint32_t sx, uint32_t sy, int tile_px, int ntx,
-                                         uint32_t* cur, uint32_t* list, int64_t cap) {
+// Append `id` to bin (tile, slab) of every tile of its range.  Called by all
+// lanes of a warp whose lanes all belong to the same primitive class; lanes
+// that hit the same bin in the same round reserve their slots with a single
+// atomic.
+__device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, uint32_t sy, int slab,
+                                         const BinPass& p) {
     int x0 = span_lo(sx), x1 = span_hi(sx), y0 = span_lo(sy), y1 = span_hi(sy);
-    if (x1 < x0 || y1 < y0) return;
-    for (int ty = y0 / tile_px; ty <= y1 / tile_px; ++ty)
-        for (int tx = x0 / tile_px; tx <= x1 / tile_px; ++tx) {
-            uint32_t slot = atomicAdd(cur + ty * ntx + tx, 1u);
-            if ((int64_t)slot < cap) list[slot] = id;
+    bool more = live && x1 >= x0 && y1 >= y0;
+    const int tp = p.tile_px;
+    int tx0 = x0 / tp, tx1 = x1 / tp, ty = y0 / tp, ty1 = y1 / tp, tx = tx0;
+    const unsigned lane = threadIdx.x & 31;
+    while (__any_sync(0xffffffffu, more)) {
+        const int tile = ty * p.ntx + tx;
+        const int key = more ? tile * NSLAB + slab : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (more) {
+            const int leader = __ffs(peers) - 1;
+            uint32_t base = 0;
+            if (lane == (unsigned)leader) base = atomicAdd(p.cnt + key, (uint32_t)__popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            const uint32_t slot = p.tile_off(tile) + base + __popc(peers & ((1u << lane) - 1u));
+            if ((int64_t)slot < p.cap) p.list[slot] = id;
+            if (++tx > tx1) { tx = tx0; if (++ty > ty1) more = false; }
         }
-}
-
-// One thread per primitive over the concatenated surfel and Gaussian ranges.
-__global__ void __launch_bounds__(256) k_fill(const SurfRec* __restrict__ srec, int64_t ns, uint32_t* cur_s,
-                                              uint32_t* list_s, int64_t cap_s, int s_tile_px, int s_ntx,
-                                              const float4* __restrict__ grec, int64_t ng, int g_kind,
-                                              uint32_t* cur_g, uint32_t* list_g, int64_t cap_g, int g_ntx) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < ns) {
-        float4 r3 = __ldg(&srec[i].r3);
-        fill_one((uint32_t)i, __float_as_uint(r3.y), __float_as_uint(r3.z), s_tile_px, s_ntx, cur_s, list_s,
-                 cap_s);
-    } else if (i < ns + ng) {
-        int64_t j = i - ns;
-        uint32_t sx, sy;
-        if (g_kind == 2) {   // Gauss2Rec: r3 = (sigma, eps, rect_x, rect_y)
-            float4 r3 = __ldg(grec + j * 5 + 3);
-            sx = __float_as_uint(r3.z); sy = __float_as_uint(r3.w);
-        } else {             // GaussRec: r2.w = rect_x, r3.x = rect_y
-            sx = __float_as_uint(__ldg(grec + j * 4 + 2).w);
-            sy = __float_as_uint(__ldg(grec + j * 4 + 3).x);
-        }
-        fill_one((uint32_t)j, sx, sy, TILE, g_ntx, cur_g, list_g, cap_g);
     }
 }
 
-cudaError_t launch_fill(const void* srec, int64_t ns, uint32_t* cur_s, uint32_t* list_s, int64_t cap_s,
-                        int s_tile_px, int s_ntx, const void* grec, int64_t ng, int g_kind,
-                        uint32_t* cur_g, uint32_t* list_g, int64_t cap_g, int g_ntx, cudaStream_t s) {
-    int64_t n = ns + ng;
-    if (n == 0) return cudaSuccess;
-    k_fill<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const SurfRec*)srec, ns, cur_s, list_s, cap_s,
-                                                        s_tile_px, s_ntx, (const float4*)grec, ng, g_kind,
-                                                        cur_g, list_g, cap_g, g_ntx);
+// Surfel blocks first, then Gaussian blocks, so every warp is one class.
+__global__ void __launch_bounds__(256) k_fill(const SurfRec* __restrict__ srec, int64_t ns, BinPass ps,
+                                              const float4* __restrict__ grec, int64_t ng, int g_kind, BinPass pg,
+                                              SlabMap sm) {
+    const int64_t sblocks = (ns + blockDim.x - 1) / blockDim.x;
+    if (blockIdx.x < sblocks) {
+        const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        const bool live = i < ns;
+        const float4 r3 = live ? __ldg(&srec[i].r3) : make_float4(0.f, 0.f, 0.f, 0.f);
+        fill_one(live, (uint32_t)i, __float_as_uint(r3.y), __float_as_uint(r3.z), sm.slab(r3.x), ps);
+    } else {
+        const int64_t j = (blockIdx.x - sblocks) * (int64_t)blockDim.x + threadIdx.x;
+        const bool live = j < ng;
+        uint32_t sx = 0, sy = 0;
+        float key = 0.f;
+        if (live && g_kind == 2) {   // Gauss2Rec: r3 = (sigma, eps, rect_x, rect_y), r5.x = key
+            const float4 r3 = __ldg(grec + j * 6 + 3);
+            sx = __float_as_uint(r3.z); sy = __float_as_uint(r3.w);
+            key = __ldg(grec + j * 6 + 5).x;
+        } else if (live) {           // GaussRec: r2 = (depth, eps, pmin, rect_x), r3.x = rect_y
+            const float4 r2 = __ldg(grec + j * 4 + 2);
+            sx = __float_as_uint(r2.w);
+            sy = __float_as_uint(__ldg(grec + j * 4 + 3).x);
+            key = gauss_key(r2.x, r2.y);
+        }
+        fill_one(live, (uint32_t)j, sx, sy, sm.slab(key), pg);
+    }
+}
+
+cudaError_t launch_fill(const void* srec, int64_t ns, const BinPass& ps, const void* grec, int64_t ng, int g_kind,
+                        const BinPass& pg, const SlabMap& sm, cudaStream_t s) {
+    const int64_t nb = (ns + 255) / 256 + (ng + 255) / 256;
+    if (nb == 0) return cudaSuccess;
+    k_fill<<<(unsigned)nb, 256, 0, s>>>((const SurfRec*)srec, ns, ps, (const float4*)grec, ng, g_kind, pg, sm);
     return cudaGetLastError();
 }
 

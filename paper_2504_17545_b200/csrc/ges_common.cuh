@@ -46,10 +46,44 @@ struct __align__(16) GaussRec {
     float4 r0, r1, r2, r3;
 };
 
-// Per-2D-Gaussian record, 80 B: ray-plane homography like SurfRec plus
-//   r3 = (sigma, eps, rect_x, rect_y), r4 = (r, g, b, zmin)
+// Per-2D-Gaussian record, 96 B: ray-plane homography like SurfRec plus
+//   r3 = (sigma, eps, rect_x, rect_y), r4 = (r, g, b, r2max), r5 = (slab key, 0, 0, 0)
 struct __align__(16) Gauss2Rec {
-    float4 r0, r1, r2, r3, r4;
+    float4 r0, r1, r2, r3, r4, r5;
+};
+
+// Depth slabs of the (tile, slab) bins: NSLAB equal slabs over the view's
+// depth range [zlo, zlo + NSLAB/inv_dz); keys outside clamp to the end slabs.
+constexpr int NSLAB = 8;
+
+struct SlabMap {
+    float zlo, inv_dz;
+    __device__ __forceinline__ int slab(float key) const {
+        float f = floorf((key - zlo) * inv_dz);
+        return f > 0.f ? (f < (float)(NSLAB - 1) ? (int)f : NSLAB - 1) : 0;   // NaN -> 0
+    }
+    // every key binned into slab s is >= this bound (slab 0 also takes keys below zlo)
+    __device__ __forceinline__ float lower(int s) const {
+        if (s == 0 || !(inv_dz > 0.f)) return -INFINITY;
+        float b = zlo + (float)s / inv_dz;
+        return b - (fabsf(b) * 1e-5f + 1e-6f);
+    }
+};
+
+// Slab key of a 3D Gaussian: it can pass the gate d < D_s + eps only where
+// D_s > d - eps (forward.py:310).
+__device__ __forceinline__ float gauss_key(float depth, float eps) { return depth - eps; }
+
+// One binning pass (surfels or Gaussians).
+struct BinPass {
+    uint32_t* cnt;      // ntiles * NSLAB: counts -> slab prefix -> slab ends
+    uint32_t* off;      // ntiles: first list slot of each tile within its scan chunk
+    uint32_t* chunk;    // nchunks + 1: first list slot of each chunk of 256 tiles; [nchunks] = total
+    uint32_t* ticket;   // scan completion counter (zeroed per frame)
+    uint32_t* list;     // cap primitive ids (packed indices)
+    int64_t cap;
+    int ntiles, ntx, tile_px;
+    __device__ __forceinline__ uint32_t tile_off(int t) const { return chunk[t >> 8] + off[t]; }
 };
 
 __device__ __forceinline__ uint32_t pack_span(int lo, int hi) {

@@ -11,12 +11,13 @@ struct PrepOut {
     void* rec;              // SurfRec / GaussRec / Gauss2Rec per primitive
     float4* rgb;            // per-primitive view colour (surfels; Gaussians 3D keep it in rec)
     float4* nrm;            // per-primitive camera-facing normal (surfels; Gaussians if geometry)
-    uint32_t* tile_count;   // per-tile pair counters (zeroed by the caller)
+    uint32_t* bin_count;    // per-(tile, slab) pair counters (zeroed by the caller)
 };
 
 // Tile grid for the pass: ntx x nty tiles of `tile_px` pixels at resolution W x H.
 struct Grid {
     int W, H, tile_px, ntx, nty;
+    SlabMap slabs;
 };
 
 CamK make_cam(const ges_camera_t& c, int scale);
@@ -26,12 +27,9 @@ cudaError_t launch_surfel_prep(const ges_scene_t& sc, const CamK& cam, const Gri
                                const PrepOut& o, cudaStream_t s);
 cudaError_t launch_gauss_prep(const ges_scene_t& sc, const CamK& cam, const Grid& g,
                               const ges_settings_t& st, const PrepOut& o, cudaStream_t s);
-cudaError_t launch_scan(uint32_t* counts_s, uint32_t* off_s, uint32_t* cur_s, int ntiles_s,
-                        uint32_t* counts_g, uint32_t* off_g, uint32_t* cur_g, int ntiles_g,
-                        int64_t cap_s, int64_t cap_g, ges_frame_status_t* status, cudaStream_t s);
-cudaError_t launch_fill(const void* srec, int64_t ns, uint32_t* cur_s, uint32_t* list_s, int64_t cap_s,
-                        int s_tile_px, int s_ntx, const void* grec, int64_t ng, int g_kind,
-                        uint32_t* cur_g, uint32_t* list_g, int64_t cap_g, int g_ntx, cudaStream_t s);
+cudaError_t launch_scan(const BinPass& s, const BinPass& g, ges_frame_status_t* status, cudaStream_t st);
+cudaError_t launch_fill(const void* srec, int64_t ns, const BinPass& ps, const void* grec, int64_t ng, int g_kind,
+                        const BinPass& pg, const SlabMap& sm, cudaStream_t s);
 
 struct TileArgs {
     int W, H, ntx, nty;           // base resolution and 16x16 tile grid
@@ -43,14 +41,15 @@ struct TileArgs {
     const float4* s_rgb;
     const float4* s_nrm;
     const uint32_t* s_list;
-    const uint32_t* s_off;
+    BinPass sbin;                 // tile offsets; cnt = per-(tile, slab) ends relative to the tile
     // Gaussian pass (base resolution)
     double gfx, gfy, gcx, gcy;
     const void* grec;
     const float4* g_rgb;          // 2D Gaussians: colours
     const float4* g_nrm;          // with_geometry normals
     const uint32_t* g_list;
-    const uint32_t* g_off;
+    BinPass gbin;
+    SlabMap slabs;
     const float* ds_in;           // external surfel depth (pass-2-only entry)
     ges_outputs_t out;
     const ges_frame_status_t* status;

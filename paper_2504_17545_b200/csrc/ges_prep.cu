@@ -80,10 +80,25 @@ __device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1,
     return x1 >= x0 && y1 >= y0;
 }
 
-__device__ __forceinline__ void count_tiles(uint32_t* cnt, const Grid& g, int x0, int x1, int y0, int y1) {
+// Count this primitive into every tile of its pixel range.  Called by ALL
+// lanes of the warp (empty ranges allowed); lanes that hit the same tile in
+// the same round are merged into one atomic (spatially ordered scenes make
+// warps' primitives share tiles).
+__device__ __forceinline__ void count_tiles(uint32_t* cnt, const Grid& g, bool live, int x0, int x1, int y0,
+                                            int y1, float zkey) {
     int tx0 = x0 / g.tile_px, tx1 = x1 / g.tile_px, ty0 = y0 / g.tile_px, ty1 = y1 / g.tile_px;
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(cnt + ty * g.ntx + tx, 1u);
+    int tx = tx0, ty = ty0;
+    bool more = live;
+    const int slab = g.slabs.slab(zkey);
+    const unsigned lane = threadIdx.x & 31;
+    while (__any_sync(0xffffffffu, more)) {
+        int key = more ? (ty * g.ntx + tx) * NSLAB + slab : -1;
+        unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (more && lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(cnt + key, (uint32_t)__popc(peers));
+        if (more) {
+            if (++tx > tx1) { tx = tx0; if (++ty > ty1) more = false; }
+        }
+    }
 }
 
 // Ray-plane homography of a planar primitive relative to pixel (xr, yr):
@@ -115,9 +130,11 @@ __device__ __forceinline__ void planar_coeffs(d3 q, d3 a1, d3 a2, d3 n, double s
 __global__ void k_pack_prims(ges_scene_src_t src, ges_scene_t dst) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < src.n_surfels) {
-        const double* p = src.s_pos + 3 * i;
-        const double* q = src.s_quat + 4 * i;
-        const double* l = src.s_log_scale + 2 * i;
+        const int64_t o = src.s_order ? src.s_order[i] : i;
+        const double* p = src.s_pos + 3 * o;
+        const double* q = src.s_quat + 4 * o;
+        const double* l = src.s_log_scale + 2 * o;
+        dst.s_id[i] = (int32_t)o;
         double nrm = 1.0 / sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
         reinterpret_cast<float4*>(dst.s_pos_s1)[i] = make_float4(p[0], p[1], p[2], exp(l[0]));
         reinterpret_cast<float4*>(dst.s_quat)[i] =
@@ -128,11 +145,12 @@ __global__ void k_pack_prims(ges_scene_src_t src, ges_scene_t dst) {
         // primitives.py:113-131: eff_scale = sqrt(s^2 + f3), eff_opacity =
         // sigma * prod(s / eff_s), epsilon = (5/D) sum eff_s.
         int D = src.gaussian_dim;
-        const double* p = src.g_pos + 3 * i;
-        const double* q = src.g_quat + 4 * i;
-        const double* l = src.g_log_scale + D * i;
-        double f3 = src.g_filter3d ? src.g_filter3d[i] : 0.0;
-        double sig = 1.0 / (1.0 + exp(-src.g_raw_opacity[i]));
+        const int64_t o = src.g_order ? src.g_order[i] : i;
+        const double* p = src.g_pos + 3 * o;
+        const double* q = src.g_quat + 4 * o;
+        const double* l = src.g_log_scale + D * o;
+        double f3 = src.g_filter3d ? src.g_filter3d[o] : 0.0;
+        double sig = 1.0 / (1.0 + exp(-src.g_raw_opacity[o]));
         double es[3] = {0.0, 0.0, 0.0}, esum = 0.0;
         for (int k = 0; k < D; ++k) {
             double s = exp(l[k]);
@@ -149,18 +167,25 @@ __global__ void k_pack_prims(ges_scene_src_t src, ges_scene_t dst) {
     }
 }
 
-__global__ void k_pack_sh(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+// Row-permuted float64 -> float32 copy of the (N, K*3) SH blocks.
+__global__ void k_pack_sh(const double* __restrict__ a, float* __restrict__ b, int64_t n, int row,
+                          const int32_t* __restrict__ order) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        b[i] = (float)a[i];
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / row, c = i - r * row;
+        int64_t src = order ? (int64_t)order[r] : r;
+        b[i] = (float)a[src * row + c];
+    }
 }
 
 cudaError_t launch_pack(const ges_scene_src_t& src, const ges_scene_t& dst, cudaStream_t s) {
     int64_t n = src.n_surfels > src.n_gaussians ? src.n_surfels : src.n_gaussians;
     if (n > 0) k_pack_prims<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, dst);
     int K = (src.sh_degree + 1) * (src.sh_degree + 1);
-    if (src.n_surfels) k_pack_sh<<<1184, 256, 0, s>>>(src.s_sh, dst.s_sh, src.n_surfels * K * 3);
-    if (src.n_gaussians) k_pack_sh<<<1184, 256, 0, s>>>(src.g_sh, dst.g_sh, src.n_gaussians * K * 3);
+    if (src.n_surfels)
+        k_pack_sh<<<1184, 256, 0, s>>>(src.s_sh, dst.s_sh, src.n_surfels * K * 3, K * 3, src.s_order);
+    if (src.n_gaussians)
+        k_pack_sh<<<1184, 256, 0, s>>>(src.g_sh, dst.g_sh, src.n_gaussians * K * 3, K * 3, src.g_order);
     return cudaGetLastError();
 }
 
@@ -169,7 +194,8 @@ cudaError_t launch_pack(const ges_scene_src_t& src, const ges_scene_t& dst, cuda
 template <int DEG>
 __global__ void __launch_bounds__(256) k_surfel_prep(ges_scene_t sc, CamK cam, Grid g, PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= sc.n_surfels) return;
+    const bool valid_thread = i < sc.n_surfels;
+    if (!valid_thread) i = sc.n_surfels - 1;   // idle lanes still join the warp-wide count
     float4 ps = __ldg(reinterpret_cast<const float4*>(sc.s_pos_s1) + i);
     float4 qf = __ldg(reinterpret_cast<const float4*>(sc.s_quat) + i);
     double s1 = ps.w, s2 = __ldg(sc.s_s2 + i);
@@ -181,28 +207,32 @@ __global__ void __launch_bounds__(256) k_surfel_prep(ges_scene_t sc, CamK cam, G
     d3 a1 = rot(cam, r0), a2 = rot(cam, r1), n = rot(cam, r2);
     SurfRec rec;
     int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
-    bool alive = q.z > NEAR;
+    bool alive = valid_thread && q.z > NEAR;
     if (alive) alive = disc_ranges(q, scl(a1, s1 * R_OPAQUE), scl(a2, s2 * R_OPAQUE), cam, x0, x1, y0, y1);
+    // nearest camera depth of the disc, made conservative against the float32
+    // evaluation of the per-pixel hit depth (culling and slab key only)
+    double zmin = q.z - R_OPAQUE * sqrt(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z);
+    zmin -= 1e-5 * fabs(zmin) + 1e-6;
+    const float zkey = (float)zmin;
+    count_tiles(o.bin_count, g, alive, x0, x1, y0, y1, zkey);
+    if (!valid_thread) return;
+    const int32_t sid = __ldg(sc.s_id + i);
     if (alive) {
         planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
-        // nearest camera depth of the disc, made conservative against the float32
-        // evaluation of the per-pixel hit depth (used only to skip surfels)
-        double zmin = q.z - R_OPAQUE * sqrt(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z);
-        zmin -= 1e-5 * fabs(zmin) + 1e-6;
-        rec.r3 = make_float4((float)zmin, __uint_as_float(pack_span(x0, x1)),
-                             __uint_as_float(pack_span(y0, y1)), 0.f);
-        count_tiles(o.tile_count, g, x0, x1, y0, y1);
+        rec.r3 = make_float4(zkey, __uint_as_float(pack_span(x0, x1)),
+                             __uint_as_float(pack_span(y0, y1)), __int_as_float(sid));
         // view colour: SH at the centre-to-camera direction (forward.py:99-103)
         d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
         double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
         float3 col = sh_color<DEG>(sc.s_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
                                    (float)(dv.y * inv), (float)(dv.z * inv));
-        o.rgb[i] = make_float4(col.x, col.y, col.z, 0.f);
+        o.rgb[sid] = make_float4(col.x, col.y, col.z, 0.f);   // indexed by source id (winner ids)
         double sgn = dot(n, q) < 0.0 ? 1.0 : -1.0;   // forward.py:152
-        o.nrm[i] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);
+        o.nrm[sid] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);
     } else {
         rec.r0 = rec.r1 = rec.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
-        rec.r3 = make_float4(0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)), 0.f);
+        rec.r3 = make_float4(0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)),
+                             __int_as_float(sid));
     }
     reinterpret_cast<SurfRec*>(o.rec)[i] = rec;
 }
@@ -231,14 +261,15 @@ template <int DEG>
 __global__ void __launch_bounds__(256) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= sc.n_gaussians) return;
+    const bool valid_thread = i < sc.n_gaussians;
+    if (!valid_thread) i = sc.n_gaussians - 1;
     float4 po = __ldg(reinterpret_cast<const float4*>(sc.g_pos_op) + i);
     float4 qf = __ldg(reinterpret_cast<const float4*>(sc.g_quat) + i);
     float4 se = __ldg(reinterpret_cast<const float4*>(sc.g_scale_eps) + i);
     d3 p = mk(po.x, po.y, po.z);
     d3 t = rot(cam, p);
     t.x += cam.t[0]; t.y += cam.t[1]; t.z += cam.t[2];
-    bool valid = t.z > NEAR;
+    bool valid = valid_thread && t.z > NEAR;
     d3 ts = valid ? t : mk(0.0, 0.0, 1.0);
     d3 r0, r1, r2;
     quat_cols(qf, r0, r1, r2);
@@ -280,19 +311,20 @@ __global__ void __launch_bounds__(256) k_gauss3_prep(ges_scene_t sc, CamK cam, G
         y1 = clampi(floor(my + ry + 0.5 - 0.5), cam.H);
         valid = x1 >= x0 && y1 >= y0;
     }
+    const float depf = (float)t.z, epsf = cfg.eps_const ? cfg.eps_value : se.w;
+    count_tiles(o.bin_count, g, valid, x0, x1, y0, y1, gauss_key(depf, epsf));
+    if (!valid_thread) return;
     if (valid) {
         double mxi = floor(mx), myi = floor(my);
         rec.r0 = make_float4((float)mxi, (float)(mx - mxi), (float)myi, (float)(my - myi));
         rec.r1 = make_float4((float)(-0.5 * la), (float)(-lb), (float)(-0.5 * lc), (float)sig);
-        float eps = cfg.eps_const ? cfg.eps_value : se.w;
-        rec.r2 = make_float4((float)t.z, eps, (float)(-0.5 * m2max) - 1e-4f,
+        rec.r2 = make_float4(depf, epsf, (float)(-0.5 * m2max) - 1e-4f,
                              __uint_as_float(pack_span(x0, x1)));
         d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
         double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
         float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
                                    (float)(dv.y * inv), (float)(dv.z * inv));
         rec.r3 = make_float4(__uint_as_float(pack_span(y0, y1)), col.x, col.y, col.z);
-        count_tiles(o.tile_count, g, x0, x1, y0, y1);
         if (cfg.geom) {   // forward.py:277-284: shortest eff_scale axis, camera-facing
             int k = 0;
             double smin = se.x;
@@ -315,7 +347,8 @@ template <int DEG>
 __global__ void __launch_bounds__(256) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= sc.n_gaussians) return;
+    const bool valid_thread = i < sc.n_gaussians;
+    if (!valid_thread) i = sc.n_gaussians - 1;
     float4 po = __ldg(reinterpret_cast<const float4*>(sc.g_pos_op) + i);
     float4 qf = __ldg(reinterpret_cast<const float4*>(sc.g_quat) + i);
     float4 se = __ldg(reinterpret_cast<const float4*>(sc.g_scale_eps) + i);
@@ -344,28 +377,34 @@ __global__ void __launch_bounds__(256) k_gauss2_prep(ges_scene_t sc, CamK cam, G
         sig *= 1.0 / (sm0 * sm1);
     }
     double m2max = 2.0 * log(fmax(255.0 * sig, 1e-12));
-    bool valid = fvalid && q.z > NEAR && m2max > 0.0;
+    bool valid = valid_thread && fvalid && q.z > NEAR && m2max > 0.0;
     double rmax = sqrt(fmax(m2max, 0.0));
     int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
     if (valid) valid = disc_ranges(q, scl(a1, s1 * rmax), scl(a2, s2 * rmax), cam, x0, x1, y0, y1);
+    // slab key: nearest depth of the alpha support minus eps (gate t < D_s + eps)
+    const float epsf = cfg.eps_const ? cfg.eps_value : se.w;
+    double zsup = q.z - rmax * sqrt(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z);
+    zsup -= 1e-5 * fabs(zsup) + 1e-6;
+    const float gkey = (float)zsup - epsf;
+    count_tiles(o.bin_count, g, valid, x0, x1, y0, y1, gkey);
+    if (!valid_thread) return;
     Gauss2Rec rec;
     if (valid) {
         planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
-        float eps = cfg.eps_const ? cfg.eps_value : se.w;
-        rec.r3 = make_float4((float)sig, eps, __uint_as_float(pack_span(x0, x1)),
+        rec.r3 = make_float4((float)sig, epsf, __uint_as_float(pack_span(x0, x1)),
                              __uint_as_float(pack_span(y0, y1)));
         d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
         double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
         float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
                                    (float)(dv.y * inv), (float)(dv.z * inv));
         rec.r4 = make_float4(col.x, col.y, col.z, (float)m2max * 1.0001f + 1e-4f);
-        count_tiles(o.tile_count, g, x0, x1, y0, y1);
+        rec.r5 = make_float4(gkey, 0.f, 0.f, 0.f);
         if (cfg.geom) {
             double sgn = dot(n, q) < 0.0 ? 1.0 : -1.0;   // forward.py:337
             o.nrm[i] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);
         }
     } else {
-        rec.r0 = rec.r1 = rec.r2 = rec.r4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        rec.r0 = rec.r1 = rec.r2 = rec.r4 = rec.r5 = make_float4(0.f, 0.f, 0.f, 0.f);
         rec.r3 = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
     }
     reinterpret_cast<Gauss2Rec*>(o.rec)[i] = rec;

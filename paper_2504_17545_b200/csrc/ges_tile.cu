@@ -32,7 +32,23 @@ struct __align__(16) TileSmem {
     int pre[NWARP][NWARP];      // exclusive prefix over src warps
     int tot[NWARP];
     float wmax[NWARP];          // per-warp max surfel depth (Gaussian culling)
+    uint32_t slab_end[NSLAB];   // this tile's slab ends (relative list positions)
 };
+
+// Slab holding relative list position `rel`, and the CTA-wide max of the
+// per-warp depths in sm.wmax (both read from shared memory: CTA-uniform).
+__device__ __forceinline__ int slab_at(const TileSmem& sm, uint32_t rel) {
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < NSLAB - 1; ++k) s += sm.slab_end[k] <= rel;
+    return s;
+}
+__device__ __forceinline__ float tile_max(const TileSmem& sm) {
+    float m = sm.wmax[0];
+#pragma unroll
+    for (int w = 1; w < NWARP; ++w) m = fmaxf(m, sm.wmax[w]);
+    return m;
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
@@ -155,10 +171,13 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
         };
         float wmx = INFINITY;          // max over this warp's (sub)pixels of the best depth
         if (lane == 0) sm.wmax[warp] = INFINITY;
+        if (threadIdx.x < NSLAB) sm.slab_end[threadIdx.x] = a.sbin.cnt[tile * NSLAB + threadIdx.x];
         __syncthreads();
         const int ox = tx * TILE * SS, oy = ty * TILE * SS;
-        const uint32_t beg = a.s_off[tile], end = a.s_off[tile + 1];
+        const uint32_t beg = a.sbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
         for (uint32_t base = beg; base < end; base += NB) {
+            // slabs are near-to-far: stop once the next slab lies behind every hit so far
+            if (a.slabs.lower(slab_at(sm, base - beg)) > tile_max(sm)) break;
             const int nb = min((uint32_t)NB, end - base);
             uint32_t mask = 0;
             if ((int)threadIdx.x < nb) {
@@ -181,7 +200,7 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                     if (r3.x > sm.wmax[w]) mask &= ~(1u << w);
                 sm.st[0][threadIdx.x] = make_float4(d0, dx_, dy_, nq);
                 sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
-                sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, __uint_as_float(id), r3.x);
+                sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.w, r3.x);   // r3.w: source id
             }
             build_lists(sm, mask, warp, lane);
             const int L = sm.tot[warp];
@@ -258,7 +277,9 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
         float wsum = 0.f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
         const float wm = warp_max(inside ? ds : -INFINITY);
         if (lane == 0) sm.wmax[warp] = wm;
+        if (threadIdx.x < NSLAB) sm.slab_end[threadIdx.x] = a.gbin.cnt[tile * NSLAB + threadIdx.x];
         __syncthreads();
+        const float dmax = tile_max(sm);
         const float lx = (float)plx, ly = (float)ply;
         float pe = 0.f;
         if constexpr (GK == 2) {
@@ -266,8 +287,10 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
             pe = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
         }
         const int ox = tx * TILE, oy = ty * TILE;
-        const uint32_t beg = a.g_off[tile], end = a.g_off[tile + 1];
+        const uint32_t beg = a.gbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
         for (uint32_t base = beg; base < end; base += NB) {
+            // keys (depth - eps) are binned near-to-far: the rest fail every gate
+            if (a.slabs.lower(slab_at(sm, base - beg)) > dmax) break;
             const int nb = min((uint32_t)NB, end - base);
             uint32_t mask = 0;
             if ((int)threadIdx.x < nb) {

@@ -40,6 +40,43 @@ def _degree(sh) -> int:
     return d
 
 
+def morton_order(pos: torch.Tensor) -> torch.Tensor:
+    """int32 permutation sorting (N, 3) positions along a 30-bit 3D Morton
+    curve over their bounding box (once per scene, at pack time)."""
+    if pos.shape[0] == 0:
+        return torch.zeros(0, dtype=torch.int32, device=pos.device)
+    lo = pos.min(dim=0).values
+    ext = (pos.max(dim=0).values - lo).clamp_min(1e-30)
+    q = ((pos - lo) / ext * 1023.0).clamp(0, 1023).to(torch.int64)
+
+    def spread(v):   # insert two zero bits between the 10 bits of v
+        v = (v | (v << 16)) & 0x030000FF
+        v = (v | (v << 8)) & 0x0300F00F
+        v = (v | (v << 4)) & 0x030C30C3
+        return (v | (v << 2)) & 0x09249249
+
+    code = spread(q[:, 0]) | (spread(q[:, 1]) << 1) | (spread(q[:, 2]) << 2)
+    return torch.argsort(code, stable=True).to(torch.int32)
+
+
+def scene_bounds(s, g, ns, ng):
+    """Centre bounding box + largest primitive radius (slab depth range only)."""
+    pts, rad = [], 0.0
+    if ns:
+        p = np.asarray(s.pos, dtype=np.float64)
+        pts += [p.min(axis=0), p.max(axis=0)]
+        rad = max(rad, 3.3290429691304455 * float(np.exp(np.max(np.asarray(s.log_scale)))))
+    if ng:
+        p = np.asarray(g.pos, dtype=np.float64)
+        pts += [p.min(axis=0), p.max(axis=0)]
+        rad = max(rad, 5.0 * float(np.exp(np.max(np.asarray(g.log_scale)))))
+    if not pts:
+        return [0.0] * 7
+    lo = np.min(np.stack(pts), axis=0)
+    hi = np.max(np.stack(pts), axis=0)
+    return [float(v) for v in lo] + [float(v) for v in hi] + [rad]
+
+
 def camera_struct(cam) -> _lib.Camera:
     m = np.asarray(cam.world_to_camera, dtype=np.float64)
     c = _lib.Camera()
@@ -68,7 +105,7 @@ class DeviceScene:
     float64 arrays are uploaded, packed by ``ges_scene_pack`` and dropped.
     """
 
-    def __init__(self, scene, device=None):
+    def __init__(self, scene, device=None, *, spatial_order: bool = True):
         self.device = torch.device(device or "cuda")
         s, g = scene.surfels, scene.gaussians
         ns, ng = int(np.asarray(s.pos).shape[0]), int(np.asarray(g.pos).shape[0])
@@ -88,6 +125,7 @@ class DeviceScene:
         K = (deg + 1) ** 2
         keep = []
         src = _lib.SceneSrc()
+        src.bounds[:] = scene_bounds(s, g, ns, ng)
         src.n_surfels, src.n_gaussians, src.sh_degree, src.gaussian_dim = ns, ng, deg, dim
         if ns:
             for name, a, shp in (("s_pos", s.pos, (ns, 3)), ("s_quat", s.quat, (ns, 4)),
@@ -95,6 +133,10 @@ class DeviceScene:
                 t = up(a, shp)
                 keep.append(t)
                 setattr(src, name, t.data_ptr())
+            if spatial_order:
+                so = morton_order(keep[0])
+                keep.append(so)
+                src.s_order = so.data_ptr()
         if ng:
             f3 = getattr(g, "filter3d", None)
             f3 = np.zeros(ng) if f3 is None else f3
@@ -104,6 +146,10 @@ class DeviceScene:
                 t = up(a, shp)
                 keep.append(t)
                 setattr(src, name, t.data_ptr())
+                if name == "g_pos" and spatial_order:
+                    go = morton_order(t)
+                    keep.append(go)
+                    src.g_order = go.data_ptr()
         L = _lib.lib()
         nbytes = L.ges_scene_bytes(ns, ng, deg)
         self.blob = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
