@@ -11,12 +11,15 @@
 // never leaves the register file, fused with the composite write
 // (forward.py:384-417).
 //
-// Both passes stream the tile's primitive list through shared memory in
-// batches of 256 (one primitive per thread, transformed to tile-relative
-// coefficients once), then build per-warp work lists: a primitive is handed
-// to the warps whose 8x4 pixel patch its pixel range overlaps (and, for
-// Gaussians, whose nearest surfel depth can pass the gate), so warps only
-// test primitives that can touch them.
+// Both passes stream the tile's (tile, depth-slab)-binned primitive list
+// through shared memory in batches of 256: one primitive per thread, turned
+// into tile-relative coefficients once, with an 8-bit mask of the warp
+// patches (8x4 pixels) its pixel range overlaps.  Each warp then scans the
+// batch 32 entries at a time, votes which entries can still matter to it
+// (patch overlap, and for surfels: disc not entirely behind every hit of the
+// patch so far; for Gaussians: depth can pass some gate in the patch) and
+// runs the per-pixel test only on those.  Culling never changes results: the
+// per-pixel tests are exact and order-independent.
 #include <math.h>
 
 #include "ges_launch.h"
@@ -27,11 +30,9 @@ constexpr int NB = TILE_PX;     // batch = one primitive per thread
 
 struct __align__(16) TileSmem {
     float4 st[5][NB];           // staged per-primitive coefficients
-    uint8_t wl[NWARP][NB];      // per-warp work lists (batch indices)
-    int cnt[NWARP][NWARP];      // cnt[src warp][dst warp]
-    int pre[NWARP][NWARP];      // exclusive prefix over src warps
-    int tot[NWARP];
-    float wmax[NWARP];          // per-warp max surfel depth (Gaussian culling)
+    float zm[NB];               // surfels: conservative nearest depth of the disc
+    uint8_t pm[NB];             // warp-patch masks
+    float wmax[NWARP];          // per-warp max depth (surfels: current hits; Gaussians: final)
     uint32_t slab_end[NSLAB];   // this tile's slab ends (relative list positions)
 };
 
@@ -48,39 +49,6 @@ __device__ __forceinline__ float tile_max(const TileSmem& sm) {
 #pragma unroll
     for (int w = 1; w < NWARP; ++w) m = fmaxf(m, sm.wmax[w]);
     return m;
-}
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-    uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-
-// Distribute the batch to per-warp lists (deterministic, batch order kept).
-__device__ __forceinline__ void build_lists(TileSmem& sm, uint32_t mask, int warp, int lane) {
-    uint32_t bal[NWARP];
-#pragma unroll
-    for (int w = 0; w < NWARP; ++w) bal[w] = __ballot_sync(0xffffffffu, (mask >> w) & 1u);
-    if (lane == 0) {
-#pragma unroll
-        for (int w = 0; w < NWARP; ++w) sm.cnt[warp][w] = __popc(bal[w]);
-    }
-    __syncthreads();
-    if (threadIdx.x < NWARP) {
-        int w = threadIdx.x, acc = 0;
-#pragma unroll
-        for (int s = 0; s < NWARP; ++s) {
-            sm.pre[s][w] = acc;
-            acc += sm.cnt[s][w];
-        }
-        sm.tot[w] = acc;
-    }
-    __syncthreads();
-    uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int w = 0; w < NWARP; ++w)
-        if ((mask >> w) & 1u) sm.wl[w][sm.pre[warp][w] + __popc(bal[w] & lt)] = (uint8_t)threadIdx.x;
-    __syncthreads();
 }
 
 // Bitmask of warp patches (8x4 base px each, 2 columns x 4 rows) that the
@@ -179,18 +147,17 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
             // slabs are near-to-far: stop once the next slab lies behind every hit so far
             if (a.slabs.lower(slab_at(sm, base - beg)) > tile_max(sm)) break;
             const int nb = min((uint32_t)NB, end - base);
-            uint32_t mask = 0;
             if ((int)threadIdx.x < nb) {
                 const uint32_t id = a.s_list[base + threadIdx.x];
                 const SurfRec* r = a.srec + id;
-                float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3);
-                float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
+                const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3);
+                const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
                 float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
-                float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
-                float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
-                uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
-                mask = patch_mask<SS>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
-                                      span_hi(syr) - oy);
+                const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
+                const float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
+                const uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
+                uint32_t mask = patch_mask<SS>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
+                                               span_hi(syr) - oy);
                 // hit depth t = nq / den: orient den so that t > 0 <=> den > 0
                 float nq = r0.w, dx_ = r0.y, dy_ = r0.z;
                 if (nq < 0.f) { nq = -nq; d0 = -d0; dx_ = -dx_; dy_ = -dy_; }
@@ -201,44 +168,50 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                 sm.st[0][threadIdx.x] = make_float4(d0, dx_, dy_, nq);
                 sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
                 sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.w, r3.x);   // r3.w: source id
+                sm.zm[threadIdx.x] = r3.x;
+                sm.pm[threadIdx.x] = (uint8_t)mask;
             }
-            build_lists(sm, mask, warp, lane);
-            const int L = sm.tot[warp];
-            for (int k = 0; k < L; ++k) {
-                if ((k & 7) == 0) wmx = patch_depth();
-                const int j = sm.wl[warp][k];
-                const float4 C = sm.st[2][j];
-                if (C.w > wmx) continue;   // disc entirely behind every pixel's current hit
-                const float4 A = sm.st[0][j], B = sm.st[1][j];
+            __syncthreads();
+            for (int c = 0; c < nb; c += 32) {
+                const int e = c + lane;
+                const bool want = e < nb && ((sm.pm[e] >> warp) & 1u) && !(sm.zm[e] > wmx);
+                uint32_t vote = __ballot_sync(0xffffffffu, want);
+                while (vote) {
+                    const int j = c + __ffs(vote) - 1;
+                    vote &= vote - 1;
+                    const float4 C = sm.st[2][j];
+                    if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
+                    const float4 A = sm.st[0][j], B = sm.st[1][j];
 #pragma unroll
-                for (int sy = 0; sy < SS; ++sy)
+                    for (int sy = 0; sy < SS; ++sy)
 #pragma unroll
-                    for (int sx = 0; sx < SS; ++sx) {
-                        const int s = sy * SS + sx;
-                        const float lx = lxf[sx], ly = lyf[sy];
-                        const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
-                        const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
-                        const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
-                        const float r2 = fmaf(U, U, V * V);
-                        // coverage u^2+v^2 <= R^2, |n.d| > eps|d|, t > 0.01, and t no
-                        // later than the current best (multiplied out; exact key below)
-                        if (den > pe[s] && r2 <= R2_F * den * den && A.w > NEAR_F * den &&
-                            A.w <= tb[s] * 1.00001f * den) {
-                            const float t = A.w / den;
-                            const unsigned long long key =
-                                ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
-                            if (t > NEAR_F && key < best[s]) {
-                                best[s] = key;
-                                tb[s] = t;
+                        for (int sx = 0; sx < SS; ++sx) {
+                            const int s = sy * SS + sx;
+                            const float lx = lxf[sx], ly = lyf[sy];
+                            const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
+                            const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
+                            const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
+                            const float r2 = fmaf(U, U, V * V);
+                            // coverage u^2+v^2 <= R^2, |n.d| > eps|d|, t > 0.01, and t no
+                            // later than the current best (multiplied out; exact key below)
+                            if (den > pe[s] && r2 <= R2_F * den * den && A.w > NEAR_F * den &&
+                                A.w <= tb[s] * 1.00001f * den) {
+                                const float t = A.w / den;
+                                const unsigned long long key =
+                                    ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
+                                if (t > NEAR_F && key < best[s]) {
+                                    best[s] = key;
+                                    tb[s] = t;
+                                }
                             }
                         }
-                    }
+                }
+                wmx = patch_depth();
             }
-            wmx = patch_depth();
             if (lane == 0) sm.wmax[warp] = wmx;
             __syncthreads();
         }
-        // resolve: depth/normal/winner from sub-sample 0, colour = box mean
+        // resolve: depth/normal/winner from sub-sample 0, colour = box mean (forward.py:201-207)
         float3 acc = make_float3(0.f, 0.f, 0.f);
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -292,15 +265,16 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
             // keys (depth - eps) are binned near-to-far: the rest fail every gate
             if (a.slabs.lower(slab_at(sm, base - beg)) > dmax) break;
             const int nb = min((uint32_t)NB, end - base);
-            uint32_t mask = 0;
             if ((int)threadIdx.x < nb) {
                 const uint32_t id = a.g_list[base + threadIdx.x];
+                uint32_t mask;
                 if constexpr (GK == 3) {
                     const GaussRec* r = reinterpret_cast<const GaussRec*>(a.grec) + id;
-                    float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3);
-                    float mxt = (r0.x - (float)ox) + (r0.y - 0.5f);
-                    float myt = (r0.z - (float)oy) + (r0.w - 0.5f);
-                    uint32_t sxr = __float_as_uint(r2.w), syr = __float_as_uint(r3.x);
+                    const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2),
+                                 r3 = __ldg(&r->r3);
+                    const float mxt = (r0.x - (float)ox) + (r0.y - 0.5f);
+                    const float myt = (r0.z - (float)oy) + (r0.w - 0.5f);
+                    const uint32_t sxr = __float_as_uint(r2.w), syr = __float_as_uint(r3.x);
                     mask = patch_mask<1>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
                                          span_hi(syr) - oy);
                     // exact conservative cull: d < fl(max_ds + eps) is necessary for the gate
@@ -312,62 +286,70 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                     sm.st[2][threadIdx.x] = make_float4(r3.y, r3.z, r3.w, r2.z);
                 } else {
                     const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + id;
-                    float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3),
-                           r4 = __ldg(&r->r4);
-                    float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
-                    float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
-                    float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
-                    float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
-                    uint32_t sxr = __float_as_uint(r3.z), syr = __float_as_uint(r3.w);
+                    const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2),
+                                 r3 = __ldg(&r->r3), r4 = __ldg(&r->r4), r5 = __ldg(&r->r5);
+                    const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
+                    const float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
+                    const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
+                    const float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
+                    const uint32_t sxr = __float_as_uint(r3.z), syr = __float_as_uint(r3.w);
                     mask = patch_mask<1>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
                                          span_hi(syr) - oy);
+#pragma unroll
+                    for (int w = 0; w < NWARP; ++w)   // key = nearest support depth - eps
+                        if (r5.x > sm.wmax[w]) mask &= ~(1u << w);
                     sm.st[0][threadIdx.x] = make_float4(d0, r0.y, r0.z, r0.w);
                     sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
                     sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.x, r3.y);
                     sm.st[3][threadIdx.x] = r4;
                 }
                 if constexpr (GEOM) sm.st[4][threadIdx.x] = __ldg(a.g_nrm + id);
+                sm.pm[threadIdx.x] = (uint8_t)mask;
             }
-            build_lists(sm, mask, warp, lane);
-            const int L = sm.tot[warp];
-            for (int k = 0; k < L; ++k) {
-                const int j = sm.wl[warp][k];
-                const float4 A = sm.st[0][j], B = sm.st[1][j], C = sm.st[2][j];
-                if constexpr (GK == 3) {
-                    // forward.py:301-311
-                    const float dx = lx - A.x, dy = ly - A.y;
-                    const float p = fmaf(A.z * dx, dx, fmaf(B.x * dy, dy, A.w * dx * dy));
-                    if (p >= C.w) {
-                        const float al = B.y * __expf(p);
-                        if (al >= ALPHA_CUTOFF_F && B.z < ds + B.w) {
-                            wsum += al;
-                            cr = fmaf(al, C.x, cr); cg = fmaf(al, C.y, cg); cb = fmaf(al, C.z, cb);
-                            if constexpr (GEOM) {
-                                const float4 N = sm.st[4][j];
-                                dsum = fmaf(al, B.z, dsum);
-                                nx = fmaf(al, N.x, nx); ny = fmaf(al, N.y, ny); nz = fmaf(al, N.z, nz);
+            __syncthreads();
+            for (int c = 0; c < nb; c += 32) {
+                const int e = c + lane;
+                uint32_t vote = __ballot_sync(0xffffffffu, e < nb && ((sm.pm[e] >> warp) & 1u));
+                while (vote) {
+                    const int j = c + __ffs(vote) - 1;
+                    vote &= vote - 1;
+                    const float4 A = sm.st[0][j], B = sm.st[1][j], C = sm.st[2][j];
+                    if constexpr (GK == 3) {
+                        // forward.py:301-311
+                        const float dx = lx - A.x, dy = ly - A.y;
+                        const float p = fmaf(A.z * dx, dx, fmaf(B.x * dy, dy, A.w * dx * dy));
+                        if (p >= C.w) {
+                            const float al = B.y * __expf(p);
+                            if (al >= ALPHA_CUTOFF_F && B.z < ds + B.w) {
+                                wsum += al;
+                                cr = fmaf(al, C.x, cr); cg = fmaf(al, C.y, cg); cb = fmaf(al, C.z, cb);
+                                if constexpr (GEOM) {
+                                    const float4 N = sm.st[4][j];
+                                    dsum = fmaf(al, B.z, dsum);
+                                    nx = fmaf(al, N.x, nx); ny = fmaf(al, N.y, ny); nz = fmaf(al, N.z, nz);
+                                }
                             }
                         }
-                    }
-                } else {
-                    // forward.py:361-379
-                    const float4 E = sm.st[3][j];
-                    const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
-                    const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
-                    const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
-                    const float r2u = fmaf(U, U, V * V);
-                    if (r2u <= E.w * den * den && fabsf(den) > pe) {
-                        const float inv = __fdividef(1.0f, den);
-                        const float t = A.w * inv;
-                        const float q2 = r2u * inv * inv;
-                        const float al = C.z * __expf(-0.5f * q2);
-                        if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds + C.w) {
-                            wsum += al;
-                            cr = fmaf(al, E.x, cr); cg = fmaf(al, E.y, cg); cb = fmaf(al, E.z, cb);
-                            if constexpr (GEOM) {
-                                const float4 N = sm.st[4][j];
-                                dsum = fmaf(al, t, dsum);
-                                nx = fmaf(al, N.x, nx); ny = fmaf(al, N.y, ny); nz = fmaf(al, N.z, nz);
+                    } else {
+                        // forward.py:361-379
+                        const float4 E = sm.st[3][j];
+                        const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
+                        const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
+                        const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
+                        const float r2u = fmaf(U, U, V * V);
+                        if (r2u <= E.w * den * den && fabsf(den) > pe) {
+                            const float inv = __fdividef(1.0f, den);
+                            const float t = A.w * inv;
+                            const float q2 = r2u * inv * inv;
+                            const float al = C.z * __expf(-0.5f * q2);
+                            if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds + C.w) {
+                                wsum += al;
+                                cr = fmaf(al, E.x, cr); cg = fmaf(al, E.y, cg); cb = fmaf(al, E.z, cb);
+                                if constexpr (GEOM) {
+                                    const float4 N = sm.st[4][j];
+                                    dsum = fmaf(al, t, dsum);
+                                    nx = fmaf(al, N.x, nx); ny = fmaf(al, N.y, ny); nz = fmaf(al, N.z, nz);
+                                }
                             }
                         }
                     }
@@ -387,11 +369,13 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                     a.out.g_normal[3 * pix + 2] = nz;
                 }
             }
-            if (a.out.image) {
+            if (a.out.image || a.out.image_rgba8) {
                 const float3 im = im_of(a, cs, wsum, cr, cg, cb);
-                a.out.image[3 * pix] = im.x; a.out.image[3 * pix + 1] = im.y; a.out.image[3 * pix + 2] = im.z;
+                if (a.out.image) {
+                    a.out.image[3 * pix] = im.x; a.out.image[3 * pix + 1] = im.y; a.out.image[3 * pix + 2] = im.z;
+                }
+                if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, im);
             }
-            if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, im_of(a, cs, wsum, cr, cg, cb));
         }
     } else if (inside) {   // surfels_only (forward.py:407-410): empty Gaussian buffers
         if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, cs);
