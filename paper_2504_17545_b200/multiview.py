@@ -39,24 +39,31 @@ def gather_frames(local: torch.Tensor, dst: int = 0, group=None):
 
 
 class ViewBatchRenderer:
-    """Renders a batch of same-resolution views of one packed scene into a
-    preallocated (V, H, W, 4) RGBA8 send buffer (plus optional fp32 images,
-    depth and winner maps), asynchronously on the current stream."""
+    """Renders a batch of views of one packed scene, asynchronously on the
+    current stream, into preallocated outputs: a (V, H, W, 4) RGBA8 send
+    buffer when all views share one resolution (a list of (H, W, 4) buffers
+    otherwise, e.g. the multi-scale Mip views), plus any other requested
+    buffers (fp32 image, depth, winner ...)."""
 
     def __init__(self, renderer, scene, cams, settings, *, want=("image_rgba8",)):
         self.r = renderer
         self.scene = scene
         self.cams = list(cams)
         self.settings = settings
-        H, W = int(self.cams[0].height), int(self.cams[0].width)
-        if any((int(c.height), int(c.width)) != (H, W) for c in self.cams):
-            raise ValueError("a view batch must share one resolution")
+        shapes = {(int(c.height), int(c.width)) for c in self.cams}
         dev = renderer.device
-        self.rgba = torch.empty((len(self.cams), H, W, 4), dtype=torch.uint8, device=dev)
         self.frames = []
-        for v, c in enumerate(self.cams):
+        if len(shapes) == 1:
+            H, W = shapes.pop()
+            self.rgba = torch.empty((len(self.cams), H, W, 4), dtype=torch.uint8, device=dev)
+            bufs = list(self.rgba.unbind(0))
+        else:
+            bufs = [torch.empty((int(c.height), int(c.width), 4), dtype=torch.uint8, device=dev)
+                    for c in self.cams]
+            self.rgba = bufs
+        for c, b in zip(self.cams, bufs):
             fr = renderer.alloc(c, settings, want=[k for k in want if k != "image_rgba8"])
-            fr.image_rgba8 = self.rgba[v]
+            fr.image_rgba8 = b
             self.frames.append(fr)
 
     def render(self, check: bool = False):
