@@ -35,16 +35,16 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
     uint32_t tot = 0;
     if (t < n) {
         uint4* c = reinterpret_cast<uint4*>(p.cnt + (size_t)t * NSLAB);
-        const uint4 a = c[0], b = c[1];
-        uint32_t v[NSLAB] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int s = 0; s < NSLAB; ++s) {
-            const uint32_t x = v[s];
-            v[s] = tot;
-            tot += x;
+        for (int q = 0; q < NSLAB / 4; ++q) {
+            uint4 v = c[q];
+            uint4 o;
+            o.x = tot; tot += v.x;
+            o.y = tot; tot += v.y;
+            o.z = tot; tot += v.z;
+            o.w = tot; tot += v.w;
+            c[q] = o;
         }
-        c[0] = make_uint4(v[0], v[1], v[2], v[3]);
-        c[1] = make_uint4(v[4], v[5], v[6], v[7]);
     }
     uint32_t ex, blk;
     Scan(tmp).ExclusiveSum(tot, ex, blk);
@@ -107,13 +107,15 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
     while (__any_sync(0xffffffffu, more)) {
         const int tile = ty * p.ntx + tx;
         const int key = more ? tile * NSLAB + slab : -1;
+        // tile offset loads are independent of the atomic: issue them first
+        const uint32_t toff = more ? p.tile_off(tile) : 0u;
         const unsigned peers = __match_any_sync(0xffffffffu, key);
         if (more) {
             const int leader = __ffs(peers) - 1;
             uint32_t base = 0;
             if (lane == (unsigned)leader) base = atomicAdd(p.cnt + key, (uint32_t)__popc(peers));
             base = __shfl_sync(peers, base, leader);
-            const uint32_t slot = p.tile_off(tile) + base + __popc(peers & ((1u << lane) - 1u));
+            const uint32_t slot = toff + base + __popc(peers & ((1u << lane) - 1u));
             if ((int64_t)slot < p.cap) p.list[slot] = id;
             if (++tx > tx1) { tx = tx0; if (++ty > ty1) more = false; }
         }
