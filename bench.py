@@ -36,6 +36,7 @@ def parse():
     p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     p.add_argument("--views", type=int, default=None, help="views per rank per step")
     p.add_argument("--ss", type=int, default=1, choices=[1, 4])
+    p.add_argument("--streams", type=int, default=2, help="CUDA streams pipelining the views of a step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     p.add_argument("--cpu-tiles", type=int, default=48, help="tiles in the CPU sample")
@@ -94,7 +95,7 @@ def base_config(cfg, per_rank, world, ss):
           "inputs fit in L2 (config 1 is the CPU-runnable parity case, not the headline)")
     return {"workload": WORKLOADS[cfg], "views_per_rank_per_step": per_rank,
             "resolution": [w, h] if cfg != 4 else "480x270, 960x540, 1920x1080, 3840x2160",
-            "supersample": ss, "parallelism": f"views x{world}",
+            "supersample": ss, "parallelism": f"views x{world}", "streams_per_gpu": ARGS.streams,
             "scene": "seeded synthetic (SURVEY 8(d), seed 0)", "l2": l2}
 
 
@@ -237,10 +238,12 @@ def run_gpu(args, rank, world, local_rank):
     upload_ms = (time.perf_counter() - t0) * 1e3
     rend = G.Renderer(dev)
     # B_alg outputs (image fp32, depth, winner) + the RGBA8 send buffer for the gather
-    vb = ViewBatchRenderer(rend, ds, cams, settings, want=("image", "s_depth", "s_winner", "image_rgba8"))
-    # size the pair lists from a checked first frame of every view
-    for c, fr in zip(vb.cams, vb.frames):
-        rend.render(ds, c, settings, frame=fr, check=True)
+    vb = ViewBatchRenderer(rend, ds, cams, settings, want=("image", "s_depth", "s_winner", "image_rgba8"),
+                           streams=args.streams)
+    # size every workspace's pair lists from a checked frame of every view
+    for r in vb.pool:
+        for c, fr in zip(vb.cams, vb.frames):
+            r.render(ds, c, settings, frame=fr, check=True)
     stream = torch.cuda.current_stream(dev)
 
     def step():

@@ -96,18 +96,54 @@ cudaError_t launch_scan(const BinPass& s, const BinPass& g, ges_frame_status_t* 
 // Append `id` to bin (tile, slab) of every tile of its range.  Called by all
 // lanes of a warp whose lanes all belong to the same primitive class; lanes
 // that hit the same bin in the same round reserve their slots with a single
-// atomic.
+// atomic.  The atomics of up to FILL_R rounds are issued back to back (their
+// results parked in registers) before any slot is written, so their L2 round
+// trips overlap instead of serialising; longer ranges finish in a plain loop.
+constexpr int FILL_R = 8;
+
 __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, uint32_t sy, int slab,
                                          const BinPass& p) {
-    int x0 = span_lo(sx), x1 = span_hi(sx), y0 = span_lo(sy), y1 = span_hi(sy);
+    const int x0 = span_lo(sx), x1 = span_hi(sx), y0 = span_lo(sy), y1 = span_hi(sy);
     bool more = live && x1 >= x0 && y1 >= y0;
     const int tp = p.tile_px;
-    int tx0 = x0 / tp, tx1 = x1 / tp, ty = y0 / tp, ty1 = y1 / tp, tx = tx0;
+    const int tx0 = x0 / tp, tx1 = x1 / tp, ty1 = y1 / tp;
+    int ty = y0 / tp, tx = tx0;
     const unsigned lane = threadIdx.x & 31;
-    while (__any_sync(0xffffffffu, more)) {
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t base_r[FILL_R], toff_r[FILL_R], peers_r[FILL_R];
+    bool act_r[FILL_R];
+#pragma unroll
+    for (int r = 0; r < FILL_R; ++r) {
+        act_r[r] = more;
+        peers_r[r] = 0u;
+        base_r[r] = 0u;
+        toff_r[r] = 0u;
+        if (__any_sync(0xffffffffu, more)) {
+            const int tile = ty * p.ntx + tx;
+            const int key = more ? tile * NSLAB + slab : -1;
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            if (more) {
+                peers_r[r] = peers;
+                toff_r[r] = p.tile_off(tile);
+                if (lane == (unsigned)(__ffs(peers) - 1))
+                    base_r[r] = atomicAdd(p.cnt + key, (uint32_t)__popc(peers));
+                if (++tx > tx1) { tx = tx0; if (++ty > ty1) more = false; }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < FILL_R; ++r) {
+        // every lane of a group takes its leader's base (inactive lanes form their own groups)
+        const int leader = act_r[r] ? __ffs(peers_r[r]) - 1 : (int)lane;
+        const uint32_t b = __shfl_sync(0xffffffffu, base_r[r], leader);
+        if (act_r[r]) {
+            const uint32_t slot = toff_r[r] + b + __popc(peers_r[r] & lt);
+            if ((int64_t)slot < p.cap) p.list[slot] = id;
+        }
+    }
+    while (__any_sync(0xffffffffu, more)) {   // ranges wider than FILL_R tiles
         const int tile = ty * p.ntx + tx;
         const int key = more ? tile * NSLAB + slab : -1;
-        // tile offset loads are independent of the atomic: issue them first
         const uint32_t toff = more ? p.tile_off(tile) : 0u;
         const unsigned peers = __match_any_sync(0xffffffffu, key);
         if (more) {
@@ -115,7 +151,7 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
             uint32_t base = 0;
             if (lane == (unsigned)leader) base = atomicAdd(p.cnt + key, (uint32_t)__popc(peers));
             base = __shfl_sync(peers, base, leader);
-            const uint32_t slot = toff + base + __popc(peers & ((1u << lane) - 1u));
+            const uint32_t slot = toff + base + __popc(peers & lt);
             if ((int64_t)slot < p.cap) p.list[slot] = id;
             if (++tx > tx1) { tx = tx0; if (++ty > ty1) more = false; }
         }

@@ -45,8 +45,13 @@ class ViewBatchRenderer:
     otherwise, e.g. the multi-scale Mip views), plus any other requested
     buffers (fp32 image, depth, winner ...)."""
 
-    def __init__(self, renderer, scene, cams, settings, *, want=("image_rgba8",)):
+    def __init__(self, renderer, scene, cams, settings, *, want=("image_rgba8",), streams: int = 1):
+        """``streams`` > 1 pipelines consecutive views on that many CUDA
+        streams, each with its own frame workspace, so one view's
+        preprocessing/binning overlaps another view's tile kernel."""
         self.r = renderer
+        self.pool = [renderer] + [type(renderer)(renderer.device) for _ in range(max(streams, 1) - 1)]
+        self.streams = [None] + [torch.cuda.Stream(renderer.device) for _ in range(max(streams, 1) - 1)]
         self.scene = scene
         self.cams = list(cams)
         self.settings = settings
@@ -67,8 +72,24 @@ class ViewBatchRenderer:
             self.frames.append(fr)
 
     def render(self, check: bool = False):
-        for c, fr in zip(self.cams, self.frames):
-            self.r.render(self.scene, c, self.settings, frame=fr, check=check)
+        if len(self.pool) == 1:
+            for c, fr in zip(self.cams, self.frames):
+                self.r.render(self.scene, c, self.settings, frame=fr, check=check)
+            return self.rgba
+        main = torch.cuda.current_stream(self.r.device)
+        start = main.record_event()
+        for s in self.streams[1:]:
+            s.wait_event(start)          # outputs may still be read by earlier work on main
+        k = len(self.pool)
+        for v, (c, fr) in enumerate(zip(self.cams, self.frames)):
+            s = self.streams[v % k]
+            if s is None:
+                self.pool[0].render(self.scene, c, self.settings, frame=fr, check=check)
+            else:
+                with torch.cuda.stream(s):
+                    self.pool[v % k].render(self.scene, c, self.settings, frame=fr, check=check)
+        for s in self.streams[1:]:
+            main.wait_stream(s)
         return self.rgba
 
     def overflowed(self) -> bool:
