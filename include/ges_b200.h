@@ -87,6 +87,7 @@ typedef struct ges_scene {
     float *s_s2;          /* n_surfels:     exp(log_scale[1])                  */
     float *s_sh;          /* n_surfels x K x 3                                 */
     int32_t *s_id;        /* n_surfels: source index of packed surfel i        */
+    int32_t *s_pack;      /* n_surfels: packed index of source surfel j        */
     float *g_pos_op;      /* n_gaussians x 4: pos.xyz, eff_opacity             */
     float *g_quat;        /* n_gaussians x 4                                   */
     float *g_scale_eps;   /* n_gaussians x 4: eff_scale (s2=0 for 2D), epsilon */

@@ -45,7 +45,7 @@ class SceneSrc(C.Structure):
 class Scene(C.Structure):
     _fields_ = [("n_surfels", C.c_int64), ("n_gaussians", C.c_int64), ("sh_degree", C.c_int32),
                 ("gaussian_dim", C.c_int32)] + [
-        (n, C.c_void_p) for n in ("s_pos_s1", "s_quat", "s_s2", "s_sh", "s_id", "g_pos_op", "g_quat",
+        (n, C.c_void_p) for n in ("s_pos_s1", "s_quat", "s_s2", "s_sh", "s_id", "s_pack", "g_pos_op", "g_quat",
                                   "g_scale_eps", "g_sh")] + [("bounds", C.c_double * 7)]
 
 

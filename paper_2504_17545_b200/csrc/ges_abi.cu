@@ -66,7 +66,7 @@ int check_cam(const ges_camera_t* c) {
 // Frame workspace layout; base == nullptr only measures.
 struct Frame {
     SurfRec* srec;
-    float4 *s_rgb, *s_nrm;
+    float4* s_rgb;
     void* grec;
     float4* g_nrm;
     uint32_t *cnt_s, *off_s, *cnt_g, *off_g, *chunk_s, *chunk_g, *tickets;
@@ -97,7 +97,6 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, int64_t
     f.chunk_g = c.take<uint32_t>(nchunk);
     f.srec = c.take<SurfRec>(ns);
     f.s_rgb = c.take<float4>(ns);
-    f.s_nrm = c.take<float4>(ns);
     f.grec = c.take<char>(ng * (sc->gaussian_dim == 2 ? sizeof(Gauss2Rec) : sizeof(GaussRec)));
     f.g_nrm = c.take<float4>(ng);
     f.list_s = c.take<uint32_t>((size_t)cap_s);
@@ -162,7 +161,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     if (!do_g) scs.n_gaussians = 0;
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, TILE * grid};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE};
-    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, f.s_rgb, f.s_nrm, f.cnt_s}, s)))
+    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, f.s_rgb, nullptr, f.cnt_s}, s)))
         return cuda_fail(e, "surfel preprocess");
     mark(1);
     if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))
@@ -179,7 +178,12 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     a.layers = st->layers;
     for (int i = 0; i < 3; ++i) a.bg[i] = st->background[i];
     a.rfx = cs.fx; a.rfy = cs.fy; a.rcx = cs.cx; a.rcy = cs.cy;
-    a.srec = f.srec; a.s_rgb = f.s_rgb; a.s_nrm = f.s_nrm; a.s_list = f.list_s; a.sbin = bs;
+    a.srec = f.srec; a.s_rgb = f.s_rgb; a.s_list = f.list_s; a.sbin = bs;
+    a.s_quat = reinterpret_cast<const float4*>(sc->s_quat);
+    a.s_pos = reinterpret_cast<const float4*>(sc->s_pos_s1);
+    a.s_pack = sc->s_pack;
+    for (int i = 0; i < 9; ++i) a.R[i] = cs.R[i];
+    for (int i = 0; i < 3; ++i) a.t[i] = cs.t[i];
     a.slabs = slabs;
     a.gfx = cg.fx; a.gfy = cg.fy; a.gcx = cg.cx; a.gcy = cg.cy;
     a.grec = f.grec; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg;
@@ -210,7 +214,7 @@ const char* ges_last_error(void) { return g_err.c_str(); }
 size_t ges_scene_bytes(int64_t ns, int64_t ng, int32_t deg) {
     if (deg < 0 || deg > 3 || ns < 0 || ng < 0) return 0;
     size_t K = (size_t)(deg + 1) * (deg + 1);
-    return al(ns * 16) + al(ns * 16) + al(ns * 4) + al(ns * K * 12) + al(ns * 4) + al(ng * 16) * 3 +
+    return al(ns * 16) + al(ns * 16) + al(ns * 4) + al(ns * K * 12) + al(ns * 4) * 2 + al(ng * 16) * 3 +
            al(ng * K * 12);
 }
 
@@ -231,6 +235,7 @@ int ges_scene_pack(const ges_scene_src_t* src, void* blob, size_t blob_bytes, ge
     sc.s_s2 = c.take<float>(ns);
     sc.s_sh = c.take<float>(ns * K * 3);
     sc.s_id = c.take<int32_t>(ns);
+    sc.s_pack = c.take<int32_t>(ns);
     for (int k = 0; k < 7; ++k) sc.bounds[k] = src->bounds[k];
     sc.g_pos_op = c.take<float>(ng * 4);
     sc.g_quat = c.take<float>(ng * 4);

@@ -38,8 +38,10 @@ struct TileArgs {
     // surfel pass (resolution = ss * base)
     double rfx, rfy, rcx, rcy;
     const SurfRec* srec;
-    const float4* s_rgb;
-    const float4* s_nrm;
+    const float4* s_rgb;          // view colour per source surfel id
+    const float4 *s_quat, *s_pos; // packed scene (n_vis of winners, on demand)
+    const int32_t* s_pack;        // source id -> packed index
+    double R[9], t[3];            // world -> camera
     const uint32_t* s_list;
     BinPass sbin;                 // tile offsets; cnt = per-(tile, slab) ends relative to the tile
     // Gaussian pass (base resolution)

@@ -135,6 +135,7 @@ __global__ void k_pack_prims(ges_scene_src_t src, ges_scene_t dst) {
         const double* q = src.s_quat + 4 * o;
         const double* l = src.s_log_scale + 2 * o;
         dst.s_id[i] = (int32_t)o;
+        dst.s_pack[o] = (int32_t)i;
         double nrm = 1.0 / sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
         reinterpret_cast<float4*>(dst.s_pos_s1)[i] = make_float4(p[0], p[1], p[2], exp(l[0]));
         reinterpret_cast<float4*>(dst.s_quat)[i] =
@@ -227,8 +228,7 @@ __global__ void __launch_bounds__(256) k_surfel_prep(ges_scene_t sc, CamK cam, G
         float3 col = sh_color<DEG>(sc.s_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
                                    (float)(dv.y * inv), (float)(dv.z * inv));
         o.rgb[sid] = make_float4(col.x, col.y, col.z, 0.f);   // indexed by source id (winner ids)
-        double sgn = dot(n, q) < 0.0 ? 1.0 : -1.0;   // forward.py:152
-        o.nrm[sid] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);
+        // n_vis (forward.py:152) is evaluated for winners only, when requested
     } else {
         rec.r0 = rec.r1 = rec.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
         rec.r3 = make_float4(0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)),

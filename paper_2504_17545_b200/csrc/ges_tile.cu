@@ -94,6 +94,25 @@ __device__ __forceinline__ void store_rgba8(uint8_t* dst, int64_t pix, float3 c)
     reinterpret_cast<uint32_t*>(dst)[pix] = q(c.x) | (q(c.y) << 8) | (q(c.z) << 16) | (255u << 24);
 }
 
+// Camera-facing plane normal of source surfel `sid` (forward.py:148, :152),
+// from the packed quaternion in float64 like the reference's frames.
+__device__ __forceinline__ float3 surfel_nvis(const TileArgs& a, uint32_t sid) {
+    const uint32_t pidx = (uint32_t)__ldg(a.s_pack + sid);
+    const float4 qf = __ldg(a.s_quat + pidx), p = __ldg(a.s_pos + pidx);
+    double w = qf.x, x = qf.y, y = qf.z, z = qf.w;
+    const double inv = 1.0 / sqrt(w * w + x * x + y * y + z * z);
+    w *= inv; x *= inv; y *= inv; z *= inv;
+    const double c[3] = {2 * (x * z + w * y), 2 * (y * z - w * x), 1 - 2 * (x * x + y * y)};
+    double n[3], q[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        n[i] = a.R[3 * i] * c[0] + a.R[3 * i + 1] * c[1] + a.R[3 * i + 2] * c[2];
+        q[i] = a.R[3 * i] * p.x + a.R[3 * i + 1] * p.y + a.R[3 * i + 2] * p.z + a.t[i];
+    }
+    const double sg = n[0] * q[0] + n[1] * q[1] + n[2] * q[2] < 0.0 ? 1.0 : -1.0;
+    return make_float3((float)(n[0] * sg), (float)(n[1] * sg), (float)(n[2] * sg));
+}
+
 template <int SS, int MODE, int GK, bool GEOM>
 __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
     __shared__ TileSmem sm;
@@ -236,7 +255,7 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                 a.out.s_color[3 * pix + 2] = cs.z;
             }
             if (a.out.s_normal) {
-                float4 n = cov ? __ldg(a.s_nrm + (uint32_t)best[0]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float3 n = cov ? surfel_nvis(a, (uint32_t)best[0]) : make_float3(0.f, 0.f, 0.f);
                 a.out.s_normal[3 * pix] = n.x; a.out.s_normal[3 * pix + 1] = n.y;
                 a.out.s_normal[3 * pix + 2] = n.z;
             }
