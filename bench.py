@@ -308,7 +308,7 @@ def run_gpu(args, rank, world, local_rank):
                                          rend.cap_s, rend.cap_g, C.c_void_p(fr.status.data_ptr()),
                                          C.c_void_p(stream.cuda_stream), arr), "profiled render")
     torch.cuda.synchronize()
-    names = ["memset+surfel_prep", "gauss_prep", "tile_scan", "tile_fill", "tile_render"]
+    names = ["memsets", "prep", "tile_scan", "tile_fill", "tile_render"]
     phase = {n: statistics.mean(row[k].elapsed_time(row[k + 1]) for row in evs) for k, n in enumerate(names)}
     frame_ms = statistics.mean(row[0].elapsed_time(row[5]) for row in evs)
 
@@ -388,7 +388,7 @@ def run_gpu(args, rank, world, local_rank):
         "config": base_config(cfg, per_rank, world, args.ss),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "unit_of_work": "one frame (ges_render: 5 kernels)",
+                     "unit_of_work": "one frame (ges_render: 5 kernels + 2 memsets)",
                      "b_alg_bytes_per_frame": balg, "frame_ms": frame_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                      "phase_ms": phase, "dominant": max(phase, key=phase.get)},

@@ -138,9 +138,9 @@ int ges_render(const ges_scene_t *scene, const ges_camera_t *cam,
                void *stream);
 
 /* ges_render that also records 6 CUDA events (cudaEvent_t, may be NULL) on
- * `stream` at the phase boundaries: [0] frame start, [1] after surfel
- * preprocess, [2] after Gaussian preprocess, [3] after the tile scan,
- * [4] after the tile fill, [5] after the fused tile kernel. */
+ * `stream` at the phase boundaries: [0] frame start, [1] after the counter
+ * memsets, [2] after the surfel and Gaussian preprocess kernels, [3] after
+ * the tile scan, [4] after the tile fill, [5] after the fused tile kernel. */
 int ges_render_profiled(const ges_scene_t *scene, const ges_camera_t *cam,
                         const ges_settings_t *st, const ges_outputs_t *out,
                         void *workspace, size_t ws_bytes, int64_t surfel_pair_cap,

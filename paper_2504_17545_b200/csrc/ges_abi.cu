@@ -153,6 +153,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     if ((e = cudaMemsetAsync(f.cnt_s, 0, f.zero_bytes, s)) != cudaSuccess) return cuda_fail(e, "memset counts");
     if ((e = cudaMemsetAsync(status, 0, sizeof(ges_frame_status_t), s)) != cudaSuccess)
         return cuda_fail(e, "memset status");
+    mark(1);
     CamK cs = make_cam(*cam, grid), cg = make_cam(*cam, 1);
     const SlabMap slabs = slab_map(*sc, cs);
     Grid gs{cs.W, cs.H, TILE * grid, f.ntx, f.nty, slabs}, gg{cg.W, cg.H, TILE, f.ntx, f.nty, slabs};
@@ -163,7 +164,6 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE};
     if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, f.s_rgb, nullptr, f.cnt_s}, s)))
         return cuda_fail(e, "surfel preprocess");
-    mark(1);
     if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))
         return cuda_fail(e, "gaussian preprocess");
     mark(2);
