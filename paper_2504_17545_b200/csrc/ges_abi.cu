@@ -177,7 +177,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     a.W = cam->width; a.H = cam->height; a.ntx = f.ntx; a.nty = f.nty;
     a.layers = st->layers;
     for (int i = 0; i < 3; ++i) a.bg[i] = st->background[i];
-    a.rfx = cs.fx; a.rfy = cs.fy; a.rcx = cs.cx; a.rcy = cs.cy;
+    a.rcx = (float)cs.cx; a.rcy = (float)cs.cy; a.rifx = (float)(1.0 / cs.fx); a.rify = (float)(1.0 / cs.fy);
     a.srec = f.srec; a.s_rgb = f.s_rgb; a.s_list = f.list_s; a.sbin = bs;
     a.s_quat = reinterpret_cast<const float4*>(sc->s_quat);
     a.s_pos = reinterpret_cast<const float4*>(sc->s_pos_s1);
@@ -185,7 +185,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     for (int i = 0; i < 9; ++i) a.R[i] = cs.R[i];
     for (int i = 0; i < 3; ++i) a.t[i] = cs.t[i];
     a.slabs = slabs;
-    a.gfx = cg.fx; a.gfy = cg.fy; a.gcx = cg.cx; a.gcy = cg.cy;
+    a.gcx = (float)cg.cx; a.gcy = (float)cg.cy; a.gifx = (float)(1.0 / cg.fx); a.gify = (float)(1.0 / cg.fy);
     a.grec = f.grec; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg;
     a.ds_in = ds_in;
     a.out = *out;

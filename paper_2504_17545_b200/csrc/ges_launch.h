@@ -36,7 +36,7 @@ struct TileArgs {
     int layers;
     float bg[3];
     // surfel pass (resolution = ss * base)
-    double rfx, rfy, rcx, rcy;
+    float rcx, rcy, rifx, rify;   // principal point and 1/f of the surfel pass
     const SurfRec* srec;
     const float4* s_rgb;          // view colour per source surfel id
     const float4 *s_quat, *s_pos; // packed scene (n_vis of winners, on demand)
@@ -45,7 +45,7 @@ struct TileArgs {
     const uint32_t* s_list;
     BinPass sbin;                 // tile offsets; cnt = per-(tile, slab) ends relative to the tile
     // Gaussian pass (base resolution)
-    double gfx, gfy, gcx, gcy;
+    float gcx, gcy, gifx, gify;
     const void* grec;
     const float4* g_rgb;          // 2D Gaussians: colours
     const float4* g_nrm;          // with_geometry normals

@@ -36,12 +36,11 @@ struct __align__(16) TileSmem {
     uint32_t slab_end[NSLAB];   // this tile's slab ends (relative list positions)
 };
 
-// Slab holding relative list position `rel`, and the CTA-wide max of the
-// per-warp depths in sm.wmax (both read from shared memory: CTA-uniform).
-__device__ __forceinline__ int slab_at(const TileSmem& sm, uint32_t rel) {
-    int s = 0;
-#pragma unroll
-    for (int k = 0; k < NSLAB - 1; ++k) s += sm.slab_end[k] <= rel;
+// Advance `s` to the slab holding relative list position `rel` (positions
+// only grow), and the CTA-wide max of the per-warp depths in sm.wmax (both
+// read from shared memory: CTA-uniform).
+__device__ __forceinline__ int slab_at(const TileSmem& sm, uint32_t rel, int s) {
+    while (s < NSLAB - 1 && sm.slab_end[s] <= rel) ++s;
     return s;
 }
 __device__ __forceinline__ float tile_max(const TileSmem& sm) {
@@ -84,8 +83,8 @@ __device__ __forceinline__ float3 im_of(const TileArgs& a, float3 cs, float w, f
         }
         return make_float3(a.bg[0], a.bg[1], a.bg[2]);
     }
-    float dn = 1.0f + w;
-    return make_float3((cs.x + cr) / dn, (cs.y + cg) / dn, (cs.z + cb) / dn);
+    const float r = 1.0f / (1.0f + w);
+    return make_float3((cs.x + cr) * r, (cs.y + cg) * r, (cs.z + cb) * r);
 }
 
 // Display/send-buffer form, datasets.py:54-56: clip(x*255+0.5, 0, 255) -> u8.
@@ -145,7 +144,8 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
 #pragma unroll
             for (int sx = 0; sx < SS; ++sx) {
                 int X = SS * x + sx, Y = SS * y + sy;
-                float dxn = (float)((X + 0.5 - a.rcx) / a.rfx), dyn = (float)((Y + 0.5 - a.rcy) / a.rfy);
+                // |d| of the pixel ray only sets the near-parallel threshold 1e-8|d|
+                const float dxn = ((float)X + 0.5f - a.rcx) * a.rifx, dyn = ((float)Y + 0.5f - a.rcy) * a.rify;
                 pe[sy * SS + sx] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
                 best[sy * SS + sx] = ~0ull;
                 tb[sy * SS + sx] = inside ? INFINITY : 0.f;
@@ -162,9 +162,11 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
         __syncthreads();
         const int ox = tx * TILE * SS, oy = ty * TILE * SS;
         const uint32_t beg = a.sbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
+        int slab = 0;
         for (uint32_t base = beg; base < end; base += NB) {
             // slabs are near-to-far: stop once the next slab lies behind every hit so far
-            if (a.slabs.lower(slab_at(sm, base - beg)) > tile_max(sm)) break;
+            slab = slab_at(sm, base - beg, slab);
+            if (a.slabs.lower(slab) > tile_max(sm)) break;
             const int nb = min((uint32_t)NB, end - base);
             if ((int)threadIdx.x < nb) {
                 const uint32_t id = a.s_list[base + threadIdx.x];
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                 const int e = c + lane;
                 const bool want = e < nb && ((sm.pm[e] >> warp) & 1u) && !(sm.zm[e] > wmx);
                 uint32_t vote = __ballot_sync(0xffffffffu, want);
+                if (!vote) continue;     // nothing tested: the patch depth is unchanged
                 while (vote) {
                     const int j = c + __ffs(vote) - 1;
                     vote &= vote - 1;
@@ -275,14 +278,16 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
         const float lx = (float)plx, ly = (float)ply;
         float pe = 0.f;
         if constexpr (GK == 2) {
-            float dxn = (float)((x + 0.5 - a.gcx) / a.gfx), dyn = (float)((y + 0.5 - a.gcy) / a.gfy);
+            const float dxn = ((float)x + 0.5f - a.gcx) * a.gifx, dyn = ((float)y + 0.5f - a.gcy) * a.gify;
             pe = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
         }
         const int ox = tx * TILE, oy = ty * TILE;
         const uint32_t beg = a.gbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
+        int slab = 0;
         for (uint32_t base = beg; base < end; base += NB) {
             // keys (depth - eps) are binned near-to-far: the rest fail every gate
-            if (a.slabs.lower(slab_at(sm, base - beg)) > dmax) break;
+            slab = slab_at(sm, base - beg, slab);
+            if (a.slabs.lower(slab) > dmax) break;
             const int nb = min((uint32_t)NB, end - base);
             if ((int)threadIdx.x < nb) {
                 const uint32_t id = a.g_list[base + threadIdx.x];

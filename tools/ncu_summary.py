@@ -63,6 +63,37 @@ def sass(rep, top):
     return res
 
 
+def lines(rep, kernel_regex, top):
+    """Per CUDA source line: warp-level instructions executed and stall samples."""
+    out = ncu("-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{kernel_regex}")
+    rows = list(csv.reader(io.StringIO(out)))
+    agg = []
+    cur_file = None
+    hdr = None
+    for r in rows:
+        if not r:
+            continue
+        if r[0] == "File Path":
+            cur_file = r[1].split("/")[-1]
+            continue
+        if r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or r[0] in ("Function Name",) or not r[0]:
+            continue
+        try:
+            ex = int(r[hdr.index("Instructions Executed")] or 0)
+            st = int(r[hdr.index("Warp Stall Sampling (All Samples)")] or 0)
+        except (ValueError, IndexError):
+            continue
+        agg.append((ex, st, f"{cur_file}:{r[0]}", r[1].strip()[:80]))
+    tot_ex = sum(a[0] for a in agg) or 1
+    tot_st = sum(a[1] for a in agg) or 1
+    print(f"total warp-instructions {tot_ex}, stall samples {tot_st}")
+    for ex, st, loc, src in sorted(agg, key=lambda a: -a[0])[:top]:
+        print(f"  {ex / tot_ex:6.1%} inst {st / tot_st:6.1%} stall  {loc:22s} {src}")
+
+
 def launches(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
@@ -81,9 +112,14 @@ def main():
     ap.add_argument("rep", nargs="?")
     ap.add_argument("--sass", type=int, default=0)
     ap.add_argument("--launches")
+    ap.add_argument("--lines", help="kernel regex: per-source-line breakdown")
+    ap.add_argument("--top", type=int, default=30)
     a = ap.parse_args()
     if a.launches:
         launches(a.launches)
+    if a.lines:
+        lines(a.rep, a.lines, a.top)
+        return
     if a.rep:
         for d, u in raw(a.rep):
             print("==", d.get("Kernel Name", "?")[:100])
