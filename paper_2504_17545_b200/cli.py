@@ -1,0 +1,149 @@
+"""Command line front end for the GPU render path,
+mirroring the reference's ``ges render`` / ``ges path`` (``cli.py:126-174``):
+
+  python -m paper_2504_17545_b200 render --model m.ges --camera cams.json --out o.png
+         [--view K] [--ss {1,4}] [--layer {full,surfels,gaussians}] [--mip] [--background R G B]
+  python -m paper_2504_17545_b200 path --model m.ges --camera cams.json --out DIR
+         [--frames N] [--radius-scale S] [--ss {1,4}]
+
+Camera files use the reference's dataset entries ({fx, fy, cx, cy, width,
+height, w2c[16]}, ``datasets.py:125-137``).  Exit codes: 0 ok, 1 error,
+2 usage (argparse).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+
+from .gesfile import load_ges
+from .types import Camera, look_at
+
+
+def camera_from_entry(e: dict) -> Camera:
+    w2c = np.array(e["w2c"], dtype=np.float64).reshape(4, 4)
+    return Camera(e["fx"], e["fy"], e["cx"], e["cy"], int(e["width"]), int(e["height"]), w2c)
+
+
+def camera_to_entry(c) -> dict:
+    return {"fx": c.fx, "fy": c.fy, "cx": c.cx, "cy": c.cy, "width": c.width, "height": c.height,
+            "w2c": [float(x) for x in np.asarray(c.world_to_camera).reshape(-1)]}
+
+
+def save_image(path, img):
+    """clip(x*255+0.5) -> 8-bit PNG (datasets.py:54-56)."""
+    from PIL import Image
+    arr = np.clip(np.asarray(img) * 255.0 + 0.5, 0, 255).astype(np.uint8)
+    Image.fromarray(arr).save(path)
+
+
+def _settings(args):
+    from .forward import RenderSettings
+    layers = {"full": "full", "surfels": "surfels_only", "gaussians": "gaussians_only"}[args.layer]
+    return RenderSettings(supersample=args.ss, layers=layers, mip=args.mip,
+                          background=tuple(args.background))
+
+
+def _load_cams(path):
+    spec = json.loads(Path(path).read_text())
+    return spec if isinstance(spec, list) else [spec]
+
+
+def cmd_render(args) -> int:
+    from .forward import render
+    scene, _ = load_ges(args.model)
+    cam = camera_from_entry(_load_cams(args.camera)[args.view])
+    out = render(scene, cam, _settings(args))
+    save_image(Path(args.out), out.image)
+    print(f"wrote {args.out}")
+    return 0
+
+
+def orbit_path(base: Camera, frames: int, radius_scale: float = 1.0):
+    """Frames on a circle through the base camera's eye around its look-at
+    point at the same distance (a multi-view batch like cli.py:154-174)."""
+    R = np.asarray(base.world_to_camera)[:3, :3]
+    eye = np.asarray(base.position)
+    fwd = R[2]
+    target = eye + fwd * np.linalg.norm(eye) * 1.0
+    rad = np.linalg.norm(eye - target) * radius_scale
+    off = eye - target
+    ang0 = math.atan2(off[1], off[0])
+    cams = []
+    for k in range(frames):
+        a = ang0 + 2 * math.pi * k / frames
+        e = target + np.array([rad * math.cos(a), rad * math.sin(a), off[2]])
+        cams.append(Camera(base.fx, base.fy, base.cx, base.cy, base.width, base.height, look_at(e, target)))
+    return cams
+
+
+def cmd_path(args) -> int:
+    import torch
+
+    from .forward import _device
+    from .multiview import ViewBatchRenderer
+    from .renderer import SCENE_CACHE, default_renderer
+    scene, _ = load_ges(args.model)
+    base = camera_from_entry(_load_cams(args.camera)[0])
+    cams = orbit_path(base, args.frames, args.radius_scale)
+    out_dir = Path(args.out)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    dev = _device()
+    ds = SCENE_CACHE.get(scene, dev)
+    vb = ViewBatchRenderer(default_renderer(dev), ds, cams, _settings(args), want=("image_rgba8",))
+    for c, fr in zip(vb.cams, vb.frames):          # size the pair lists, then render the batch
+        vb.r.render(ds, c, vb.settings, frame=fr, check=True)
+    rgba = vb.render(check=False)
+    torch.cuda.synchronize(dev)
+    if vb.overflowed():
+        rgba = vb.render(check=True)
+    from PIL import Image
+    frames = rgba if isinstance(rgba, list) else list(rgba.unbind(0))
+    for k, f in enumerate(frames):
+        Image.fromarray(f[..., :3].cpu().numpy()).save(out_dir / f"frame_{k:04d}.png")
+    (out_dir / "path.json").write_text(json.dumps([camera_to_entry(c) for c in cams], indent=1))
+    print(f"wrote {len(frames)} frames to {out_dir}")
+    return 0
+
+
+def build_parser():
+    p = argparse.ArgumentParser(prog="paper_2504_17545_b200")
+    sub = p.add_subparsers(dest="cmd", required=True)
+
+    def common(sp):
+        sp.add_argument("--model", required=True)
+        sp.add_argument("--camera", required=True)
+        sp.add_argument("--out", required=True)
+        sp.add_argument("--ss", type=int, default=4, choices=[1, 4])
+        sp.add_argument("--layer", default="full", choices=["full", "surfels", "gaussians"])
+        sp.add_argument("--mip", action="store_true")
+        sp.add_argument("--background", type=float, nargs=3, default=[0.0, 0.0, 0.0])
+
+    r = sub.add_parser("render", help="render one view of a .ges model")
+    common(r)
+    r.add_argument("--view", type=int, default=0)
+    r.set_defaults(fn=cmd_render)
+    pa = sub.add_parser("path", help="render an orbit of views as a batch")
+    common(pa)
+    pa.add_argument("--frames", type=int, default=16)
+    pa.add_argument("--radius-scale", type=float, default=1.0)
+    pa.set_defaults(fn=cmd_path)
+    return p
+
+
+def main(argv=None) -> int:
+    args = build_parser().parse_args(argv)
+    try:
+        return args.fn(args)
+    except Exception as e:   # noqa: BLE001  (reference CLI maps failures to exit 1, cli.py:255-262)
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

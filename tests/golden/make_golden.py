@@ -96,8 +96,37 @@ def cases():
     yield "config1", S.config_scene(1), S.config_cameras(1)[0], {}
 
 
+def ges_goldens():
+    """.ges fixtures written by the reference's export_ges (gesfile.py:42-76),
+    with the reference's load_ges result and its float64 render of the
+    float32-quantised scene."""
+    from ges.gesfile import export_ges, load_ges
+    r = np.random.default_rng(41)
+    sc3 = Scene(S.random_surfels(r, 120, 3, scale_range=(0.05, 0.15)),
+                S.random_gaussians(r, 60, 3, scale_range=(0.03, 0.1)), 3, Stage.FROZEN)
+    sc3 = Scene(sc3.surfels, S.mip_world_filter(sc3.gaussians, [S.make_camera(64, 64)]), 3, Stage.FROZEN)
+    sc2 = S.random_scene(np.random.default_rng(42), 40, 30, degree=1, kind=GaussianKind.TWO_D)
+    cam = S.make_camera(48, 40)
+    for name, sc, rgb in (("ges_3d_deg3", sc3, False), ("ges_2d_rgb", sc2, True)):
+        path = os.path.join(HERE, name + ".ges")
+        export_ges(to_ref(sc), path, rgb_surfels=rgb)
+        rs, info = load_ges(path)
+        out = render(rs, to_ref_cam(cam), RenderSettings(dtype=np.float64, threads=1))
+        np.savez_compressed(os.path.join(HERE, name + "_load.npz"),
+                            sp=rs.surfels.pos, sq=rs.surfels.quat, sl=rs.surfels.log_scale,
+                            ssh=rs.surfels.sh, gp=rs.gaussians.pos, go=rs.gaussians.raw_opacity,
+                            gq=rs.gaussians.quat, gl=rs.gaussians.log_scale, gsh=rs.gaussians.sh,
+                            eps=info["epsilon"], flags=info["flags"],
+                            fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy, width=cam.width,
+                            height=cam.height, w2c=cam.world_to_camera,
+                            image=out.image, s_winner=out.surfels.winner, s_depth=out.surfels.depth)
+        print(name, os.path.getsize(path), "bytes")
+
+
 def main():
     only = set(sys.argv[1:])
+    if not only or "ges" in only:
+        ges_goldens()
     for name, scene, cam, st in cases():
         if only and name not in only:
             continue

@@ -1,0 +1,87 @@
+"""GPU tests of the callers either side of the path:
+.ges -> device render, the CLI, and the winner-map consumer covering_counts."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2504_17545_b200 as G  # noqa: E402
+from paper_2504_17545_b200 import cli, scenes as S  # noqa: E402
+from paper_2504_17545_b200.consumers import covering_counts  # noqa: E402
+from paper_2504_17545_b200.gesfile import load_ges  # noqa: E402
+from paper_2504_17545_b200.types import Camera  # noqa: E402
+from golden_io import settings_ns  # noqa: E402
+from oracle import ges_oracle as O  # noqa: E402
+from parity import assert_parity, compare  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _cam(z):
+    return Camera(float(z["fx"]), float(z["fy"]), float(z["cx"]), float(z["cy"]), int(z["width"]),
+                  int(z["height"]), z["w2c"])
+
+
+@pytest.mark.parametrize("name", ["ges_3d_deg3", "ges_2d_rgb"])
+def test_ges_file_renders_like_reference(name):
+    scene, _ = load_ges(os.path.join(GOLD, name + ".ges"))
+    z = np.load(os.path.join(GOLD, name + "_load.npz"))
+    cam = _cam(z)
+    out = G.render(scene, cam)
+    ora = O.render(scene, cam, settings_ns({}), ties=True)
+    rep = compare(dict(image=out.image, s_winner=out.surfels.winner, s_depth=out.surfels.depth),
+                  dict(image=z["image"], s_winner=z["s_winner"], s_depth=z["s_depth"]), ora.tie)
+    assert_parity(rep)
+
+
+def test_cli_render_writes_png(tmp_path):
+    from PIL import Image
+    z = np.load(os.path.join(GOLD, "ges_3d_deg3_load.npz"))
+    cam = _cam(z)
+    (tmp_path / "cams.json").write_text(json.dumps([cli.camera_to_entry(cam)]))
+    rc = cli.main(["render", "--model", os.path.join(GOLD, "ges_3d_deg3.ges"), "--camera",
+                   str(tmp_path / "cams.json"), "--out", str(tmp_path / "o.png"), "--ss", "1"])
+    assert rc == 0
+    img = np.asarray(Image.open(tmp_path / "o.png")).astype(int)
+    ref = np.clip(z["image"] * 255.0 + 0.5, 0, 255).astype(int)
+    scene, _ = load_ges(os.path.join(GOLD, "ges_3d_deg3.ges"))
+    tie = O.render(scene, cam, settings_ns({}), ties=True).tie
+    assert np.abs(img - ref)[~tie].max() <= 1
+
+
+def test_cli_path_and_errors(tmp_path):
+    z = np.load(os.path.join(GOLD, "ges_2d_rgb_load.npz"))
+    (tmp_path / "cams.json").write_text(json.dumps(cli.camera_to_entry(_cam(z))))
+    rc = cli.main(["path", "--model", os.path.join(GOLD, "ges_2d_rgb.ges"), "--camera",
+                   str(tmp_path / "cams.json"), "--out", str(tmp_path / "p"), "--frames", "5"])
+    assert rc == 0
+    assert len(list((tmp_path / "p").glob("frame_*.png"))) == 5
+    assert cli.main(["render", "--model", str(tmp_path / "missing.ges"), "--camera",
+                     str(tmp_path / "cams.json"), "--out", str(tmp_path / "x.png")]) == 1
+
+
+def test_covering_counts_match_oracle_winners():
+    scene = S.random_scene(np.random.default_rng(8), 60, 0, degree=1)
+    cams = S.orbit_views(3, 48, 40)
+    got = covering_counts(scene, cams)
+    best = np.zeros(60, np.int64)
+    slack = np.zeros(60, np.int64)
+    for c in cams:
+        o = O.rasterize_surfels(scene, c, settings_ns({}), ties=True)
+        w = o.winner.reshape(-1)
+        best = np.maximum(best, np.bincount(w[w >= 0], minlength=60))
+        tw = o.winner[o.tie]
+        slack += np.bincount(tw[tw >= 0], minlength=60) + int(o.tie.sum())
+    assert np.all(np.abs(got - best) <= slack)
+    assert got.sum() > 0
