@@ -123,9 +123,11 @@ SlabMap slab_map(const ges_scene_t& sc, const CamK& c) {
     if (!(zhi > zlo + 1e-9)) {   // degenerate or missing bounds: everything in slab 0
         m.zlo = 0.f;
         m.inv_dz = 0.f;
+        m.dz = 0.f;
     } else {
         m.zlo = (float)zlo;
         m.inv_dz = (float)(NSLAB / (zhi - zlo));
+        m.dz = (float)((zhi - zlo) / NSLAB);
     }
     return m;
 }

@@ -63,10 +63,11 @@ struct SlabMap {
         float f = floorf((key - zlo) * inv_dz);
         return f > 0.f ? (f < (float)(NSLAB - 1) ? (int)f : NSLAB - 1) : 0;   // NaN -> 0
     }
+    float dz;   // 1 / inv_dz
     // every key binned into slab s is >= this bound (slab 0 also takes keys below zlo)
     __device__ __forceinline__ float lower(int s) const {
         if (s == 0 || !(inv_dz > 0.f)) return -INFINITY;
-        float b = zlo + (float)s / inv_dz;
+        const float b = fmaf((float)s, dz, zlo);
         return b - (fabsf(b) * 1e-5f + 1e-6f);
     }
 };

@@ -30,18 +30,19 @@ constexpr int NB = TILE_PX;     // batch = one primitive per thread
 
 struct __align__(16) TileSmem {
     float4 st[5][NB];           // staged per-primitive coefficients
-    float zm[NB];               // surfels: conservative nearest depth of the disc
-    uint8_t pm[NB];             // warp-patch masks
+    uint8_t pm[NB];             // Gaussians: warp-patch masks
+    uint32_t zp[NB];            // surfels: nearest disc depth with the low byte = warp-patch mask
     float wmax[NWARP];          // per-warp max depth (surfels: current hits; Gaussians: final)
     uint32_t slab_end[NSLAB];   // this tile's slab ends (relative list positions)
 };
 
-// Advance `s` to the slab holding relative list position `rel` (positions
-// only grow), and the CTA-wide max of the per-warp depths in sm.wmax (both
-// read from shared memory: CTA-uniform).
-__device__ __forceinline__ int slab_at(const TileSmem& sm, uint32_t rel, int s) {
-    while (s < NSLAB - 1 && sm.slab_end[s] <= rel) ++s;
-    return s;
+// Lower depth bound of the slab holding relative list position `rel` (slab
+// ends are non-decreasing, so the slab index is the number of ends <= rel:
+// one vote per warp) and the CTA-wide max of the per-warp depths in sm.wmax.
+// Both read shared memory only, so every warp gets the same answer.
+__device__ __forceinline__ float slab_floor(const TileSmem& sm, const SlabMap& m, uint32_t rel, int lane) {
+    const bool le = lane < NSLAB - 1 && sm.slab_end[lane] <= rel;
+    return m.lower(__popc(__ballot_sync(0xffffffffu, le)));
 }
 __device__ __forceinline__ float tile_max(const TileSmem& sm) {
     float m = sm.wmax[0];
@@ -66,6 +67,14 @@ __device__ __forceinline__ uint32_t patch_mask(int x0, int x1, int y0, int y1) {
     for (int r = 0; r < 4; ++r)
         if ((my >> r) & 1u) m |= mx << (2 * r);
     return m;
+}
+
+// Nearest disc depth and 8-bit patch mask in one word: the depth rounded DOWN
+// to 15 mantissa bits (conservative for culling), the mask in the low byte.
+__device__ __forceinline__ uint32_t zkey_mask(float z, uint32_t mask) {
+    uint32_t b = __float_as_uint(z);
+    if (!(z >= 0.f)) b = __float_as_uint(-3.0e38f);   // negative / NaN: never culled
+    return (b & ~0xFFu) | mask;
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -117,8 +126,8 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
     __shared__ TileSmem sm;
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = blockIdx.x;
-    const int tx = tile % a.ntx, ty = tile / a.ntx;
+    const int tx = blockIdx.x, ty = blockIdx.y;
+    const int tile = ty * a.ntx + tx;
     const int plx = (warp & 1) * 8 + (lane & 7), ply = (warp >> 1) * 4 + (lane >> 3);
     const int x = tx * TILE + plx, y = ty * TILE + ply;
     const bool inside = x < a.W && y < a.H;
@@ -162,11 +171,9 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
         __syncthreads();
         const int ox = tx * TILE * SS, oy = ty * TILE * SS;
         const uint32_t beg = a.sbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
-        int slab = 0;
         for (uint32_t base = beg; base < end; base += NB) {
             // slabs are near-to-far: stop once the next slab lies behind every hit so far
-            slab = slab_at(sm, base - beg, slab);
-            if (a.slabs.lower(slab) > tile_max(sm)) break;
+            if (slab_floor(sm, a.slabs, base - beg, lane) > tile_max(sm)) break;
             const int nb = min((uint32_t)NB, end - base);
             if ((int)threadIdx.x < nb) {
                 const uint32_t id = a.s_list[base + threadIdx.x];
@@ -189,13 +196,13 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                 sm.st[0][threadIdx.x] = make_float4(d0, dx_, dy_, nq);
                 sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
                 sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.w, r3.x);   // r3.w: source id
-                sm.zm[threadIdx.x] = r3.x;
-                sm.pm[threadIdx.x] = (uint8_t)mask;
+                sm.zp[threadIdx.x] = zkey_mask(r3.x, mask);
             }
             __syncthreads();
             for (int c = 0; c < nb; c += 32) {
                 const int e = c + lane;
-                const bool want = e < nb && ((sm.pm[e] >> warp) & 1u) && !(sm.zm[e] > wmx);
+                const uint32_t zp = e < nb ? sm.zp[e] : 0u;
+                const bool want = ((zp >> warp) & 1u) && !(__uint_as_float(zp & ~0xFFu) > wmx);
                 uint32_t vote = __ballot_sync(0xffffffffu, want);
                 if (!vote) continue;     // nothing tested: the patch depth is unchanged
                 while (vote) {
@@ -283,11 +290,9 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
         }
         const int ox = tx * TILE, oy = ty * TILE;
         const uint32_t beg = a.gbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
-        int slab = 0;
         for (uint32_t base = beg; base < end; base += NB) {
             // keys (depth - eps) are binned near-to-far: the rest fail every gate
-            slab = slab_at(sm, base - beg, slab);
-            if (a.slabs.lower(slab) > dmax) break;
+            if (slab_floor(sm, a.slabs, base - beg, lane) > dmax) break;
             const int nb = min((uint32_t)NB, end - base);
             if ((int)threadIdx.x < nb) {
                 const uint32_t id = a.g_list[base + threadIdx.x];
@@ -415,7 +420,7 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
 
 template <int SS, int MODE>
 static void launch_kind(const TileArgs& a, int g_kind, bool geom, cudaStream_t s) {
-    unsigned nt = (unsigned)(a.ntx * a.nty);
+    const dim3 nt((unsigned)a.ntx, (unsigned)a.nty);
     if (g_kind == 2) {
         if (geom) k_tile<SS, MODE, 2, true><<<nt, NB, 0, s>>>(a);
         else k_tile<SS, MODE, 2, false><<<nt, NB, 0, s>>>(a);
