@@ -193,7 +193,7 @@ cudaError_t launch_pack(const ges_scene_src_t& src, const ges_scene_t& dst, cuda
 // ---------------------------------------------------------------- K1 surfels
 // forward.py:148-158 (frames, colour, n_vis, cull, bounds, ranges) for one surfel.
 template <int DEG>
-__global__ void __launch_bounds__(256) k_surfel_prep(ges_scene_t sc, CamK cam, Grid g, PrepOut o) {
+__global__ void __launch_bounds__(256, 4) k_surfel_prep(ges_scene_t sc, CamK cam, Grid g, PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_surfels;
     if (!valid_thread) i = sc.n_surfels - 1;   // idle lanes still join the warp-wide count
@@ -258,7 +258,7 @@ struct GaussCfg {
 
 // 3D EWA: geometry.py:114-132 + forward.py:252-290.
 template <int DEG>
-__global__ void __launch_bounds__(256) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+__global__ void __launch_bounds__(256, 4) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_gaussians;
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(256) k_gauss3_prep(ges_scene_t sc, CamK cam, G
 
 // Planar 2D Gaussians: forward.py:324-351 (+ filters.py:84-109 when mip).
 template <int DEG>
-__global__ void __launch_bounds__(256) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+__global__ void __launch_bounds__(256, 4) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_gaussians;
