@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--streams", type=int, default=2, help="CUDA streams pipelining the views of a step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    p.add_argument("--cpu-tiles", type=int, default=48, help="tiles in the CPU sample")
+    p.add_argument("--cpu-tiles", type=int, default=64, help="tiles in the CPU sample")
     p.add_argument("--profile-only", action="store_true", help="render a few frames, no JSON (for ncu)")
     return p.parse_args()
 
@@ -102,8 +102,9 @@ def base_config(cfg, per_rank, world, ss):
 # ----------------------------------------------------------------------------- CPU
 def cpu_sample(cfg, scene, cam, n_tiles, threads, ss=1):
     """Time the reference algorithm (oracle/ges_oracle.py, float32 like the
-    reference default) on a bounded sample: full per-frame preprocessing plus
-    ``n_tiles`` of the frame's tiles, extrapolated to the whole frame."""
+    reference default) on a bounded sample: the full per-frame preprocessing
+    plus ``n_tiles`` random tiles of the frame; the tile time is extrapolated
+    to all tiles.  Returns (frame seconds, wall seconds, tiles, total tiles)."""
     from oracle import ges_oracle as O
     from types import SimpleNamespace
     st = SimpleNamespace(supersample=ss, background=(0.0, 0.0, 0.0), layers="full", mip=cfg == 4,
@@ -112,15 +113,13 @@ def cpu_sample(cfg, scene, cam, n_tiles, threads, ss=1):
     nt = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
     rng = np.random.default_rng(7)
     tiles = sorted(rng.choice(nt, min(n_tiles, nt), replace=False).tolist())
+    O.TILE_SECONDS[0] = 0.0
     t0 = time.perf_counter()
-    O.render(scene, cam, st, tiles=[])            # per-frame preprocessing only
-    t1 = time.perf_counter()
-    O.render(scene, cam, st, tiles=tiles)         # preprocessing + sampled tiles
-    t2 = time.perf_counter()
-    pre = t1 - t0
-    per_tile = max((t2 - t1) - pre, 0.0) / len(tiles)
-    frame_s = pre + per_tile * nt
-    return frame_s, t2 - t0, len(tiles), nt
+    O.render(scene, cam, st, tiles=tiles)
+    wall = time.perf_counter() - t0
+    tile_s = O.TILE_SECONDS[0]
+    frame_s = (wall - tile_s) + tile_s * nt / len(tiles)
+    return frame_s, wall, len(tiles), nt
 
 
 def run_reference(args, rank, world):
@@ -132,7 +131,7 @@ def run_reference(args, rank, world):
     cam = views_for(cfg, 0, 1, 1)[0]
     threads = os.cpu_count() or 1
     per_rank = args.views or DEFAULT_VIEWS[cfg]
-    n_tiles = 8
+    n_tiles = 64
     times = []
     wall = 0.0
     for i in range(args.warmup + args.steps):

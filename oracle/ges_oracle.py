@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import math
 import os
+import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -207,13 +208,20 @@ def _select(idx, x0, x1, y0, y1, t):
                & (y0[idx] <= ty1 - 1) & (y1[idx] >= ty0)]
 
 
+# Seconds spent inside per-tile loops since the last reset (lets the CPU
+# baseline separate per-frame preprocessing from per-tile work).
+TILE_SECONDS = [0.0]
+
+
 def _run(fn, tiles, threads):
+    t0 = time.perf_counter()
     if threads <= 1:
         for t in tiles:
             fn(t)
     else:
         with ThreadPoolExecutor(max_workers=threads) as ex:
             list(ex.map(fn, tiles))
+    TILE_SECONDS[0] += time.perf_counter() - t0
 
 
 def _tiles_for(height, width, tiles):
