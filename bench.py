@@ -37,6 +37,7 @@ def parse():
     p.add_argument("--views", type=int, default=None, help="views per rank per step")
     p.add_argument("--ss", type=int, default=1, choices=[1, 4])
     p.add_argument("--streams", type=int, default=2, help="CUDA streams pipelining the views of a step")
+    p.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     p.add_argument("--cpu-tiles", type=int, default=64, help="tiles in the CPU sample")
@@ -96,6 +97,7 @@ def base_config(cfg, per_rank, world, ss):
     return {"workload": WORKLOADS[cfg], "views_per_rank_per_step": per_rank,
             "resolution": [w, h] if cfg != 4 else "480x270, 960x540, 1920x1080, 3840x2160",
             "supersample": ss, "parallelism": f"views x{world}", "streams_per_gpu": ARGS.streams,
+            "cuda_graph": not ARGS.no_graph,
             "scene": "seeded synthetic (SURVEY 8(d), seed 0)", "l2": l2}
 
 
@@ -243,6 +245,7 @@ def run_gpu(args, rank, world, local_rank):
     for r in vb.pool:
         for c, fr in zip(vb.cams, vb.frames):
             r.render(ds, c, settings, frame=fr, check=True)
+    graphed = False if args.no_graph else vb.capture()
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -397,6 +400,7 @@ def run_gpu(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "scene_upload_ms": upload_ms,
         "pairs_per_frame": {"surfel": s_pairs, "gaussian": g_pairs},
+        "cuda_graph_captured": graphed,
     }
     print(json.dumps(line), flush=True)
 

@@ -71,7 +71,29 @@ class ViewBatchRenderer:
             fr.image_rgba8 = b
             self.frames.append(fr)
 
+    def capture(self) -> bool:
+        """Record the whole batch (all views, all streams) into one CUDA graph
+        so a step is a single graph launch.  Call after a checked render has
+        sized every workspace; returns False (and keeps eager launches) if
+        capture is unavailable."""
+        try:
+            torch.cuda.synchronize(self.r.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch(check=False)
+            self.graph = g
+            return True
+        except RuntimeError:
+            self.graph = None
+            return False
+
     def render(self, check: bool = False):
+        if getattr(self, "graph", None) is not None and not check:
+            self.graph.replay()
+            return self.rgba
+        return self._launch(check)
+
+    def _launch(self, check: bool):
         if len(self.pool) == 1:
             for c, fr in zip(self.cams, self.frames):
                 self.r.render(self.scene, c, self.settings, frame=fr, check=check)
