@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
     if constexpr (MODE & 1) {
         constexpr int NS = SS * SS;
         // best[s]: packed (t_bits << 32 | id) of the nearest hit so far; tb[s]: its t
-        // (pixels outside the image start at 0 so they never take work or block culling)
+        // inflated by 1e-5 (candidate filter and culling bound; pixels outside the
+        // image start at 0 so they never take work or block culling)
         unsigned long long best[NS];
         float tb[NS], lxf[SS], lyf[SS], pe[NS];
 #pragma unroll
@@ -193,9 +194,11 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
 #pragma unroll
                 for (int w = 0; w < NWARP; ++w)   // already hidden behind warp w's surface
                     if (r3.x > sm.wmax[w]) mask &= ~(1u << w);
+                // U, V pre-divided by R: coverage becomes U'^2 + V'^2 <= den^2
+                constexpr float IR = 1.0f / 3.3290429691304455f;
                 sm.st[0][threadIdx.x] = make_float4(d0, dx_, dy_, nq);
-                sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
-                sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.w, r3.x);   // r3.w: source id
+                sm.st[1][threadIdx.x] = make_float4(u0 * IR, r1.y * IR, r1.z * IR, v0 * IR);
+                sm.st[2][threadIdx.x] = make_float4(r2.y * IR, r2.z * IR, r3.w, r3.x);   // r3.w: source id
                 sm.zp[threadIdx.x] = zkey_mask(r3.x, mask);
             }
             __syncthreads();
@@ -221,16 +224,16 @@ __global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
                             const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
                             const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
                             const float r2 = fmaf(U, U, V * V);
-                            // coverage u^2+v^2 <= R^2, |n.d| > eps|d|, t > 0.01, and t no
-                            // later than the current best (multiplied out; exact key below)
-                            if (den > pe[s] && r2 <= R2_F * den * den && A.w > NEAR_F * den &&
-                                A.w <= tb[s] * 1.00001f * den) {
+                            // coverage u^2+v^2 <= R^2, |n.d| > eps|d| and t no later than the
+                            // current best (all multiplied out, den > 0 <=> t > 0); the exact
+                            // t > 0.01 and packed-key comparison run only for candidates
+                            if (den > pe[s] && r2 <= den * den && A.w <= tb[s] * den) {
                                 const float t = A.w / den;
                                 const unsigned long long key =
                                     ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
                                 if (t > NEAR_F && key < best[s]) {
                                     best[s] = key;
-                                    tb[s] = t;
+                                    tb[s] = t * 1.00001f;   // margin-inflated best depth
                                 }
                             }
                         }
