@@ -37,6 +37,7 @@ def parse():
     p.add_argument("--views", type=int, default=None, help="views per rank per step")
     p.add_argument("--ss", type=int, default=1, choices=[1, 4])
     p.add_argument("--streams", type=int, default=2, help="CUDA streams pipelining the views of a step")
+    p.add_argument("--layers", default="full", choices=["full", "surfels_only", "gaussians_only"])
     p.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
@@ -97,7 +98,7 @@ def base_config(cfg, per_rank, world, ss):
     return {"workload": WORKLOADS[cfg], "views_per_rank_per_step": per_rank,
             "resolution": [w, h] if cfg != 4 else "480x270, 960x540, 1920x1080, 3840x2160",
             "supersample": ss, "parallelism": f"views x{world}", "streams_per_gpu": ARGS.streams,
-            "cuda_graph": not ARGS.no_graph,
+            "cuda_graph": not ARGS.no_graph, "layers": ARGS.layers,
             "scene": "seeded synthetic (SURVEY 8(d), seed 0)", "l2": l2}
 
 
@@ -231,7 +232,7 @@ def run_gpu(args, rank, world, local_rank):
     per_rank = args.views or DEFAULT_VIEWS[cfg]
     scene = S.config_scene(cfg)
     cams = views_for(cfg, rank, world, per_rank)
-    settings = G.RenderSettings(supersample=args.ss, mip=(cfg == 4))
+    settings = G.RenderSettings(supersample=args.ss, mip=(cfg == 4), layers=args.layers)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ds = G.DeviceScene(scene, dev)

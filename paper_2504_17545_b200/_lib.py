@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libges_b200.so")
+# GES_B200_LIB overrides the library path (A/B runs of alternative builds)
+LIB_PATH = os.environ.get("GES_B200_LIB") or os.path.join(HERE, "libges_b200.so")
 
 GES_OK, GES_EINVAL, GES_EDEGREE, GES_EWORKSPACE, GES_ECUDA = 0, 1, 2, 3, 4
 LAYERS = {"full": 0, "surfels_only": 1, "gaussians_only": 2}

@@ -54,7 +54,7 @@ struct __align__(16) Gauss2Rec {
 
 // Depth slabs of the (tile, slab) bins: NSLAB equal slabs over the view's
 // depth range [zlo, zlo + NSLAB/inv_dz); keys outside clamp to the end slabs.
-constexpr int NSLAB = 16;   // multiple of 4
+constexpr int NSLAB = 32;   // multiple of 4
 static_assert(NSLAB % 4 == 0, "scan reads slab counters as uint4");
 
 struct SlabMap {
