@@ -72,3 +72,17 @@ def test_error_codes_map_to_reference_exceptions():
 
 def test_build_is_up_to_date():
     assert not _build.stale(), "libges_b200.so older than its sources: run __graft_entry__.build()"
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without the CUDA library the render API raises."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, paper_2504_17545_b200 as G\n"
+            "from paper_2504_17545_b200 import scenes as S\n"
+            "sc = S.random_scene(np.random.default_rng(0), 3, 3)\n"
+            "G.render(sc, S.make_camera())\n")
+    env = dict(os.environ, GES_B200_LIB=str(tmp_path / "nope.so"))
+    p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
+    assert p.returncode != 0
+    assert "ImportError" in p.stderr or "RuntimeError" in p.stderr

@@ -252,3 +252,75 @@ def test_smooth_geometry_identity():
     assert np.allclose(n[cov], out.surfels.normal[cov], atol=1e-6)
     with pytest.raises(ValueError):
         G.smooth_geometry(out.surfels, G.GaussianBuffers(out.gaussians.color, out.gaussians.weight))
+
+
+def test_supersample4_480x270_stress():
+    r = np.random.default_rng(21)
+    sc = Scene(S.random_surfels(r, 15000, 2, scale_range=(0.006, 0.02)),
+               S.random_gaussians(r, 4000, 2, scale_range=(0.004, 0.02), extent=1.2), 2, Stage.FROZEN)
+    cam = S.make_camera(480, 270)
+    st = {"supersample": 4, "background": [0.1, 0.2, 0.3]}
+    out = G.render(sc, cam, settings32(st))
+    ora = O.render(sc, cam, settings_ns(st), ties=True)
+    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+
+
+def test_mip_filtered_scene_multiscale():
+    """Config-4 style: world-filtered Gaussians + mip=True at two scales."""
+    r = np.random.default_rng(22)
+    g = S.random_gaussians(r, 5000, 3, scale_range=(0.002, 0.02), extent=1.2)
+    sc = Scene(S.random_surfels(r, 12000, 3, scale_range=(0.004, 0.016)),
+               S.mip_world_filter(g, [S.make_camera(960, 540)]), 3, Stage.FROZEN)
+    for w, h in ((120, 68), (480, 270)):
+        cam = S.make_camera(w, h)
+        out = G.render(sc, cam, settings32({"mip": True}))
+        ora = O.render(sc, cam, settings_ns({"mip": True}), ties=True)
+        assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+
+
+def test_pair_list_overflow_grows_and_rerenders():
+    """A too-small pair capacity is detected on the device, reported in the
+    frame status, and the checked render grows the lists and re-renders."""
+    from paper_2504_17545_b200.renderer import DeviceScene, Renderer
+    sc = S.random_scene(np.random.default_rng(6), 300, 200, degree=1)
+    cam = S.make_camera(96, 64)
+    ds = DeviceScene(sc)
+    r = Renderer()
+    st = G.RenderSettings()
+    r._caps(ds, 1)
+    r.cap_s, r.cap_g = 16, 16                      # force overflow
+    orig_caps = r._caps
+    r._caps = lambda ds_, ss: None                 # keep the tiny capacity for the first attempt
+    fr = r.render(ds, cam, st, check=False)
+    sp, gp, ovf = fr.pairs()
+    assert ovf and sp > 16
+    r._caps = orig_caps
+    fr = r.render(ds, cam, st, check=True)
+    assert fr.pairs()[2] == 0
+    ref = G.render(sc, cam)
+    assert np.array_equal(fr.s_winner.cpu().numpy(), ref.surfels.winner)
+    assert np.max(np.abs(fr.image.cpu().numpy() - ref.image)) <= 1e-6
+
+
+def test_view_batch_streams_and_graph_match_single_renders():
+    from paper_2504_17545_b200.multiview import ViewBatchRenderer
+    from paper_2504_17545_b200.renderer import DeviceScene, Renderer
+    sc = S.random_scene(np.random.default_rng(10), 2000, 800, degree=3)
+    cams = S.orbit_views(6, 128, 96)
+    ds = DeviceScene(sc)
+    st = G.RenderSettings()
+    vb = ViewBatchRenderer(Renderer(), ds, cams, st, want=("image", "s_winner", "image_rgba8"), streams=2)
+    for rr in vb.pool:
+        for c, fr in zip(vb.cams, vb.frames):
+            rr.render(ds, c, st, frame=fr, check=True)
+    assert vb.capture()
+    for _ in range(2):
+        vb.render()
+    torch.cuda.synchronize()
+    assert not vb.overflowed()
+    for c, fr, rgba in zip(cams, vb.frames, vb.rgba):
+        ref = G.render(sc, c)
+        assert np.array_equal(fr.s_winner.cpu().numpy(), ref.surfels.winner)
+        assert np.max(np.abs(fr.image.cpu().numpy() - ref.image)) <= 1e-6
+        q = np.clip(ref.image * 255.0 + 0.5, 0, 255).astype(np.int32)
+        assert np.abs(rgba[..., :3].cpu().numpy().astype(np.int32) - q).max() <= 1
