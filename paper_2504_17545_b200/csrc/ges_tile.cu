@@ -122,7 +122,7 @@ __device__ __forceinline__ float3 surfel_nvis(const TileArgs& a, uint32_t sid) {
 }
 
 template <int SS, int MODE, int GK, bool GEOM>
-__global__ void __launch_bounds__(NB) k_tile(TileArgs a) {
+__global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
     __shared__ TileSmem sm;
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
