@@ -33,15 +33,16 @@ struct __align__(16) TileSmem {
     uint8_t pm[NB];             // Gaussians: warp-patch masks
     uint32_t zp[NB];            // surfels: nearest disc depth with the low byte = warp-patch mask
     float wmax[NWARP];          // per-warp max depth (surfels: current hits; Gaussians: final)
-    uint32_t slab_end[NSLAB];   // this tile's slab ends (relative list positions)
+    uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
+    uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
 };
 
 // Lower depth bound of the slab holding relative list position `rel` (slab
 // ends are non-decreasing, so the slab index is the number of ends <= rel:
 // one vote per warp) and the CTA-wide max of the per-warp depths in sm.wmax.
 // Both read shared memory only, so every warp gets the same answer.
-__device__ __forceinline__ float slab_floor(const TileSmem& sm, const SlabMap& m, uint32_t rel, int lane) {
-    const bool le = lane < NSLAB - 1 && sm.slab_end[lane] <= rel;
+__device__ __forceinline__ float slab_floor(const uint32_t* ends, const SlabMap& m, uint32_t rel, int lane) {
+    const bool le = lane < NSLAB - 1 && ends[lane] <= rel;
     return m.lower(__popc(__ballot_sync(0xffffffffu, le)));
 }
 __device__ __forceinline__ float tile_max(const TileSmem& sm) {
@@ -136,6 +137,18 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
     float ds = INFINITY;             // surfel depth of this pixel (sub-sample 0)
     float3 cs = make_float3(a.bg[0], a.bg[1], a.bg[2]);
 
+    // Issue every list-position load of both passes now: tile offsets, slab
+    // ends and the first batch of Gaussian ids are independent of pass 1, so
+    // their latency (and, below, the first Gaussian records via an L2
+    // prefetch) overlaps the surfel pass.
+    uint32_t gbeg = 0, gend = 0, gid = 0;
+    if constexpr ((MODE & 2) != 0) {
+        if (threadIdx.x < NSLAB) sm.gslab_end[threadIdx.x] = a.gbin.cnt[tile * NSLAB + threadIdx.x];
+        gbeg = a.gbin.tile_off(tile);
+        gend = gbeg + a.gbin.cnt[tile * NSLAB + NSLAB - 1];
+        if (gbeg + threadIdx.x < gend) gid = a.g_list[gbeg + threadIdx.x];
+    }
+
     // ------------------------------------------------------------ pass 1
     if constexpr (MODE & 1) {
         constexpr int NS = SS * SS;
@@ -172,12 +185,20 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
         __syncthreads();
         const int ox = tx * TILE * SS, oy = ty * TILE * SS;
         const uint32_t beg = a.sbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
+        uint32_t nid = beg + threadIdx.x < end ? a.s_list[beg + threadIdx.x] : 0u;
+        if constexpr ((MODE & 2) != 0) {
+            if (gbeg + threadIdx.x < gend) {
+                const char* gp = static_cast<const char*>(a.grec) + (size_t)gid * (GK == 2 ? sizeof(Gauss2Rec) : sizeof(GaussRec));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(gp));
+            }
+        }
         for (uint32_t base = beg; base < end; base += NB) {
             // slabs are near-to-far: stop once the next slab lies behind every hit so far
-            if (slab_floor(sm, a.slabs, base - beg, lane) > tile_max(sm)) break;
+            if (slab_floor(sm.slab_end, a.slabs, base - beg, lane) > tile_max(sm)) break;
             const int nb = min((uint32_t)NB, end - base);
+            const uint32_t id = nid;   // ids of this batch were loaded one batch ahead
+            if (base + NB + threadIdx.x < end) nid = a.s_list[base + NB + threadIdx.x];
             if ((int)threadIdx.x < nb) {
-                const uint32_t id = a.s_list[base + threadIdx.x];
                 const SurfRec* r = a.srec + id;
                 const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3);
                 const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
@@ -282,7 +303,6 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
         float wsum = 0.f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
         const float wm = warp_max(inside ? ds : -INFINITY);
         if (lane == 0) sm.wmax[warp] = wm;
-        if (threadIdx.x < NSLAB) sm.slab_end[threadIdx.x] = a.gbin.cnt[tile * NSLAB + threadIdx.x];
         __syncthreads();
         const float dmax = tile_max(sm);
         const float lx = (float)plx, ly = (float)ply;
@@ -292,13 +312,14 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
             pe = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
         }
         const int ox = tx * TILE, oy = ty * TILE;
-        const uint32_t beg = a.gbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
+        const uint32_t beg = gbeg, end = gend;
         for (uint32_t base = beg; base < end; base += NB) {
             // keys (depth - eps) are binned near-to-far: the rest fail every gate
-            if (slab_floor(sm, a.slabs, base - beg, lane) > dmax) break;
+            if (slab_floor(sm.gslab_end, a.slabs, base - beg, lane) > dmax) break;
             const int nb = min((uint32_t)NB, end - base);
+            const uint32_t id = gid;   // ids loaded one batch ahead (first batch: at kernel start)
+            if (base + NB + threadIdx.x < end) gid = a.g_list[base + NB + threadIdx.x];
             if ((int)threadIdx.x < nb) {
-                const uint32_t id = a.g_list[base + threadIdx.x];
                 uint32_t mask;
                 if constexpr (GK == 3) {
                     const GaussRec* r = reinterpret_cast<const GaussRec*>(a.grec) + id;
