@@ -66,7 +66,6 @@ int check_cam(const ges_camera_t* c) {
 // Frame workspace layout; base == nullptr only measures.
 struct Frame {
     SurfRec* srec;
-    float4* s_rgb;
     void* grec;
     float4* g_nrm;
     uint32_t *cnt_s, *off_s, *cnt_g, *off_g, *chunk_s, *chunk_g, *tickets;
@@ -96,7 +95,6 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, int64_t
     f.chunk_s = c.take<uint32_t>(nchunk);
     f.chunk_g = c.take<uint32_t>(nchunk);
     f.srec = c.take<SurfRec>(ns);
-    f.s_rgb = c.take<float4>(ns);
     f.grec = c.take<char>(ng * (sc->gaussian_dim == 2 ? sizeof(Gauss2Rec) : sizeof(GaussRec)));
     f.g_nrm = c.take<float4>(ng);
     f.list_s = c.take<uint32_t>((size_t)cap_s);
@@ -164,7 +162,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     if (!do_g) scs.n_gaussians = 0;
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, TILE * grid};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE};
-    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, f.s_rgb, nullptr, f.cnt_s}, s)))
+    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, nullptr, f.cnt_s}, s)))
         return cuda_fail(e, "surfel preprocess");
     if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))
         return cuda_fail(e, "gaussian preprocess");
@@ -180,7 +178,9 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     a.layers = st->layers;
     for (int i = 0; i < 3; ++i) a.bg[i] = st->background[i];
     a.rcx = (float)cs.cx; a.rcy = (float)cs.cy; a.rifx = (float)(1.0 / cs.fx); a.rify = (float)(1.0 / cs.fy);
-    a.srec = f.srec; a.s_rgb = f.s_rgb; a.s_list = f.list_s; a.sbin = bs;
+    a.srec = f.srec; a.s_list = f.list_s; a.sbin = bs;
+    a.s_sh = sc->s_sh; a.sh_deg = sc->sh_degree; a.sh_bytes = (sc->sh_degree + 1) * (sc->sh_degree + 1) * 12;
+    for (int i = 0; i < 3; ++i) a.cpos[i] = cs.pos[i];
     a.s_quat = reinterpret_cast<const float4*>(sc->s_quat);
     a.s_pos = reinterpret_cast<const float4*>(sc->s_pos_s1);
     a.s_pack = sc->s_pack;

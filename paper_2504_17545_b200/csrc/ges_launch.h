@@ -38,7 +38,9 @@ struct TileArgs {
     // surfel pass (resolution = ss * base)
     float rcx, rcy, rifx, rify;   // principal point and 1/f of the surfel pass
     const SurfRec* srec;
-    const float4* s_rgb;          // view colour per source surfel id
+    const float* s_sh;            // packed SH (deferred colour of winners)
+    int sh_deg, sh_bytes;
+    double cpos[3];               // camera centre (world)
     const float4 *s_quat, *s_pos; // packed scene (n_vis of winners, on demand)
     const int32_t* s_pack;        // source id -> packed index
     double R[9], t[3];            // world -> camera

@@ -222,13 +222,8 @@ __global__ void __launch_bounds__(256, 4) k_surfel_prep(ges_scene_t sc, CamK cam
         planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
         rec.r3 = make_float4(zkey, __uint_as_float(pack_span(x0, x1)),
                              __uint_as_float(pack_span(y0, y1)), __int_as_float(sid));
-        // view colour: SH at the centre-to-camera direction (forward.py:99-103)
-        d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
-        double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
-        float3 col = sh_color<DEG>(sc.s_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
-                                   (float)(dv.y * inv), (float)(dv.z * inv));
-        o.rgb[sid] = make_float4(col.x, col.y, col.z, 0.f);   // indexed by source id (winner ids)
-        // n_vis (forward.py:152) is evaluated for winners only, when requested
+        // view colour (forward.py:99-103) and n_vis (:152) are evaluated for
+        // winners only, in the tile kernel
     } else {
         rec.r0 = rec.r1 = rec.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
         rec.r3 = make_float4(0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)),

@@ -23,6 +23,7 @@
 #include <math.h>
 
 #include "ges_launch.h"
+#include "ges_sh.cuh"
 
 namespace ges {
 
@@ -32,6 +33,7 @@ struct __align__(16) TileSmem {
     float4 st[5][NB];           // staged per-primitive coefficients
     uint8_t pm[NB];             // Gaussians: warp-patch masks
     uint32_t zp[NB];            // surfels: nearest disc depth with the low byte = warp-patch mask
+    uint32_t sp[NB];            // surfels: packed index of the staged primitive
     float wmax[NWARP];          // per-warp max depth (surfels: current hits; Gaussians: final)
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
     uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
@@ -122,6 +124,48 @@ __device__ __forceinline__ float3 surfel_nvis(const TileArgs& a, uint32_t sid) {
     return make_float3((float)(n[0] * sg), (float)(n[1] * sg), (float)(n[2] * sg));
 }
 
+// View colour of packed surfel `pidx` (forward.py:99-103, sh.py:117-133):
+// SH at the centre-to-camera direction.  Out of line and scalar-argument so
+// the rarely executed, register-hungry evaluation does not raise the
+// kernel's register count or copy the kernel parameters to the stack.
+static __device__ __noinline__ float3 surfel_color_eval(const float* __restrict__ sh, const float4* __restrict__ pos,
+                                                        int deg, double cx, double cy, double cz, uint32_t pidx) {
+    const float4 p = __ldg(pos + pidx);
+    const double dx = cx - p.x, dy = cy - p.y, dz = cz - p.z;
+    const double inv = 1.0 / fmax(sqrt(dx * dx + dy * dy + dz * dz), 1e-12);
+    const int K3 = (deg + 1) * (deg + 1) * 3;
+    return sh_color_dyn(deg, sh + (size_t)pidx * K3, (float)(dx * inv), (float)(dy * inv), (float)(dz * inv));
+}
+
+// Deferred surfel colour (SURVEY 7 "SH only for winning surfels"): after pass
+// 1 each lane knows its winners; lanes of a warp that share a winner elect
+// one lane to evaluate its SH (all elected lanes evaluate in one SIMT pass)
+// and broadcast it.  Box mean over sub-samples for ss=4 (forward.py:201-203).
+// Must be called by all 32 lanes.
+template <int NS>
+__device__ __forceinline__ float3 resolve_surfel_color(const TileArgs& a, const unsigned long long* best,
+                                                       const uint32_t* bp, int lane) {
+    float3 acc = make_float3(0.f, 0.f, 0.f);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const bool cov = best[s] != ~0ull;
+        const unsigned peers = __match_any_sync(0xffffffffu, cov ? bp[s] : 0xffffffffu);
+        const int leader = __ffs(peers) - 1;
+        float3 c = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+        if (cov && lane == leader)
+            c = surfel_color_eval(a.s_sh, a.s_pos, a.sh_deg, a.cpos[0], a.cpos[1], a.cpos[2], bp[s]);
+        c.x = __shfl_sync(0xffffffffu, c.x, leader);
+        c.y = __shfl_sync(0xffffffffu, c.y, leader);
+        c.z = __shfl_sync(0xffffffffu, c.z, leader);
+        if (!cov) c = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+        acc.x += c.x; acc.y += c.y; acc.z += c.z;
+    }
+    if (NS > 1) {
+        acc.x /= (float)NS; acc.y /= (float)NS; acc.z /= (float)NS;
+    }
+    return acc;
+}
+
 template <int SS, int MODE, int GK, bool GEOM>
 __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
     __shared__ TileSmem sm;
@@ -149,13 +193,16 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
         if (gbeg + threadIdx.x < gend) gid = a.g_list[gbeg + threadIdx.x];
     }
 
+    // best[s]: packed (t_bits << 32 | id) of the nearest surfel hit so far;
+    // bp[s]: its packed index (SH address of the deferred colour)
+    constexpr int NS = SS * SS;
+    unsigned long long best[NS];
+    uint32_t bp[NS];
+
     // ------------------------------------------------------------ pass 1
     if constexpr (MODE & 1) {
-        constexpr int NS = SS * SS;
-        // best[s]: packed (t_bits << 32 | id) of the nearest hit so far; tb[s]: its t
-        // inflated by 1e-5 (candidate filter and culling bound; pixels outside the
-        // image start at 0 so they never take work or block culling)
-        unsigned long long best[NS];
+        // tb[s]: the best t inflated by 1e-5 (candidate filter and culling bound;
+        // pixels outside the image start at 0 so they never take work or block culling)
         float tb[NS], lxf[SS], lyf[SS], pe[NS];
 #pragma unroll
         for (int s = 0; s < SS; ++s) {
@@ -171,6 +218,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                 const float dxn = ((float)X + 0.5f - a.rcx) * a.rifx, dyn = ((float)Y + 0.5f - a.rcy) * a.rify;
                 pe[sy * SS + sx] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
                 best[sy * SS + sx] = ~0ull;
+                bp[sy * SS + sx] = 0u;
                 tb[sy * SS + sx] = inside ? INFINITY : 0.f;
             }
         auto patch_depth = [&]() {
@@ -221,6 +269,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                 sm.st[1][threadIdx.x] = make_float4(u0 * IR, r1.y * IR, r1.z * IR, v0 * IR);
                 sm.st[2][threadIdx.x] = make_float4(r2.y * IR, r2.z * IR, r3.w, r3.x);   // r3.w: source id
                 sm.zp[threadIdx.x] = zkey_mask(r3.x, mask);
+                sm.sp[threadIdx.x] = id;
             }
             __syncthreads();
             for (int c = 0; c < nb; c += 32) {
@@ -254,6 +303,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                                     ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
                                 if (t > NEAR_F && key < best[s]) {
                                     best[s] = key;
+                                    bp[s] = sm.sp[j];
                                     tb[s] = t * 1.00001f;   // margin-inflated best depth
                                 }
                             }
@@ -264,30 +314,22 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
             if (lane == 0) sm.wmax[warp] = wmx;
             __syncthreads();
         }
-        // resolve: depth/normal/winner from sub-sample 0, colour = box mean (forward.py:201-207)
-        float3 acc = make_float3(0.f, 0.f, 0.f);
+        // the winners' SH blocks are read at the end (deferred colour): start
+        // pulling them into L2 now, overlapping the Gaussian pass
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-            float3 c = make_float3(a.bg[0], a.bg[1], a.bg[2]);
             if (best[s] != ~0ull) {
-                float4 v = __ldg(a.s_rgb + (uint32_t)best[s]);
-                c = make_float3(v.x, v.y, v.z);
+                const char* p = reinterpret_cast<const char*>(a.s_sh) + (size_t)bp[s] * a.sh_bytes;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+                if (a.sh_bytes > 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + a.sh_bytes - 4));
             }
-            acc.x += c.x; acc.y += c.y; acc.z += c.z;
         }
-        if (NS > 1) {
-            acc.x /= (float)NS; acc.y /= (float)NS; acc.z /= (float)NS;
-        }
-        cs = acc;
+        // depth/normal/winner from sub-sample 0 (forward.py:205-207)
         const bool cov = best[0] != ~0ull;
         ds = cov ? __uint_as_float((uint32_t)(best[0] >> 32)) : INFINITY;
         if (inside) {
             if (a.out.s_depth) a.out.s_depth[pix] = ds;
             if (a.out.s_winner) a.out.s_winner[pix] = cov ? (int32_t)(uint32_t)best[0] : -1;
-            if (a.out.s_color) {
-                a.out.s_color[3 * pix] = cs.x; a.out.s_color[3 * pix + 1] = cs.y;
-                a.out.s_color[3 * pix + 2] = cs.z;
-            }
             if (a.out.s_normal) {
                 const float3 n = cov ? surfel_nvis(a, (uint32_t)best[0]) : make_float3(0.f, 0.f, 0.f);
                 a.out.s_normal[3 * pix] = n.x; a.out.s_normal[3 * pix + 1] = n.y;
@@ -410,7 +452,14 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
             }
             __syncthreads();
         }
+        if constexpr ((MODE & 1) != 0) cs = resolve_surfel_color<SS * SS>(a, best, bp, lane);
         if (inside) {
+            if constexpr ((MODE & 1) != 0) {
+                if (a.out.s_color) {
+                    a.out.s_color[3 * pix] = cs.x; a.out.s_color[3 * pix + 1] = cs.y;
+                    a.out.s_color[3 * pix + 2] = cs.z;
+                }
+            }
             if (a.out.g_weight) a.out.g_weight[pix] = wsum;
             if (a.out.g_color) {
                 a.out.g_color[3 * pix] = cr; a.out.g_color[3 * pix + 1] = cg; a.out.g_color[3 * pix + 2] = cb;
@@ -430,7 +479,12 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                 if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, im);
             }
         }
-    } else if (inside) {   // surfels_only (forward.py:407-410): empty Gaussian buffers
+    } else {   // surfels_only (forward.py:407-410): empty Gaussian buffers
+      cs = resolve_surfel_color<SS * SS>(a, best, bp, lane);
+      if (inside) {
+        if (a.out.s_color) {
+            a.out.s_color[3 * pix] = cs.x; a.out.s_color[3 * pix + 1] = cs.y; a.out.s_color[3 * pix + 2] = cs.z;
+        }
         if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, cs);
         if (a.out.image) {
             a.out.image[3 * pix] = cs.x; a.out.image[3 * pix + 1] = cs.y; a.out.image[3 * pix + 2] = cs.z;
@@ -439,6 +493,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
         if (a.out.g_color) {
             a.out.g_color[3 * pix] = 0.f; a.out.g_color[3 * pix + 1] = 0.f; a.out.g_color[3 * pix + 2] = 0.f;
         }
+      }
     }
 }
 
