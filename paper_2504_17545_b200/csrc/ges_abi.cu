@@ -160,8 +160,9 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     ges_scene_t scs = *sc;
     if (!do_s) scs.n_surfels = 0;
     if (!do_g) scs.n_gaussians = 0;
-    const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, TILE * grid};
-    const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE};
+    const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, TILE * grid,
+                     grid == 2 ? 5 : 4};
+    const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE, 4};
     if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, nullptr, f.cnt_s}, s)))
         return cuda_fail(e, "surfel preprocess");
     if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))

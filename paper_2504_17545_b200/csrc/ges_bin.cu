@@ -105,9 +105,9 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
                                          const BinPass& p) {
     const int x0 = span_lo(sx), x1 = span_hi(sx), y0 = span_lo(sy), y1 = span_hi(sy);
     bool more = live && x1 >= x0 && y1 >= y0;
-    const int tp = p.tile_px;
-    const int tx0 = x0 / tp, tx1 = x1 / tp, ty1 = y1 / tp;
-    int ty = y0 / tp, tx = tx0;
+    const int sh = p.tile_shift;   // tiles are 16 or 32 px: shifts, not divisions
+    const int tx0 = x0 >> sh, tx1 = x1 >> sh, ty1 = y1 >> sh;
+    int ty = y0 >> sh, tx = tx0;
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     uint32_t base_r[FILL_R], toff_r[FILL_R], peers_r[FILL_R];

@@ -84,7 +84,7 @@ struct BinPass {
     uint32_t* ticket;   // scan completion counter (zeroed per frame)
     uint32_t* list;     // cap primitive ids (packed indices)
     int64_t cap;
-    int ntiles, ntx, tile_px;
+    int ntiles, ntx, tile_px, tile_shift;
     __device__ __forceinline__ uint32_t tile_off(int t) const { return chunk[t >> 8] + off[t]; }
 };
 
