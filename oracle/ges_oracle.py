@@ -14,7 +14,8 @@ real reference (imported read-only in the build container by
 this restatement against them at atol 1e-9 in float64.
 
 Beyond the reference's outputs this oracle can
-  * evaluate only a subset of 16x16 tiles (``tiles=``), which lets the GPU
+  * evaluate only a subset of 16x16 base-resolution tiles (``tiles=``; with
+    supersample=4 the surfel pass covers the same pixels), which lets the GPU
     parity tests spot-check full-size frames (config 2) in seconds;
   * report per-pixel *tie flags*: pixels whose float64 decision margin is so
     small that a float32 evaluation may legitimately decide differently
@@ -224,6 +225,25 @@ def _run(fn, tiles, threads):
     TILE_SECONDS[0] += time.perf_counter() - t0
 
 
+def _hires_tiles(tiles, base, grid):
+    """Base-resolution tile indices -> the hi-res (grid x grid) tiles covering
+    the same pixels, for the supersampled surfel pass."""
+    if tiles is None or grid == 1:
+        return tiles
+    ntx = (base.width + TILE - 1) // TILE
+    ntx_hi = (base.width * grid + TILE - 1) // TILE
+    nty_hi = (base.height * grid + TILE - 1) // TILE
+    out = []
+    for t in tiles:
+        by, bx = divmod(t, ntx)
+        for dy in range(grid):
+            for dx in range(grid):
+                hy, hx = by * grid + dy, bx * grid + dx
+                if hy < nty_hi and hx < ntx_hi:
+                    out.append(hy * ntx_hi + hx)
+    return out
+
+
 def _tiles_for(height, width, tiles):
     allt = tile_list(height, width)
     if tiles is None:
@@ -351,7 +371,7 @@ def rasterize_surfels(scene, cam, settings=None, *, tiles=None, ties=False) -> S
                     flag = close | np.any(fragile & (front | near_par), axis=0)
                 tie[ty0:ty1, tx0:tx1] = flag.reshape(shp)
 
-        _run(do_tile, _tiles_for(H, W, tiles), st["threads"])
+        _run(do_tile, _tiles_for(H, W, _hires_tiles(tiles, base, grid)), st["threads"])
 
     if grid > 1:
         h, w = base.height, base.width

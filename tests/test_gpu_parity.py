@@ -324,3 +324,60 @@ def test_view_batch_streams_and_graph_match_single_renders():
         assert np.max(np.abs(fr.image.cpu().numpy() - ref.image)) <= 1e-6
         q = np.clip(ref.image * 255.0 + 0.5, 0, 255).astype(np.int32)
         assert np.abs(rgba[..., :3].cpu().numpy().astype(np.int32) - q).max() <= 1
+
+
+def _tile_region(cam, tiles):
+    region = np.zeros((cam.height, cam.width), bool)
+    for ti in tiles:
+        ty0, ty1, tx0, tx1 = O.tile_list(cam.height, cam.width)[ti]
+        region[ty0:ty1, tx0:tx1] = True
+    return region
+
+
+def test_camera_inside_scene_near_plane():
+    """Camera inside the primitive cloud: many surfels straddle the focal
+    plane (whole-screen ranges, geometry.py:295-297) or lie behind it."""
+    r = np.random.default_rng(33)
+    sc = Scene(S.random_surfels(r, 3000, 2, scale_range=(0.01, 0.05)),
+               S.random_gaussians(r, 1500, 2, scale_range=(0.01, 0.05), extent=1.2), 2, Stage.FROZEN)
+    cam = S.make_camera(160, 120, dist=0.3)
+    out = G.render(sc, cam)
+    ora = O.render(sc, cam, settings_ns({}), ties=True)
+    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+
+
+def test_4k_supersampled_config2_scene_tile_sample():
+    """The config-2 scene at 3840x2160 with supersample=4 (7680x4320 surfel
+    pass): GPU frame vs the oracle on sampled tiles."""
+    sc = S.config_scene(2, scale_down=4)
+    cam = S.make_camera(3840, 2160)
+    st = {"supersample": 4}
+    out = G.render(sc, cam, settings32(st))
+    nt = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    tiles = sorted(np.random.default_rng(9).choice(nt, 6, replace=False).tolist() + [nt // 2 + 120])
+    ora = O.render(sc, cam, settings_ns(st), tiles=tiles, ties=True)
+    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie, region=_tile_region(cam, tiles))
+    assert_parity(rep)
+
+
+def test_planar_gaussians_dense_with_geometry():
+    r = np.random.default_rng(44)
+    sc = Scene(S.random_surfels(r, 8000, 1, scale_range=(0.008, 0.03)),
+               S.random_gaussians(r, 4000, 1, kind=GaussianKind.TWO_D, scale_range=(0.006, 0.03),
+                                  extent=1.2), 1, Stage.FROZEN)
+    cam = S.make_camera(320, 200)
+    st = {"with_geometry": True, "mip": True}
+    out = G.render(sc, cam, settings32(st))
+    ora = O.render(sc, cam, settings_ns(st), ties=True)
+    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie)
+    assert_parity(rep)
+    assert rep["g_depth_maxabs"] < 1e-3 and rep["g_normal_maxabs"] < 1e-3, rep
+
+
+def test_odd_sizes_and_aspect():
+    sc = S.random_scene(np.random.default_rng(45), 400, 200, degree=1)
+    for w, h in ((17, 33), (1, 1), (257, 3)):
+        cam = S.make_camera(w, h)
+        out = G.render(sc, cam)
+        ora = O.render(sc, cam, settings_ns({}), ties=True)
+        assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))

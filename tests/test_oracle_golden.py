@@ -64,3 +64,12 @@ def test_oracle_fp32_close_to_fp64():
     scene, cam, st, gold, _ = load("config1")
     out = O.render(scene, cam, settings_ns(st, np.float32))
     assert np.max(np.abs(out.image - gold["image"])) < 1e-4
+
+
+def test_oracle_tile_subset_supersampled():
+    scene, cam, st, gold, _ = load("deg3_64x48_ss4")
+    tiles = [0, 5, 10]
+    out = O.render(scene, cam, settings_ns(st), tiles=tiles)
+    for ti in tiles:
+        ty0, ty1, tx0, tx1 = O.tile_list(cam.height, cam.width)[ti]
+        _close(out.image[ty0:ty1, tx0:tx1], gold["image"][ty0:ty1, tx0:tx1])
