@@ -184,6 +184,10 @@ int ges_render_views_host(const ges_scene_t *scene, const ges_camera_t *host_cam
                           int64_t gaussian_pair_cap, void *image_dev,
                           ges_frame_status_t *status_dev, void *stream, void *copy_stream);
 
+/* Tile-kernel work counters (16 x u64), then reset.  All zero unless the
+ * library was built with -DGES_STATS (tuning builds only; synchronous). */
+int ges_debug_stats(uint64_t *out16);
+
 #ifdef __cplusplus
 }
 #endif

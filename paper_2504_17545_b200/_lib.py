@@ -21,7 +21,7 @@ LAYERS = {"full": 0, "surfels_only": 1, "gaussians_only": 2}
 EXPORTS = ("ges_abi_version", "ges_last_error", "ges_scene_bytes", "ges_scene_pack",
            "ges_workspace_bytes", "ges_render", "ges_render_profiled", "ges_rasterize_surfels",
            "ges_accumulate_gaussians", "ges_composite", "ges_smooth_geometry",
-           "ges_render_views_host")
+           "ges_render_views_host", "ges_debug_stats")
 
 
 class Camera(C.Structure):
@@ -96,6 +96,7 @@ def lib():
                                             C.c_void_p, C.c_size_t, C.c_int64, C.c_int64, C.c_void_p,
                                             C.c_void_p, C.c_void_p, C.c_void_p]),
     }
+    sig["ges_debug_stats"] = (C.c_int, [C.POINTER(C.c_uint64)])
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
         fn.restype = res

@@ -300,6 +300,12 @@ int ges_smooth_geometry(const float* sd, const float* sn, const float* gd, const
     return e == cudaSuccess ? GES_OK : cuda_fail(e, "smooth_geometry");
 }
 
+int ges_debug_stats(uint64_t* out16) {
+    if (!out16) return fail(GES_EINVAL, "NULL argument");
+    if (read_stats(reinterpret_cast<unsigned long long*>(out16))) return fail(GES_ECUDA, "stats copy failed");
+    return GES_OK;
+}
+
 int ges_render_views_host(const ges_scene_t* sc, const ges_camera_t* host_cams, int32_t n_views,
                           const ges_settings_t* st, float* host_images, void* ws, size_t ws_bytes, int64_t cap_s,
                           int64_t cap_g, void* image_dev, ges_frame_status_t* status_dev, void* stream,

@@ -173,15 +173,10 @@ __global__ void __launch_bounds__(256) k_fill(const SurfRec* __restrict__ srec, 
         const bool live = j < ng;
         uint32_t sx = 0, sy = 0;
         float key = 0.f;
-        if (live && g_kind == 2) {   // Gauss2Rec: r3 = (sigma, eps, rect_x, rect_y), r5.x = key
-            const float4 r3 = __ldg(grec + j * 6 + 3);
-            sx = __float_as_uint(r3.z); sy = __float_as_uint(r3.w);
-            key = __ldg(grec + j * 6 + 5).x;
-        } else if (live) {           // GaussRec: r2 = (depth, eps, pmin, rect_x), r3.x = rect_y
-            const float4 r2 = __ldg(grec + j * 4 + 2);
-            sx = __float_as_uint(r2.w);
-            sy = __float_as_uint(__ldg(grec + j * 4 + 3).x);
-            key = gauss_key(r2.x, r2.y);
+        if (live) {   // cull fields: c = (depth or key, eps, rect_x, rect_y)
+            const float4 c = __ldg(grec + j * (g_kind == 2 ? 6 : 4));
+            sx = __float_as_uint(c.z); sy = __float_as_uint(c.w);
+            key = g_kind == 2 ? c.x : gauss_key(c.x, c.y);
         }
         fill_one(live, (uint32_t)j, sx, sy, sm.slab(key), pg);
     }

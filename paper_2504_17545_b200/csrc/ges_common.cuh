@@ -37,19 +37,24 @@ struct __align__(16) SurfRec {
     float4 r0, r1, r2, r3;
 };
 
-// Per-Gaussian screen record (3D EWA), 64 B.
+// Per-Gaussian screen records.  The first float4 `c` holds everything the
+// cull needs (depth test inputs and pixel range), so binning and the tile
+// kernel's staging read 16 B per entry and fetch the rest only for the few
+// entries that survive.
+// 3D EWA, 64 B:
+//   c  = (depth, eps, rect_x, rect_y)
 //   r0 = (mx_int, mx_frac, my_int, my_frac)       mean2d split for precision
 //   r1 = (pa, pb, pc, sigma)  power = pa dx^2 + pb dx dy + pc dy^2
-//   r2 = (depth, eps, pmin, rect_x)  pmin: power below which alpha < 1/255
-//   r3 = (rect_y, r, g, b)
+//   r2 = (pmin, r, g, b)      pmin: power below which alpha < 1/255
 struct __align__(16) GaussRec {
-    float4 r0, r1, r2, r3;
+    float4 c, r0, r1, r2;
 };
 
-// Per-2D-Gaussian record, 96 B: ray-plane homography like SurfRec plus
-//   r3 = (sigma, eps, rect_x, rect_y), r4 = (r, g, b, r2max), r5 = (slab key, 0, 0, 0)
+// Planar 2D Gaussian, 96 B: c = (slab/cull key, eps, rect_x, rect_y), then the
+// ray-plane homography r0..r2 like SurfRec, r3 = (sigma, r2max, 0, 0),
+// r4 = (r, g, b, 0).
 struct __align__(16) Gauss2Rec {
-    float4 r0, r1, r2, r3, r4, r5;
+    float4 c, r0, r1, r2, r3, r4;
 };
 
 // Depth slabs of the (tile, slab) bins: NSLAB equal slabs over the view's

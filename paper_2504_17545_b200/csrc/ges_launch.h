@@ -62,6 +62,8 @@ struct TileArgs {
 // mode: 1 = surfels only, 2 = Gaussians only (external depth), 3 = both.
 cudaError_t launch_tile(const TileArgs& a, int ss, int mode, int g_kind, bool geom, cudaStream_t s);
 
+int read_stats(unsigned long long* out);   // 16 counters, then reset (GES_STATS builds)
+
 cudaError_t launch_composite(const float* sc, const float* gc, const float* gw, float sw, float* img,
                              int64_t n, cudaStream_t s);
 cudaError_t launch_smooth(const float* sd, const float* sn, const float* gd, const float* gn,

@@ -312,15 +312,15 @@ __global__ void __launch_bounds__(256, 4) k_gauss3_prep(ges_scene_t sc, CamK cam
     if (!valid_thread) return;
     if (valid) {
         double mxi = floor(mx), myi = floor(my);
+        rec.c = make_float4(depf, epsf, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)));
         rec.r0 = make_float4((float)mxi, (float)(mx - mxi), (float)myi, (float)(my - myi));
         rec.r1 = make_float4((float)(-0.5 * la), (float)(-lb), (float)(-0.5 * lc), (float)sig);
-        rec.r2 = make_float4(depf, epsf, (float)(-0.5 * m2max) - 1e-4f,
-                             __uint_as_float(pack_span(x0, x1)));
+        const float pmin = (float)(-0.5 * m2max) - 1e-4f;
         d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
         double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
         float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
                                    (float)(dv.y * inv), (float)(dv.z * inv));
-        rec.r3 = make_float4(__uint_as_float(pack_span(y0, y1)), col.x, col.y, col.z);
+        rec.r2 = make_float4(pmin, col.x, col.y, col.z);
         if (cfg.geom) {   // forward.py:277-284: shortest eff_scale axis, camera-facing
             int k = 0;
             double smin = se.x;
@@ -331,9 +331,8 @@ __global__ void __launch_bounds__(256, 4) k_gauss3_prep(ges_scene_t sc, CamK cam
             o.nrm[i] = make_float4((float)(nv.x * sgn), (float)(nv.y * sgn), (float)(nv.z * sgn), 0.f);
         }
     } else {
-        rec.r0 = rec.r1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        rec.r2 = make_float4(0.f, 0.f, 0.f, __uint_as_float(pack_span(1, 0)));
-        rec.r3 = make_float4(__uint_as_float(pack_span(1, 0)), 0.f, 0.f, 0.f);
+        rec.r0 = rec.r1 = rec.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        rec.c = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
     }
     reinterpret_cast<GaussRec*>(o.rec)[i] = rec;
 }
@@ -387,21 +386,20 @@ __global__ void __launch_bounds__(256, 4) k_gauss2_prep(ges_scene_t sc, CamK cam
     Gauss2Rec rec;
     if (valid) {
         planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
-        rec.r3 = make_float4((float)sig, epsf, __uint_as_float(pack_span(x0, x1)),
-                             __uint_as_float(pack_span(y0, y1)));
+        rec.c = make_float4(gkey, epsf, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)));
         d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
         double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
         float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
                                    (float)(dv.y * inv), (float)(dv.z * inv));
-        rec.r4 = make_float4(col.x, col.y, col.z, (float)m2max * 1.0001f + 1e-4f);
-        rec.r5 = make_float4(gkey, 0.f, 0.f, 0.f);
+        rec.r3 = make_float4((float)sig, (float)m2max * 1.0001f + 1e-4f, 0.f, 0.f);
+        rec.r4 = make_float4(col.x, col.y, col.z, 0.f);
         if (cfg.geom) {
             double sgn = dot(n, q) < 0.0 ? 1.0 : -1.0;   // forward.py:337
             o.nrm[i] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);
         }
     } else {
-        rec.r0 = rec.r1 = rec.r2 = rec.r4 = rec.r5 = make_float4(0.f, 0.f, 0.f, 0.f);
-        rec.r3 = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
+        rec.r0 = rec.r1 = rec.r2 = rec.r3 = rec.r4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        rec.c = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
     }
     reinterpret_cast<Gauss2Rec*>(o.rec)[i] = rec;
 }

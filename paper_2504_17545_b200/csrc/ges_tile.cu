@@ -29,6 +29,18 @@ namespace ges {
 
 constexpr int NB = TILE_PX;     // batch = one primitive per thread
 
+// Work counters for tuning (compiled in only with -DGES_STATS; read with
+// ges_debug_stats).  0 surfel batches, 1 surfel entries staged, 2 staged with
+// a live warp mask, 3 surfel warp tests, 4 candidate lanes, 5 Gaussian
+// batches, 6 Gaussian entries staged, 7 staged with a live mask, 8 Gaussian
+// warp tests, 9 contributing lanes, 10 tiles, 11 tiles with uncovered pixels.
+__device__ unsigned long long g_stats[16];
+#ifdef GES_STATS
+#define GES_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
+#else
+#define GES_STAT(i, v) ((void)0)
+#endif
+
 struct __align__(16) TileSmem {
     float4 st[5][NB];           // staged per-primitive coefficients
     uint8_t pm[NB];             // Gaussians: warp-patch masks
@@ -271,6 +283,13 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                 sm.zp[threadIdx.x] = zkey_mask(r3.x, mask);
                 sm.sp[threadIdx.x] = id;
             }
+#ifdef GES_STATS
+            {
+                const unsigned live = __ballot_sync(0xffffffffu, (int)threadIdx.x < nb && (sm.zp[threadIdx.x] & 0xFFu));
+                if (lane == 0) GES_STAT(2, __popc(live));
+                if (threadIdx.x == 0) { GES_STAT(0, 1); GES_STAT(1, nb); }
+            }
+#endif
             __syncthreads();
             for (int c = 0; c < nb; c += 32) {
                 const int e = c + lane;
@@ -283,6 +302,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                     vote &= vote - 1;
                     const float4 C = sm.st[2][j];
                     if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
+                    if (lane == 0) GES_STAT(3, 1);
                     const float4 A = sm.st[0][j], B = sm.st[1][j];
 #pragma unroll
                     for (int sy = 0; sy < SS; ++sy)
@@ -301,6 +321,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                                 const float t = A.w / den;
                                 const unsigned long long key =
                                     ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
+                                GES_STAT(4, 1);
                                 if (t > NEAR_F && key < best[s]) {
                                     best[s] = key;
                                     bp[s] = sm.sp[j];
@@ -347,6 +368,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
         if (lane == 0) sm.wmax[warp] = wm;
         __syncthreads();
         const float dmax = tile_max(sm);
+        if (threadIdx.x == 0) { GES_STAT(10, 1); GES_STAT(11, dmax == INFINITY); }
         const float lx = (float)plx, ly = (float)ply;
         float pe = 0.f;
         if constexpr (GK == 2) {
@@ -364,43 +386,58 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
             if ((int)threadIdx.x < nb) {
                 uint32_t mask;
                 if constexpr (GK == 3) {
+                    // the cull needs only c; the rest is fetched for survivors only
                     const GaussRec* r = reinterpret_cast<const GaussRec*>(a.grec) + id;
-                    const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2),
-                                 r3 = __ldg(&r->r3);
-                    const float mxt = (r0.x - (float)ox) + (r0.y - 0.5f);
-                    const float myt = (r0.z - (float)oy) + (r0.w - 0.5f);
-                    const uint32_t sxr = __float_as_uint(r2.w), syr = __float_as_uint(r3.x);
+                    const float4 c = __ldg(&r->c);
+                    const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
                     mask = patch_mask<1>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
                                          span_hi(syr) - oy);
                     // exact conservative cull: d < fl(max_ds + eps) is necessary for the gate
 #pragma unroll
                     for (int w = 0; w < NWARP; ++w)
-                        if (!(r2.x < sm.wmax[w] + r2.y)) mask &= ~(1u << w);
-                    sm.st[0][threadIdx.x] = make_float4(mxt, myt, r1.x, r1.y);
-                    sm.st[1][threadIdx.x] = make_float4(r1.z, r1.w, r2.x, r2.y);
-                    sm.st[2][threadIdx.x] = make_float4(r3.y, r3.z, r3.w, r2.z);
+                        if (!(c.x < sm.wmax[w] + c.y)) mask &= ~(1u << w);
+                    if (mask) {
+                        const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2);
+                        const float mxt = (r0.x - (float)ox) + (r0.y - 0.5f);
+                        const float myt = (r0.z - (float)oy) + (r0.w - 0.5f);
+                        sm.st[0][threadIdx.x] = make_float4(mxt, myt, r1.x, r1.y);
+                        sm.st[1][threadIdx.x] = make_float4(r1.z, r1.w, c.x, c.y);
+                        sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r2.w, r2.x);
+                    }
                 } else {
                     const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + id;
-                    const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2),
-                                 r3 = __ldg(&r->r3), r4 = __ldg(&r->r4), r5 = __ldg(&r->r5);
-                    const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
-                    const float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
-                    const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
-                    const float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
-                    const uint32_t sxr = __float_as_uint(r3.z), syr = __float_as_uint(r3.w);
+                    const float4 c = __ldg(&r->c);
+                    const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
                     mask = patch_mask<1>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
                                          span_hi(syr) - oy);
 #pragma unroll
                     for (int w = 0; w < NWARP; ++w)   // key = nearest support depth - eps
-                        if (r5.x > sm.wmax[w]) mask &= ~(1u << w);
-                    sm.st[0][threadIdx.x] = make_float4(d0, r0.y, r0.z, r0.w);
-                    sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
-                    sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.x, r3.y);
-                    sm.st[3][threadIdx.x] = r4;
+                        if (c.x > sm.wmax[w]) mask &= ~(1u << w);
+                    if (mask) {
+                        const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2),
+                                     r3 = __ldg(&r->r3), r4 = __ldg(&r->r4);
+                        const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
+                        const float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
+                        const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
+                        const float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
+                        sm.st[0][threadIdx.x] = make_float4(d0, r0.y, r0.z, r0.w);
+                        sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
+                        sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.x, c.y);
+                        sm.st[3][threadIdx.x] = make_float4(r4.x, r4.y, r4.z, r3.y);
+                    }
                 }
-                if constexpr (GEOM) sm.st[4][threadIdx.x] = __ldg(a.g_nrm + id);
+                if constexpr (GEOM) {
+                    if (mask) sm.st[4][threadIdx.x] = __ldg(a.g_nrm + id);
+                }
                 sm.pm[threadIdx.x] = (uint8_t)mask;
             }
+#ifdef GES_STATS
+            {
+                const unsigned live = __ballot_sync(0xffffffffu, (int)threadIdx.x < nb && sm.pm[threadIdx.x]);
+                if (lane == 0) GES_STAT(7, __popc(live));
+                if (threadIdx.x == 0) { GES_STAT(5, 1); GES_STAT(6, nb); }
+            }
+#endif
             __syncthreads();
             for (int c = 0; c < nb; c += 32) {
                 const int e = c + lane;
@@ -409,6 +446,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                     const int j = c + __ffs(vote) - 1;
                     vote &= vote - 1;
                     const float4 A = sm.st[0][j], B = sm.st[1][j], C = sm.st[2][j];
+                    if (lane == 0) GES_STAT(8, 1);
                     if constexpr (GK == 3) {
                         // forward.py:301-311
                         const float dx = lx - A.x, dy = ly - A.y;
@@ -416,6 +454,7 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                         if (p >= C.w) {
                             const float al = B.y * __expf(p);
                             if (al >= ALPHA_CUTOFF_F && B.z < ds + B.w) {
+                                GES_STAT(9, 1);
                                 wsum += al;
                                 cr = fmaf(al, C.x, cr); cg = fmaf(al, C.y, cg); cb = fmaf(al, C.z, cb);
                                 if constexpr (GEOM) {
@@ -546,6 +585,12 @@ __global__ void k_smooth(const float* __restrict__ sd, const float* __restrict__
         float inv = ok ? 1.0f / fmaxf(nr, 1e-12f) : 0.f;
         nout[3 * i] = v0 * inv; nout[3 * i + 1] = v1 * inv; nout[3 * i + 2] = v2 * inv;
     }
+}
+
+int read_stats(unsigned long long* out) {
+    if (cudaMemcpyFromSymbol(out, g_stats, sizeof(g_stats)) != cudaSuccess) return 1;
+    unsigned long long z[16] = {};
+    return cudaMemcpyToSymbol(g_stats, z, sizeof(z)) == cudaSuccess ? 0 : 1;
 }
 
 cudaError_t launch_composite(const float* sc, const float* gc, const float* gw, float sw, float* img, int64_t n,

@@ -1,0 +1,40 @@
+"""Work counters of the tile kernel for one config-2 frame (tuning aid).
+
+  python -m paper_2504_17545_b200._build stats
+  GES_B200_LIB=paper_2504_17545_b200/libges_b200_stats.so python tools/tile_stats.py [--ss 4]
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2504_17545_b200 as G  # noqa: E402
+from paper_2504_17545_b200 import _lib, scenes as S  # noqa: E402
+
+NAMES = ["surfel batches", "surfel entries staged", "  with live mask", "surfel warp tests",
+         "candidate lanes", "gauss batches", "gauss entries staged", "  with live mask",
+         "gauss warp tests", "contributing lanes", "tiles", "tiles with uncovered px"]
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--ss", type=int, default=1)
+a = ap.parse_args()
+sc = S.config_scene(a.config)
+cam = S.config_cameras(a.config)[0]
+ds = G.DeviceScene(sc)
+r = G.Renderer()
+st = G.RenderSettings(supersample=a.ss)
+fr = r.render(ds, cam, st, check=True)
+buf = (C.c_uint64 * 16)()
+_lib.lib().ges_debug_stats(buf)            # reset after the sizing render
+fr = r.render(ds, cam, st, check=True)
+torch.cuda.synchronize()
+_lib.lib().ges_debug_stats(buf)
+sp, gp, _ = fr.pairs()
+print(f"pairs: surfel {sp}  gaussian {gp}   pixels {cam.width * cam.height}")
+for n, v in zip(NAMES, buf):
+    print(f"{n:28s} {v:14d}")
