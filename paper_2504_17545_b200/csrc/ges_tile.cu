@@ -42,8 +42,7 @@ __device__ unsigned long long g_stats[16];
 #endif
 
 struct __align__(16) TileSmem {
-    float4 st[5][NB];           // staged per-primitive coefficients
-    uint8_t pm[NB];             // Gaussians: warp-patch masks
+    float4 st[3][NB];           // staged surfel coefficients
     uint32_t zp[NB];            // surfels: nearest disc depth with the low byte = warp-patch mask
     uint32_t sp[NB];            // surfels: packed index of the staged primitive
     float wmax[NWARP];          // per-warp max depth (surfels: current hits; Gaussians: final)
@@ -364,11 +363,17 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
     // ------------------------------------------------------------ pass 2
     if constexpr (MODE & 2) {
         float wsum = 0.f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
-        const float wm = warp_max(inside ? ds : -INFINITY);
-        if (lane == 0) sm.wmax[warp] = wm;
-        __syncthreads();
-        const float dmax = tile_max(sm);
-        if (threadIdx.x == 0) { GES_STAT(10, 1); GES_STAT(11, dmax == INFINITY); }
+        // Warp-independent: each warp walks the tile's Gaussian list itself, 32
+        // entries at a time, culls against ITS patch (pixel range and the
+        // warp's own max surfel depth) from the 16-byte cull record, and
+        // evaluates the few survivors lane by lane (the survivor's lane loads
+        // its record once and broadcasts it).  No shared staging, no CTA
+        // barriers: the pass is latency-bound and warps must not wait on each
+        // other.
+        if constexpr ((MODE & 1) == 0) __syncthreads();   // gslab_end written in the prologue
+        const float wdmax = warp_max(inside ? ds : -INFINITY);
+        if (threadIdx.x == 0) GES_STAT(10, 1);
+        if (lane == 0) GES_STAT(11, wdmax == INFINITY);
         const float lx = (float)plx, ly = (float)ply;
         float pe = 0.f;
         if constexpr (GK == 2) {
@@ -376,120 +381,100 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
             pe = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
         }
         const int ox = tx * TILE, oy = ty * TILE;
-        const uint32_t beg = gbeg, end = gend;
-        for (uint32_t base = beg; base < end; base += NB) {
-            // keys (depth - eps) are binned near-to-far: the rest fail every gate
-            if (slab_floor(sm.gslab_end, a.slabs, base - beg, lane) > dmax) break;
-            const int nb = min((uint32_t)NB, end - base);
-            const uint32_t id = gid;   // ids loaded one batch ahead (first batch: at kernel start)
-            if (base + NB + threadIdx.x < end) gid = a.g_list[base + NB + threadIdx.x];
-            if ((int)threadIdx.x < nb) {
-                uint32_t mask;
+        const int px0 = (warp & 1) * 8, py0 = (warp >> 1) * 4;   // this warp's 8x4 patch
+        for (uint32_t base = gbeg; base < gend; base += 32) {
+            // keys (depth - eps) are binned near-to-far: the rest fail every gate of the patch
+            if (slab_floor(sm.gslab_end, a.slabs, base - gbeg, lane) > wdmax) break;
+            const uint32_t e = base + lane;
+            bool live = false;
+            float v[16];
+            if (e < gend) {
+                const uint32_t id = a.g_list[e];
                 if constexpr (GK == 3) {
-                    // the cull needs only c; the rest is fetched for survivors only
                     const GaussRec* r = reinterpret_cast<const GaussRec*>(a.grec) + id;
                     const float4 c = __ldg(&r->c);
                     const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
-                    mask = patch_mask<1>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
-                                         span_hi(syr) - oy);
                     // exact conservative cull: d < fl(max_ds + eps) is necessary for the gate
-#pragma unroll
-                    for (int w = 0; w < NWARP; ++w)
-                        if (!(c.x < sm.wmax[w] + c.y)) mask &= ~(1u << w);
-                    if (mask) {
+                    live = span_lo(sxr) - ox <= px0 + 7 && span_hi(sxr) - ox >= px0 &&
+                           span_lo(syr) - oy <= py0 + 3 && span_hi(syr) - oy >= py0 && c.x < wdmax + c.y;
+                    if (live) {
                         const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2);
-                        const float mxt = (r0.x - (float)ox) + (r0.y - 0.5f);
-                        const float myt = (r0.z - (float)oy) + (r0.w - 0.5f);
-                        sm.st[0][threadIdx.x] = make_float4(mxt, myt, r1.x, r1.y);
-                        sm.st[1][threadIdx.x] = make_float4(r1.z, r1.w, c.x, c.y);
-                        sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r2.w, r2.x);
+                        v[0] = (r0.x - (float)ox) + (r0.y - 0.5f);   // mean relative to the tile
+                        v[1] = (r0.z - (float)oy) + (r0.w - 0.5f);
+                        v[2] = r1.x; v[3] = r1.y; v[4] = r1.z; v[5] = r1.w;
+                        v[6] = c.x; v[7] = c.y; v[8] = r2.x; v[9] = r2.y; v[10] = r2.z; v[11] = r2.w;
+                        if constexpr (GEOM) {
+                            const float4 nv = __ldg(a.g_nrm + id);
+                            v[12] = nv.x; v[13] = nv.y; v[14] = nv.z;
+                        }
                     }
                 } else {
                     const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + id;
                     const float4 c = __ldg(&r->c);
                     const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
-                    mask = patch_mask<1>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
-                                         span_hi(syr) - oy);
-#pragma unroll
-                    for (int w = 0; w < NWARP; ++w)   // key = nearest support depth - eps
-                        if (c.x > sm.wmax[w]) mask &= ~(1u << w);
-                    if (mask) {
+                    live = span_lo(sxr) - ox <= px0 + 7 && span_hi(sxr) - ox >= px0 &&
+                           span_lo(syr) - oy <= py0 + 3 && span_hi(syr) - oy >= py0 && !(c.x > wdmax);
+                    if (live) {
                         const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2),
                                      r3 = __ldg(&r->r3), r4 = __ldg(&r->r4);
                         const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
-                        const float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
-                        const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
-                        const float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
-                        sm.st[0][threadIdx.x] = make_float4(d0, r0.y, r0.z, r0.w);
-                        sm.st[1][threadIdx.x] = make_float4(u0, r1.y, r1.z, v0);
-                        sm.st[2][threadIdx.x] = make_float4(r2.y, r2.z, r3.x, c.y);
-                        sm.st[3][threadIdx.x] = make_float4(r4.x, r4.y, r4.z, r3.y);
+                        v[0] = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x)); v[1] = r0.y; v[2] = r0.z; v[3] = r0.w;
+                        v[4] = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x)); v[5] = r1.y; v[6] = r1.z;
+                        v[7] = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x)); v[8] = r2.y; v[9] = r2.z;
+                        v[10] = r3.x; v[11] = c.y; v[12] = r3.y;          // sigma, eps, r2max
+                        v[13] = r4.x; v[14] = r4.y; v[15] = r4.z;         // colour
                     }
                 }
-                if constexpr (GEOM) {
-                    if (mask) sm.st[4][threadIdx.x] = __ldg(a.g_nrm + id);
-                }
-                sm.pm[threadIdx.x] = (uint8_t)mask;
             }
-#ifdef GES_STATS
-            {
-                const unsigned live = __ballot_sync(0xffffffffu, (int)threadIdx.x < nb && sm.pm[threadIdx.x]);
-                if (lane == 0) GES_STAT(7, __popc(live));
-                if (threadIdx.x == 0) { GES_STAT(5, 1); GES_STAT(6, nb); }
-            }
-#endif
-            __syncthreads();
-            for (int c = 0; c < nb; c += 32) {
-                const int e = c + lane;
-                uint32_t vote = __ballot_sync(0xffffffffu, e < nb && ((sm.pm[e] >> warp) & 1u));
-                while (vote) {
-                    const int j = c + __ffs(vote) - 1;
-                    vote &= vote - 1;
-                    const float4 A = sm.st[0][j], B = sm.st[1][j], C = sm.st[2][j];
-                    if (lane == 0) GES_STAT(8, 1);
-                    if constexpr (GK == 3) {
-                        // forward.py:301-311
-                        const float dx = lx - A.x, dy = ly - A.y;
-                        const float p = fmaf(A.z * dx, dx, fmaf(B.x * dy, dy, A.w * dx * dy));
-                        if (p >= C.w) {
-                            const float al = B.y * __expf(p);
-                            if (al >= ALPHA_CUTOFF_F && B.z < ds + B.w) {
-                                GES_STAT(9, 1);
-                                wsum += al;
-                                cr = fmaf(al, C.x, cr); cg = fmaf(al, C.y, cg); cb = fmaf(al, C.z, cb);
-                                if constexpr (GEOM) {
-                                    const float4 N = sm.st[4][j];
-                                    dsum = fmaf(al, B.z, dsum);
-                                    nx = fmaf(al, N.x, nx); ny = fmaf(al, N.y, ny); nz = fmaf(al, N.z, nz);
-                                }
+            uint32_t vote = __ballot_sync(0xffffffffu, live);
+            while (vote) {
+                const int j = __ffs(vote) - 1;
+                vote &= vote - 1;
+                if (lane == 0) GES_STAT(8, 1);
+                float w[16];
+                constexpr int NV = GK == 3 ? (GEOM ? 15 : 12) : 16;
+#pragma unroll
+                for (int k = 0; k < NV; ++k) w[k] = __shfl_sync(0xffffffffu, v[k], j);
+                if constexpr (GK == 3) {
+                    // forward.py:301-311
+                    const float dx = lx - w[0], dy = ly - w[1];
+                    const float p = fmaf(w[2] * dx, dx, fmaf(w[4] * dy, dy, w[3] * dx * dy));
+                    if (p >= w[8]) {
+                        const float al = w[5] * __expf(p);
+                        if (al >= ALPHA_CUTOFF_F && w[6] < ds + w[7]) {
+                            GES_STAT(9, 1);
+                            wsum += al;
+                            cr = fmaf(al, w[9], cr); cg = fmaf(al, w[10], cg); cb = fmaf(al, w[11], cb);
+                            if constexpr (GEOM) {
+                                dsum = fmaf(al, w[6], dsum);
+                                nx = fmaf(al, w[12], nx); ny = fmaf(al, w[13], ny); nz = fmaf(al, w[14], nz);
                             }
                         }
-                    } else {
-                        // forward.py:361-379
-                        const float4 E = sm.st[3][j];
-                        const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
-                        const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
-                        const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
-                        const float r2u = fmaf(U, U, V * V);
-                        if (r2u <= E.w * den * den && fabsf(den) > pe) {
-                            const float inv = __fdividef(1.0f, den);
-                            const float t = A.w * inv;
-                            const float q2 = r2u * inv * inv;
-                            const float al = C.z * __expf(-0.5f * q2);
-                            if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds + C.w) {
-                                wsum += al;
-                                cr = fmaf(al, E.x, cr); cg = fmaf(al, E.y, cg); cb = fmaf(al, E.z, cb);
-                                if constexpr (GEOM) {
-                                    const float4 N = sm.st[4][j];
-                                    dsum = fmaf(al, t, dsum);
-                                    nx = fmaf(al, N.x, nx); ny = fmaf(al, N.y, ny); nz = fmaf(al, N.z, nz);
-                                }
+                    }
+                } else {
+                    // forward.py:361-379
+                    const float den = fmaf(w[2], ly, fmaf(w[1], lx, w[0]));
+                    const float U = fmaf(w[6], ly, fmaf(w[5], lx, w[4]));
+                    const float V = fmaf(w[9], ly, fmaf(w[8], lx, w[7]));
+                    const float r2u = fmaf(U, U, V * V);
+                    if (r2u <= w[12] * den * den && fabsf(den) > pe) {
+                        const float inv = __fdividef(1.0f, den);
+                        const float t = w[3] * inv;
+                        const float q2 = r2u * inv * inv;
+                        const float al = w[10] * __expf(-0.5f * q2);
+                        if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds + w[11]) {
+                            wsum += al;
+                            cr = fmaf(al, w[13], cr); cg = fmaf(al, w[14], cg); cb = fmaf(al, w[15], cb);
+                            if constexpr (GEOM) {
+                                // planar normal: camera-facing plane normal (forward.py:337, :379)
+                                const float4 nv = __ldg(a.g_nrm + a.g_list[base + j]);
+                                dsum = fmaf(al, t, dsum);
+                                nx = fmaf(al, nv.x, nx); ny = fmaf(al, nv.y, ny); nz = fmaf(al, nv.z, nz);
                             }
                         }
                     }
                 }
             }
-            __syncthreads();
         }
         if constexpr ((MODE & 1) != 0) cs = resolve_surfel_color<SS * SS>(a, best, bp, lane);
         if (inside) {
