@@ -140,12 +140,12 @@ __device__ __forceinline__ float3 surfel_nvis(const TileArgs& a, uint32_t sid) {
 // the rarely executed, register-hungry evaluation does not raise the
 // kernel's register count or copy the kernel parameters to the stack.
 static __device__ __noinline__ float3 surfel_color_eval(const float* __restrict__ sh, const float4* __restrict__ pos,
-                                                        int deg, double cx, double cy, double cz, uint32_t pidx) {
+                                                        int deg, float cx, float cy, float cz, uint32_t pidx) {
     const float4 p = __ldg(pos + pidx);
-    const double dx = cx - p.x, dy = cy - p.y, dz = cz - p.z;
-    const double inv = 1.0 / fmax(sqrt(dx * dx + dy * dy + dz * dz), 1e-12);
+    const float dx = cx - p.x, dy = cy - p.y, dz = cz - p.z;   // |d| ~ scene distance: fp32 is ample
+    const float inv = 1.0f / fmaxf(sqrtf(dx * dx + dy * dy + dz * dz), 1e-12f);
     const int K3 = (deg + 1) * (deg + 1) * 3;
-    return sh_color_dyn(deg, sh + (size_t)pidx * K3, (float)(dx * inv), (float)(dy * inv), (float)(dz * inv));
+    return sh_color_dyn(deg, sh + (size_t)pidx * K3, dx * inv, dy * inv, dz * inv);
 }
 
 // Deferred surfel colour (SURVEY 7 "SH only for winning surfels"): after pass
@@ -164,7 +164,8 @@ __device__ __forceinline__ float3 resolve_surfel_color(const TileArgs& a, const 
         const int leader = __ffs(peers) - 1;
         float3 c = make_float3(a.bg[0], a.bg[1], a.bg[2]);
         if (cov && lane == leader)
-            c = surfel_color_eval(a.s_sh, a.s_pos, a.sh_deg, a.cpos[0], a.cpos[1], a.cpos[2], bp[s]);
+            c = surfel_color_eval(a.s_sh, a.s_pos, a.sh_deg, (float)a.cpos[0], (float)a.cpos[1], (float)a.cpos[2],
+                                  bp[s]);
         c.x = __shfl_sync(0xffffffffu, c.x, leader);
         c.y = __shfl_sync(0xffffffffu, c.y, leader);
         c.z = __shfl_sync(0xffffffffu, c.z, leader);
