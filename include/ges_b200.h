@@ -55,6 +55,8 @@ typedef struct ges_settings {
     float epsilon_value;
     int32_t with_geometry;    /* 0/1 */
     float background[3];
+    int32_t tile_mode;        /* 0 auto; 1: 16x16-pixel tiles; 2: 32x32-pixel tiles,
+                                 2x2 pixels per thread (ss=1 without geometry) */
 } ges_settings_t;
 
 /* Source scene in the reference's storage layout (primitives.py:42-161),

@@ -32,7 +32,7 @@ class Camera(C.Structure):
 class Settings(C.Structure):
     _fields_ = [("supersample", C.c_int32), ("layers", C.c_int32), ("mip", C.c_int32),
                 ("epsilon_mode", C.c_int32), ("epsilon_value", C.c_float),
-                ("with_geometry", C.c_int32), ("background", C.c_float * 3)]
+                ("with_geometry", C.c_int32), ("background", C.c_float * 3), ("tile_mode", C.c_int32)]
 
 
 class SceneSrc(C.Structure):

@@ -42,6 +42,7 @@ int check_settings(const ges_settings_t* st) {
     if (st->supersample != 1 && st->supersample != 4) return fail(GES_EINVAL, "supersample must be 1 or 4");
     if (st->layers < 0 || st->layers > 2) return fail(GES_EINVAL, "unknown layer mode");
     if (st->epsilon_mode != 0 && st->epsilon_mode != 1) return fail(GES_EINVAL, "unknown epsilon mode");
+    if (st->tile_mode < 0 || st->tile_mode > 2) return fail(GES_EINVAL, "tile_mode must be 0, 1 or 2");
     return GES_OK;
 }
 
@@ -73,14 +74,25 @@ struct Frame {
     uint32_t *list_s, *list_g;
     ges_frame_status_t* status;
     size_t bytes;
-    int ntx, nty, ntiles;
+    int ntx, nty, ntiles, px;
 };
 
-Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, int64_t cap_s, int64_t cap_g) {
+// Base pixels per tile-kernel thread per axis: 2 (32x32-pixel tiles, 2x2
+// pixels per thread) for plain frames large enough to fill the GPU, else 1.
+int tile_px_of(const ges_camera_t* cam, const ges_settings_t* st) {
+    if (st->supersample != 1 || st->with_geometry) return 1;
+    if (st->tile_mode == 1 || st->tile_mode == 2) return st->tile_mode;
+    return (int64_t)cam->width * cam->height >= 512 * 512 ? 2 : 1;
+}
+
+Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st, int64_t cap_s,
+             int64_t cap_g) {
     Frame f{};
     Carve c{static_cast<char*>(base)};
-    f.ntx = (cam->width + TILE - 1) / TILE;
-    f.nty = (cam->height + TILE - 1) / TILE;
+    f.px = tile_px_of(cam, st);
+    const int tp = TILE * f.px;
+    f.ntx = (cam->width + tp - 1) / tp;
+    f.nty = (cam->height + tp - 1) / tp;
     f.ntiles = f.ntx * f.nty;
     size_t ns = (size_t)sc->n_surfels, ng = (size_t)sc->n_gaussians;
     f.status = c.take<ges_frame_status_t>(1);
@@ -139,7 +151,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     if (!out) return fail(GES_EINVAL, "outputs is NULL");
     if (cap_s < 0 || cap_g < 0 || cap_s >= (1ll << 32) || cap_g >= (1ll << 32))
         return fail(GES_EINVAL, "pair capacity out of range");
-    Frame f = layout(ws, sc, cam, cap_s, cap_g);
+    Frame f = layout(ws, sc, cam, st, cap_s, cap_g);
     if (!ws || ws_bytes < f.bytes) return fail(GES_EWORKSPACE, "workspace too small (see ges_workspace_bytes)");
     ges_frame_status_t* status = status_dev ? status_dev : f.status;
     const int grid = st->supersample == 4 ? 2 : 1;
@@ -156,13 +168,15 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     mark(1);
     CamK cs = make_cam(*cam, grid), cg = make_cam(*cam, 1);
     const SlabMap slabs = slab_map(*sc, cs);
-    Grid gs{cs.W, cs.H, TILE * grid, f.ntx, f.nty, slabs}, gg{cg.W, cg.H, TILE, f.ntx, f.nty, slabs};
+    const int tp = TILE * f.px;   // tile edge in base pixels
+    Grid gs{cs.W, cs.H, tp * grid, f.ntx, f.nty, slabs}, gg{cg.W, cg.H, tp, f.ntx, f.nty, slabs};
     ges_scene_t scs = *sc;
     if (!do_s) scs.n_surfels = 0;
     if (!do_g) scs.n_gaussians = 0;
-    const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, TILE * grid,
-                     grid == 2 ? 5 : 4};
-    const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE, 4};
+    auto log2i = [](int v) { int k = 0; while ((1 << k) < v) ++k; return k; };
+    const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, tp * grid,
+                     log2i(tp * grid)};
+    const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, tp, log2i(tp)};
     if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, nullptr, f.cnt_s}, s)))
         return cuda_fail(e, "surfel preprocess");
     if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))
@@ -200,7 +214,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
         // ignores layers); force the Gaussian pass.
         tmode = 2;
     }
-    if ((e = launch_tile(a, st->supersample, tmode, sc->gaussian_dim, st->with_geometry != 0, s)))
+    if ((e = launch_tile(a, st->supersample, f.px, tmode, sc->gaussian_dim, st->with_geometry != 0, s)))
         return cuda_fail(e, "tile kernel");
     mark(5);
     return GES_OK;
@@ -253,7 +267,7 @@ int ges_scene_pack(const ges_scene_src_t* src, void* blob, size_t blob_bytes, ge
 size_t ges_workspace_bytes(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st,
                            int64_t cap_s, int64_t cap_g) {
     if (check_scene(sc) || check_cam(cam) || check_settings(st) || cap_s < 0 || cap_g < 0) return 0;
-    return layout(nullptr, sc, cam, cap_s, cap_g).bytes;
+    return layout(nullptr, sc, cam, st, cap_s, cap_g).bytes;
 }
 
 int ges_render(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st, const ges_outputs_t* out,

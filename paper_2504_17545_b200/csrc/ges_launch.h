@@ -59,8 +59,9 @@ struct TileArgs {
     const ges_frame_status_t* status;
 };
 
-// mode: 1 = surfels only, 2 = Gaussians only (external depth), 3 = both.
-cudaError_t launch_tile(const TileArgs& a, int ss, int mode, int g_kind, bool geom, cudaStream_t s);
+// mode: 1 = surfels only, 2 = Gaussians only (external depth), 3 = both;
+// px: base pixels per thread per axis (1: 16x16 tiles, 2: 32x32 tiles).
+cudaError_t launch_tile(const TileArgs& a, int ss, int px, int mode, int g_kind, bool geom, cudaStream_t s);
 
 int read_stats(unsigned long long* out);   // 16 counters, then reset (GES_STATS builds)
 

@@ -86,7 +86,7 @@ __device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1,
 // warps' primitives share tiles).
 __device__ __forceinline__ void count_tiles(uint32_t* cnt, const Grid& g, bool live, int x0, int x1, int y0,
                                             int y1, float zkey) {
-    const int sh = g.tile_px == 32 ? 5 : 4;   // 16- or 32-px tiles
+    const int sh = __ffs(g.tile_px) - 1;   // tiles are 16, 32 or 64 px
     int tx0 = x0 >> sh, tx1 = x1 >> sh, ty0 = y0 >> sh, ty1 = y1 >> sh;
     int tx = tx0, ty = ty0;
     bool more = live;

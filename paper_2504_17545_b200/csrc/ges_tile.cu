@@ -151,12 +151,10 @@ static __device__ __noinline__ float3 surfel_color_eval(const float* __restrict_
 // Deferred surfel colour (SURVEY 7 "SH only for winning surfels"): after pass
 // 1 each lane knows its winners; lanes of a warp that share a winner elect
 // one lane to evaluate its SH (all elected lanes evaluate in one SIMT pass)
-// and broadcast it.  Box mean over sub-samples for ss=4 (forward.py:201-203).
-// Must be called by all 32 lanes.
+// and broadcast it.  Must be called by all 32 lanes.
 template <int NS>
-__device__ __forceinline__ float3 resolve_surfel_color(const TileArgs& a, const unsigned long long* best,
-                                                       const uint32_t* bp, int lane) {
-    float3 acc = make_float3(0.f, 0.f, 0.f);
+__device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, const unsigned long long* best,
+                                                      const uint32_t* bp, int lane, float3* col) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
         const bool cov = best[s] != ~0ull;
@@ -169,29 +167,31 @@ __device__ __forceinline__ float3 resolve_surfel_color(const TileArgs& a, const 
         c.x = __shfl_sync(0xffffffffu, c.x, leader);
         c.y = __shfl_sync(0xffffffffu, c.y, leader);
         c.z = __shfl_sync(0xffffffffu, c.z, leader);
-        if (!cov) c = make_float3(a.bg[0], a.bg[1], a.bg[2]);
-        acc.x += c.x; acc.y += c.y; acc.z += c.z;
+        col[s] = cov ? c : make_float3(a.bg[0], a.bg[1], a.bg[2]);
     }
-    if (NS > 1) {
-        acc.x /= (float)NS; acc.y /= (float)NS; acc.z /= (float)NS;
-    }
-    return acc;
 }
 
-template <int SS, int MODE, int GK, bool GEOM>
-__global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
+// SS: supersampling of the surfel pass (1, or 2 = the 2x2 grid of ss=4);
+// PX: base pixels per thread per axis (1: 16x16-pixel tiles; 2: 32x32-pixel
+// tiles, each thread a 2x2 pixel block, so every staged surfel and every
+// list step is shared by 4 pixels).  A thread owns G x G = (SS*PX)^2 samples
+// in pass 1 and PX x PX pixels in pass 2.
+template <int SS, int PX, int MODE, int GK, bool GEOM>
+__global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileArgs a) {
+    constexpr int G = SS * PX, NS = G * G, NP = PX * PX, TP = TILE * PX;
     __shared__ TileSmem sm;
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = blockIdx.x, ty = blockIdx.y;
     const int tile = ty * a.ntx + tx;
     const int plx = (warp & 1) * 8 + (lane & 7), ply = (warp >> 1) * 4 + (lane >> 3);
-    const int x = tx * TILE + plx, y = ty * TILE + ply;
-    const bool inside = x < a.W && y < a.H;
-    const int64_t pix = (int64_t)y * a.W + x;
+    const int bx = tx * TP + PX * plx, by = ty * TP + PX * ply;   // first base pixel of the thread
 
-    float ds = INFINITY;             // surfel depth of this pixel (sub-sample 0)
-    float3 cs = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+    float ds[NP];                    // surfel depth per pixel (sub-sample 0 of the pixel)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) ds[p] = INFINITY;
+    auto inside_px = [&](int p) { return bx + p % PX < a.W && by + p / PX < a.H; };
+    auto pix_of = [&](int p) { return (int64_t)(by + p / PX) * a.W + (bx + p % PX); };
 
     // Issue every list-position load of both passes now: tile offsets, slab
     // ends and the first batch of Gaussian ids are independent of pass 1, so
@@ -207,31 +207,31 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
 
     // best[s]: packed (t_bits << 32 | id) of the nearest surfel hit so far;
     // bp[s]: its packed index (SH address of the deferred colour)
-    constexpr int NS = SS * SS;
     unsigned long long best[NS];
     uint32_t bp[NS];
 
     // ------------------------------------------------------------ pass 1
     if constexpr (MODE & 1) {
         // tb[s]: the best t inflated by 1e-5 (candidate filter and culling bound;
-        // pixels outside the image start at 0 so they never take work or block culling)
-        float tb[NS], lxf[SS], lyf[SS], pe[NS];
+        // samples outside the image start at 0 so they never take work or block culling)
+        float tb[NS], lxf[G], lyf[G], pe[NS];
 #pragma unroll
-        for (int s = 0; s < SS; ++s) {
-            lxf[s] = (float)(SS * plx + s);
-            lyf[s] = (float)(SS * ply + s);
+        for (int g = 0; g < G; ++g) {
+            lxf[g] = (float)(G * plx + g);
+            lyf[g] = (float)(G * ply + g);
         }
 #pragma unroll
-        for (int sy = 0; sy < SS; ++sy)
+        for (int gy = 0; gy < G; ++gy)
 #pragma unroll
-            for (int sx = 0; sx < SS; ++sx) {
-                int X = SS * x + sx, Y = SS * y + sy;
+            for (int gx = 0; gx < G; ++gx) {
+                const int X = bx * SS + gx, Y = by * SS + gy;
                 // |d| of the pixel ray only sets the near-parallel threshold 1e-8|d|
                 const float dxn = ((float)X + 0.5f - a.rcx) * a.rifx, dyn = ((float)Y + 0.5f - a.rcy) * a.rify;
-                pe[sy * SS + sx] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
-                best[sy * SS + sx] = ~0ull;
-                bp[sy * SS + sx] = 0u;
-                tb[sy * SS + sx] = inside ? INFINITY : 0.f;
+                pe[gy * G + gx] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
+                best[gy * G + gx] = ~0ull;
+                bp[gy * G + gx] = 0u;
+                const bool in = bx + gx / SS < a.W && by + gy / SS < a.H;
+                tb[gy * G + gx] = in ? INFINITY : 0.f;
             }
         auto patch_depth = [&]() {
             float m = tb[0];
@@ -239,11 +239,11 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
             for (int s = 1; s < NS; ++s) m = fmaxf(m, tb[s]);
             return warp_max(m);
         };
-        float wmx = INFINITY;          // max over this warp's (sub)pixels of the best depth
+        float wmx = INFINITY;          // max over this warp's samples of the best depth
         if (lane == 0) sm.wmax[warp] = INFINITY;
         if (threadIdx.x < NSLAB) sm.slab_end[threadIdx.x] = a.sbin.cnt[tile * NSLAB + threadIdx.x];
         __syncthreads();
-        const int ox = tx * TILE * SS, oy = ty * TILE * SS;
+        const int ox = tx * TP * SS, oy = ty * TP * SS;
         const uint32_t beg = a.sbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
         uint32_t nid = beg + threadIdx.x < end ? a.s_list[beg + threadIdx.x] : 0u;
         if constexpr ((MODE & 2) != 0) {
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                 const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
                 const float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
                 const uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
-                uint32_t mask = patch_mask<SS>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
-                                               span_hi(syr) - oy);
+                uint32_t mask = patch_mask<G>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
+                                              span_hi(syr) - oy);
                 // hit depth t = nq / den: orient den so that t > 0 <=> den > 0
                 float nq = r0.w, dx_ = r0.y, dy_ = r0.z;
                 if (nq < 0.f) { nq = -nq; d0 = -d0; dx_ = -dx_; dy_ = -dy_; }
@@ -305,11 +305,11 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                     if (lane == 0) GES_STAT(3, 1);
                     const float4 A = sm.st[0][j], B = sm.st[1][j];
 #pragma unroll
-                    for (int sy = 0; sy < SS; ++sy)
+                    for (int gy = 0; gy < G; ++gy)
 #pragma unroll
-                        for (int sx = 0; sx < SS; ++sx) {
-                            const int s = sy * SS + sx;
-                            const float lx = lxf[sx], ly = lyf[sy];
+                        for (int gx = 0; gx < G; ++gx) {
+                            const int s = gy * G + gx;
+                            const float lx = lxf[gx], ly = lyf[gy];
                             const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
                             const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
                             const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
@@ -345,25 +345,37 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                 if (a.sh_bytes > 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + a.sh_bytes - 4));
             }
         }
-        // depth/normal/winner from sub-sample 0 (forward.py:205-207)
-        const bool cov = best[0] != ~0ull;
-        ds = cov ? __uint_as_float((uint32_t)(best[0] >> 32)) : INFINITY;
-        if (inside) {
-            if (a.out.s_depth) a.out.s_depth[pix] = ds;
-            if (a.out.s_winner) a.out.s_winner[pix] = cov ? (int32_t)(uint32_t)best[0] : -1;
-            if (a.out.s_normal) {
-                const float3 n = cov ? surfel_nvis(a, (uint32_t)best[0]) : make_float3(0.f, 0.f, 0.f);
-                a.out.s_normal[3 * pix] = n.x; a.out.s_normal[3 * pix + 1] = n.y;
-                a.out.s_normal[3 * pix + 2] = n.z;
+        // depth/normal/winner of each pixel from its sub-sample 0 (forward.py:205-207)
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int s0 = (p / PX) * SS * G + (p % PX) * SS;
+            const bool cov = best[s0] != ~0ull;
+            ds[p] = cov ? __uint_as_float((uint32_t)(best[s0] >> 32)) : INFINITY;
+            if (inside_px(p)) {
+                const int64_t pix = pix_of(p);
+                if (a.out.s_depth) a.out.s_depth[pix] = ds[p];
+                if (a.out.s_winner) a.out.s_winner[pix] = cov ? (int32_t)(uint32_t)best[s0] : -1;
+                if (a.out.s_normal) {
+                    const float3 n = cov ? surfel_nvis(a, (uint32_t)best[s0]) : make_float3(0.f, 0.f, 0.f);
+                    a.out.s_normal[3 * pix] = n.x; a.out.s_normal[3 * pix + 1] = n.y;
+                    a.out.s_normal[3 * pix + 2] = n.z;
+                }
             }
         }
     } else {
-        if (inside && a.ds_in) ds = a.ds_in[pix];
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+            if (inside_px(p) && a.ds_in) ds[p] = a.ds_in[pix_of(p)];
     }
 
     // ------------------------------------------------------------ pass 2
+    float wsum[NP], cr[NP], cg[NP], cb[NP], dsum[NP], nx[NP], ny[NP], nz[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        wsum[p] = cr[p] = cg[p] = cb[p] = 0.f;
+        dsum[p] = nx[p] = ny[p] = nz[p] = 0.f;
+    }
     if constexpr (MODE & 2) {
-        float wsum = 0.f, cr = 0.f, cg = 0.f, cb = 0.f, dsum = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
         // Warp-independent: each warp walks the tile's Gaussian list itself, 32
         // entries at a time, culls against ITS patch (pixel range and the
         // warp's own max surfel depth) from the 16-byte cull record, and
@@ -372,17 +384,24 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
         // barriers: the pass is latency-bound and warps must not wait on each
         // other.
         if constexpr ((MODE & 1) == 0) __syncthreads();   // gslab_end written in the prologue
-        const float wdmax = warp_max(inside ? ds : -INFINITY);
+        float dm = -INFINITY;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) dm = fmaxf(dm, inside_px(p) ? ds[p] : -INFINITY);
+        const float wdmax = warp_max(dm);
         if (threadIdx.x == 0) GES_STAT(10, 1);
         if (lane == 0) GES_STAT(11, wdmax == INFINITY);
-        const float lx = (float)plx, ly = (float)ply;
-        float pe = 0.f;
-        if constexpr (GK == 2) {
-            const float dxn = ((float)x + 0.5f - a.gcx) * a.gifx, dyn = ((float)y + 0.5f - a.gcy) * a.gify;
-            pe = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
+        float pe[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            pe[p] = 0.f;
+            if constexpr (GK == 2) {
+                const float dxn = ((float)(bx + p % PX) + 0.5f - a.gcx) * a.gifx;
+                const float dyn = ((float)(by + p / PX) + 0.5f - a.gcy) * a.gify;
+                pe[p] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
+            }
         }
-        const int ox = tx * TILE, oy = ty * TILE;
-        const int px0 = (warp & 1) * 8, py0 = (warp >> 1) * 4;   // this warp's 8x4 patch
+        const int ox = tx * TP, oy = ty * TP;
+        const int px0 = (warp & 1) * 8 * PX, py0 = (warp >> 1) * 4 * PX;   // this warp's patch
         for (uint32_t base = gbeg; base < gend; base += 32) {
             // keys (depth - eps) are binned near-to-far: the rest fail every gate of the patch
             if (slab_floor(sm.gslab_end, a.slabs, base - gbeg, lane) > wdmax) break;
@@ -396,8 +415,9 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                     const float4 c = __ldg(&r->c);
                     const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
                     // exact conservative cull: d < fl(max_ds + eps) is necessary for the gate
-                    live = span_lo(sxr) - ox <= px0 + 7 && span_hi(sxr) - ox >= px0 &&
-                           span_lo(syr) - oy <= py0 + 3 && span_hi(syr) - oy >= py0 && c.x < wdmax + c.y;
+                    live = span_lo(sxr) - ox <= px0 + 8 * PX - 1 && span_hi(sxr) - ox >= px0 &&
+                           span_lo(syr) - oy <= py0 + 4 * PX - 1 && span_hi(syr) - oy >= py0 &&
+                           c.x < wdmax + c.y;
                     if (live) {
                         const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2);
                         v[0] = (r0.x - (float)ox) + (r0.y - 0.5f);   // mean relative to the tile
@@ -413,8 +433,8 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                     const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + id;
                     const float4 c = __ldg(&r->c);
                     const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
-                    live = span_lo(sxr) - ox <= px0 + 7 && span_hi(sxr) - ox >= px0 &&
-                           span_lo(syr) - oy <= py0 + 3 && span_hi(syr) - oy >= py0 && !(c.x > wdmax);
+                    live = span_lo(sxr) - ox <= px0 + 8 * PX - 1 && span_hi(sxr) - ox >= px0 &&
+                           span_lo(syr) - oy <= py0 + 4 * PX - 1 && span_hi(syr) - oy >= py0 && !(c.x > wdmax);
                     if (live) {
                         const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2),
                                      r3 = __ldg(&r->r3), r4 = __ldg(&r->r4);
@@ -436,114 +456,145 @@ __global__ void __launch_bounds__(NB, 6) k_tile(TileArgs a) {
                 constexpr int NV = GK == 3 ? (GEOM ? 15 : 12) : 16;
 #pragma unroll
                 for (int k = 0; k < NV; ++k) w[k] = __shfl_sync(0xffffffffu, v[k], j);
-                if constexpr (GK == 3) {
-                    // forward.py:301-311
-                    const float dx = lx - w[0], dy = ly - w[1];
-                    const float p = fmaf(w[2] * dx, dx, fmaf(w[4] * dy, dy, w[3] * dx * dy));
-                    if (p >= w[8]) {
-                        const float al = w[5] * __expf(p);
-                        if (al >= ALPHA_CUTOFF_F && w[6] < ds + w[7]) {
-                            GES_STAT(9, 1);
-                            wsum += al;
-                            cr = fmaf(al, w[9], cr); cg = fmaf(al, w[10], cg); cb = fmaf(al, w[11], cb);
-                            if constexpr (GEOM) {
-                                dsum = fmaf(al, w[6], dsum);
-                                nx = fmaf(al, w[12], nx); ny = fmaf(al, w[13], ny); nz = fmaf(al, w[14], nz);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    const float lx = (float)(PX * plx + p % PX), ly = (float)(PX * ply + p / PX);
+                    if constexpr (GK == 3) {
+                        // forward.py:301-311
+                        const float dx = lx - w[0], dy = ly - w[1];
+                        const float pw = fmaf(w[2] * dx, dx, fmaf(w[4] * dy, dy, w[3] * dx * dy));
+                        if (pw >= w[8]) {
+                            const float al = w[5] * __expf(pw);
+                            if (al >= ALPHA_CUTOFF_F && w[6] < ds[p] + w[7]) {
+                                GES_STAT(9, 1);
+                                wsum[p] += al;
+                                cr[p] = fmaf(al, w[9], cr[p]); cg[p] = fmaf(al, w[10], cg[p]);
+                                cb[p] = fmaf(al, w[11], cb[p]);
+                                if constexpr (GEOM) {
+                                    dsum[p] = fmaf(al, w[6], dsum[p]);
+                                    nx[p] = fmaf(al, w[12], nx[p]); ny[p] = fmaf(al, w[13], ny[p]);
+                                    nz[p] = fmaf(al, w[14], nz[p]);
+                                }
                             }
                         }
-                    }
-                } else {
-                    // forward.py:361-379
-                    const float den = fmaf(w[2], ly, fmaf(w[1], lx, w[0]));
-                    const float U = fmaf(w[6], ly, fmaf(w[5], lx, w[4]));
-                    const float V = fmaf(w[9], ly, fmaf(w[8], lx, w[7]));
-                    const float r2u = fmaf(U, U, V * V);
-                    if (r2u <= w[12] * den * den && fabsf(den) > pe) {
-                        const float inv = __fdividef(1.0f, den);
-                        const float t = w[3] * inv;
-                        const float q2 = r2u * inv * inv;
-                        const float al = w[10] * __expf(-0.5f * q2);
-                        if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds + w[11]) {
-                            wsum += al;
-                            cr = fmaf(al, w[13], cr); cg = fmaf(al, w[14], cg); cb = fmaf(al, w[15], cb);
-                            if constexpr (GEOM) {
-                                // planar normal: camera-facing plane normal (forward.py:337, :379)
-                                const float4 nv = __ldg(a.g_nrm + a.g_list[base + j]);
-                                dsum = fmaf(al, t, dsum);
-                                nx = fmaf(al, nv.x, nx); ny = fmaf(al, nv.y, ny); nz = fmaf(al, nv.z, nz);
+                    } else {
+                        // forward.py:361-379
+                        const float den = fmaf(w[2], ly, fmaf(w[1], lx, w[0]));
+                        const float U = fmaf(w[6], ly, fmaf(w[5], lx, w[4]));
+                        const float V = fmaf(w[9], ly, fmaf(w[8], lx, w[7]));
+                        const float r2u = fmaf(U, U, V * V);
+                        if (r2u <= w[12] * den * den && fabsf(den) > pe[p]) {
+                            const float inv = __fdividef(1.0f, den);
+                            const float t = w[3] * inv;
+                            const float q2 = r2u * inv * inv;
+                            const float al = w[10] * __expf(-0.5f * q2);
+                            if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds[p] + w[11]) {
+                                wsum[p] += al;
+                                cr[p] = fmaf(al, w[13], cr[p]); cg[p] = fmaf(al, w[14], cg[p]);
+                                cb[p] = fmaf(al, w[15], cb[p]);
+                                if constexpr (GEOM) {
+                                    // planar normal: camera-facing plane normal (forward.py:337, :379)
+                                    const float4 nv = __ldg(a.g_nrm + a.g_list[base + j]);
+                                    dsum[p] = fmaf(al, t, dsum[p]);
+                                    nx[p] = fmaf(al, nv.x, nx[p]); ny[p] = fmaf(al, nv.y, ny[p]);
+                                    nz[p] = fmaf(al, nv.z, nz[p]);
+                                }
                             }
                         }
                     }
                 }
             }
         }
-        if constexpr ((MODE & 1) != 0) cs = resolve_surfel_color<SS * SS>(a, best, bp, lane);
-        if (inside) {
-            if constexpr ((MODE & 1) != 0) {
-                if (a.out.s_color) {
-                    a.out.s_color[3 * pix] = cs.x; a.out.s_color[3 * pix + 1] = cs.y;
-                    a.out.s_color[3 * pix + 2] = cs.z;
-                }
+    }
+
+    // ------------------------------------------------------------ resolve + write
+    float3 cs[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) cs[p] = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+    if constexpr ((MODE & 1) != 0) {
+        float3 col[NS];
+        resolve_surfel_colors<NS>(a, best, bp, lane, col);
+        if constexpr (PX == 1) {   // box mean over the sub-samples (forward.py:201-203)
+            float3 acc = make_float3(0.f, 0.f, 0.f);
+#pragma unroll
+            for (int s = 0; s < NS; ++s) { acc.x += col[s].x; acc.y += col[s].y; acc.z += col[s].z; }
+            if (NS > 1) { acc.x /= (float)NS; acc.y /= (float)NS; acc.z /= (float)NS; }
+            cs[0] = acc;
+        } else {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) cs[p] = col[p];   // SS == 1: one sample per pixel
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        if (!inside_px(p)) continue;
+        const int64_t pix = pix_of(p);
+        if constexpr ((MODE & 1) != 0) {
+            if (a.out.s_color) {
+                a.out.s_color[3 * pix] = cs[p].x; a.out.s_color[3 * pix + 1] = cs[p].y;
+                a.out.s_color[3 * pix + 2] = cs[p].z;
             }
-            if (a.out.g_weight) a.out.g_weight[pix] = wsum;
+        }
+        if constexpr ((MODE & 2) != 0) {
+            if (a.out.g_weight) a.out.g_weight[pix] = wsum[p];
             if (a.out.g_color) {
-                a.out.g_color[3 * pix] = cr; a.out.g_color[3 * pix + 1] = cg; a.out.g_color[3 * pix + 2] = cb;
+                a.out.g_color[3 * pix] = cr[p]; a.out.g_color[3 * pix + 1] = cg[p];
+                a.out.g_color[3 * pix + 2] = cb[p];
             }
             if constexpr (GEOM) {
-                if (a.out.g_depth) a.out.g_depth[pix] = dsum;
+                if (a.out.g_depth) a.out.g_depth[pix] = dsum[p];
                 if (a.out.g_normal) {
-                    a.out.g_normal[3 * pix] = nx; a.out.g_normal[3 * pix + 1] = ny;
-                    a.out.g_normal[3 * pix + 2] = nz;
+                    a.out.g_normal[3 * pix] = nx[p]; a.out.g_normal[3 * pix + 1] = ny[p];
+                    a.out.g_normal[3 * pix + 2] = nz[p];
                 }
             }
             if (a.out.image || a.out.image_rgba8) {
-                const float3 im = im_of(a, cs, wsum, cr, cg, cb);
+                const float3 im = im_of(a, cs[p], wsum[p], cr[p], cg[p], cb[p]);
                 if (a.out.image) {
                     a.out.image[3 * pix] = im.x; a.out.image[3 * pix + 1] = im.y; a.out.image[3 * pix + 2] = im.z;
                 }
                 if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, im);
             }
+        } else {   // surfels_only (forward.py:407-410): empty Gaussian buffers
+            if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, cs[p]);
+            if (a.out.image) {
+                a.out.image[3 * pix] = cs[p].x; a.out.image[3 * pix + 1] = cs[p].y;
+                a.out.image[3 * pix + 2] = cs[p].z;
+            }
+            if (a.out.g_weight) a.out.g_weight[pix] = 0.f;
+            if (a.out.g_color) {
+                a.out.g_color[3 * pix] = 0.f; a.out.g_color[3 * pix + 1] = 0.f; a.out.g_color[3 * pix + 2] = 0.f;
+            }
         }
-    } else {   // surfels_only (forward.py:407-410): empty Gaussian buffers
-      cs = resolve_surfel_color<SS * SS>(a, best, bp, lane);
-      if (inside) {
-        if (a.out.s_color) {
-            a.out.s_color[3 * pix] = cs.x; a.out.s_color[3 * pix + 1] = cs.y; a.out.s_color[3 * pix + 2] = cs.z;
-        }
-        if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, cs);
-        if (a.out.image) {
-            a.out.image[3 * pix] = cs.x; a.out.image[3 * pix + 1] = cs.y; a.out.image[3 * pix + 2] = cs.z;
-        }
-        if (a.out.g_weight) a.out.g_weight[pix] = 0.f;
-        if (a.out.g_color) {
-            a.out.g_color[3 * pix] = 0.f; a.out.g_color[3 * pix + 1] = 0.f; a.out.g_color[3 * pix + 2] = 0.f;
-        }
-      }
     }
 }
 
-template <int SS, int MODE>
+template <int SS, int PX, int MODE>
 static void launch_kind(const TileArgs& a, int g_kind, bool geom, cudaStream_t s) {
     const dim3 nt((unsigned)a.ntx, (unsigned)a.nty);
     if (g_kind == 2) {
-        if (geom) k_tile<SS, MODE, 2, true><<<nt, NB, 0, s>>>(a);
-        else k_tile<SS, MODE, 2, false><<<nt, NB, 0, s>>>(a);
+        if (geom) k_tile<SS, PX, MODE, 2, true><<<nt, NB, 0, s>>>(a);
+        else k_tile<SS, PX, MODE, 2, false><<<nt, NB, 0, s>>>(a);
     } else {
-        if (geom) k_tile<SS, MODE, 3, true><<<nt, NB, 0, s>>>(a);
-        else k_tile<SS, MODE, 3, false><<<nt, NB, 0, s>>>(a);
+        if (geom) k_tile<SS, PX, MODE, 3, true><<<nt, NB, 0, s>>>(a);
+        else k_tile<SS, PX, MODE, 3, false><<<nt, NB, 0, s>>>(a);
     }
 }
 
-cudaError_t launch_tile(const TileArgs& a, int ss, int mode, int g_kind, bool geom, cudaStream_t s) {
+cudaError_t launch_tile(const TileArgs& a, int ss, int px, int mode, int g_kind, bool geom, cudaStream_t s) {
     if (a.ntx * a.nty == 0) return cudaSuccess;
-    if (mode == 2) {
-        launch_kind<1, 2>(a, g_kind, geom, s);
+    if (px == 2) {   // 32x32-pixel tiles, 2x2 pixels per thread (ss=1, no geometry)
+        if (mode == 1) launch_kind<1, 2, 1>(a, 3, false, s);
+        else if (mode == 2) launch_kind<1, 2, 2>(a, g_kind, false, s);
+        else launch_kind<1, 2, 3>(a, g_kind, false, s);
+    } else if (mode == 2) {
+        launch_kind<1, 1, 2>(a, g_kind, geom, s);
     } else if (ss == 4) {
-        if (mode == 1) launch_kind<2, 1>(a, 3, false, s);
-        else launch_kind<2, 3>(a, g_kind, geom, s);
+        if (mode == 1) launch_kind<2, 1, 1>(a, 3, false, s);
+        else launch_kind<2, 1, 3>(a, g_kind, geom, s);
     } else {
-        if (mode == 1) launch_kind<1, 1>(a, 3, false, s);
-        else launch_kind<1, 3>(a, g_kind, geom, s);
+        if (mode == 1) launch_kind<1, 1, 1>(a, 3, false, s);
+        else launch_kind<1, 1, 3>(a, g_kind, geom, s);
     }
     return cudaGetLastError();
 }

@@ -95,6 +95,7 @@ def settings_struct(st) -> _lib.Settings:
     s.epsilon_value = float(st.epsilon_value)
     s.with_geometry = int(bool(st.with_geometry))
     s.background[:] = [float(v) for v in st.background]
+    s.tile_mode = int(getattr(st, "tile_mode", 0))   # not a reference field: 0 = auto
     return s
 
 

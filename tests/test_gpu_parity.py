@@ -381,3 +381,35 @@ def test_odd_sizes_and_aspect():
         out = G.render(sc, cam)
         ora = O.render(sc, cam, settings_ns({}), ties=True)
         assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+
+
+@pytest.mark.parametrize("name", ["g3d_500", "g2d_901", "bg_gonly", "bg_sonly", "eps_const", "mip3d",
+                                  "deg3_64x48", "config1"])
+def test_golden_parity_2x2_pixel_tiles(name):
+    """The 32x32-tile / 2x2-pixels-per-thread kernel variant (auto-selected
+    for large plain frames) forced on the golden cases."""
+    scene, cam, st, gold, _ = load(name)
+    s32 = settings32(st)
+    s32.tile_mode = 2
+    out = G.render(scene, cam, s32)
+    ora = O.render(scene, cam, settings_ns(st), ties=True)
+    ref = dict(image=gold["image"], s_winner=gold["s_winner"], s_depth=gold["s_depth"],
+               s_color=gold["s_color"], s_normal=gold["s_normal"], g_color=gold["g_color"],
+               g_weight=gold["g_weight"])
+    assert_parity(compare(gpu_dict(out), ref, ora.tie), weight_tol=5e-4)
+
+
+def test_tile_modes_agree_480x270():
+    r = np.random.default_rng(46)
+    sc = Scene(S.random_surfels(r, 20000, 3, scale_range=(0.005, 0.02)),
+               S.random_gaussians(r, 6000, 3, scale_range=(0.004, 0.025), extent=1.2), 3, Stage.FROZEN)
+    cam = S.make_camera(481, 271)
+    outs = []
+    for mode in (1, 2):
+        st = G.RenderSettings()
+        st.tile_mode = mode
+        outs.append(G.render(sc, cam, st))
+    assert np.array_equal(outs[0].surfels.winner, outs[1].surfels.winner)
+    assert np.max(np.abs(outs[0].image - outs[1].image)) <= 1e-5
+    ora = O.render(sc, cam, settings_ns({}), ties=True)
+    assert_parity(compare(gpu_dict(outs[1]), ora_dict(ora), ora.tie))
