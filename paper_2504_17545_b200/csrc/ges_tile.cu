@@ -42,7 +42,7 @@ __device__ unsigned long long g_stats[16];
 #endif
 
 struct __align__(16) TileSmem {
-    float4 st[3][NB];           // staged surfel coefficients
+    float4 st[4][NB];           // pass 1: staged surfel coefficients; pass 2: per-warp survivor records
     uint32_t zp[NB];            // surfels: nearest disc depth with the low byte = warp-patch mask
     uint32_t sp[NB];            // surfels: packed index of the staged primitive
     float wmax[NWARP];          // per-warp max depth (surfels: current hits; Gaussians: final)
@@ -447,15 +447,33 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
                     }
                 }
             }
+            // survivors park their record in this warp's slice of shared memory;
+            // every lane then reads each survivor with broadcast loads
+            const int slot = warp * 32 + lane;
+            if (live) {
+                sm.st[0][slot] = make_float4(v[0], v[1], v[2], v[3]);
+                sm.st[1][slot] = make_float4(v[4], v[5], v[6], v[7]);
+                sm.st[2][slot] = make_float4(v[8], v[9], v[10], v[11]);
+                sm.st[3][slot] = make_float4(v[12], v[13], v[14], v[15]);
+            }
             uint32_t vote = __ballot_sync(0xffffffffu, live);
+            __syncwarp();
             while (vote) {
                 const int j = __ffs(vote) - 1;
                 vote &= vote - 1;
                 if (lane == 0) GES_STAT(8, 1);
                 float w[16];
-                constexpr int NV = GK == 3 ? (GEOM ? 15 : 12) : 16;
-#pragma unroll
-                for (int k = 0; k < NV; ++k) w[k] = __shfl_sync(0xffffffffu, v[k], j);
+                {
+                    const float4 q0 = sm.st[0][warp * 32 + j], q1 = sm.st[1][warp * 32 + j],
+                                 q2 = sm.st[2][warp * 32 + j];
+                    w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+                    w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+                    w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
+                    if constexpr (GK == 2 || GEOM) {
+                        const float4 q3 = sm.st[3][warp * 32 + j];
+                        w[12] = q3.x; w[13] = q3.y; w[14] = q3.z; w[15] = q3.w;
+                    }
+                }
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
                     const float lx = (float)(PX * plx + p % PX), ly = (float)(PX * ply + p / PX);
@@ -504,6 +522,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
                     }
                 }
             }
+            __syncwarp();   // the slots are rewritten by the next step
         }
     }
 
