@@ -172,19 +172,25 @@ int ges_smooth_geometry(const float *s_depth, const float *s_normal, const float
                         const float *g_normal, const float *g_weight, float *depth_out,
                         float *normal_out, int64_t n, void *stream);
 
+#define GES_IMAGE_F32_RGB 0   /* (H,W,3) float32: RenderResult.image */
+#define GES_IMAGE_RGBA8 1     /* (H,W,4) uint8: the saved frame, datasets.py:54-56 */
+
 /* End-to-end view batch with HOST buffers (the multi-view caller loop of
  * metrics.py:60-66 / cli.py:165-168): for each host camera, render on the
- * device-resident scene and copy the (H,W,3) f32 image into host_images
- * (pinned memory recommended; all views must share one resolution).
- * image_dev holds TWO device image buffers (2*H*W*3 floats) so the copy of
- * view v on copy_stream overlaps the render of view v+1 on stream.  Returns
- * after enqueueing; synchronise copy_stream before reading host_images.
+ * device-resident scene and copy the image (format GES_IMAGE_*) into
+ * host_images (pinned memory recommended; all views share one resolution).
+ * View v runs on lane v % n_lanes: streams[lane] with its own workspace
+ * workspaces[lane] (ws_bytes each) and status slot, so views of different
+ * lanes overlap; image_dev holds 2 * n_lanes device image buffers and each
+ * copy runs on copy_stream, overlapped with later renders.  Returns after
+ * enqueueing; synchronise copy_stream before reading host_images.
  * status_dev: n_views ges_frame_status_t (device) or NULL. */
 int ges_render_views_host(const ges_scene_t *scene, const ges_camera_t *host_cams,
-                          int32_t n_views, const ges_settings_t *st, float *host_images,
-                          void *workspace, size_t ws_bytes, int64_t surfel_pair_cap,
-                          int64_t gaussian_pair_cap, void *image_dev,
-                          ges_frame_status_t *status_dev, void *stream, void *copy_stream);
+                          int32_t n_views, const ges_settings_t *st, int32_t format,
+                          void *host_images, int32_t n_lanes, void *const *workspaces,
+                          size_t ws_bytes, int64_t surfel_pair_cap, int64_t gaussian_pair_cap,
+                          void *image_dev, ges_frame_status_t *status_dev, void *const *streams,
+                          void *copy_stream);
 
 /* Tile-kernel work counters (16 x u64), then reset.  All zero unless the
  * library was built with -DGES_STATS (tuning builds only; synchronous). */

@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GES_B200_LIB") or os.path.join(HERE, "libges_b200.so")
 
 GES_OK, GES_EINVAL, GES_EDEGREE, GES_EWORKSPACE, GES_ECUDA = 0, 1, 2, 3, 4
+GES_IMAGE_F32_RGB, GES_IMAGE_RGBA8 = 0, 1
 LAYERS = {"full": 0, "surfels_only": 1, "gaussians_only": 2}
 
 # Every symbol include/ges_b200.h declares (checked by tests/test_abi.py).
@@ -92,9 +93,9 @@ def lib():
         "ges_composite": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,
                                     C.c_int64, C.c_void_p]),
         "ges_smooth_geometry": (C.c_int, [C.c_void_p] * 7 + [C.c_int64, C.c_void_p]),
-        "ges_render_views_host": (C.c_int, [P(Scene), P(Camera), C.c_int32, P(Settings), C.c_void_p,
-                                            C.c_void_p, C.c_size_t, C.c_int64, C.c_int64, C.c_void_p,
-                                            C.c_void_p, C.c_void_p, C.c_void_p]),
+        "ges_render_views_host": (C.c_int, [P(Scene), P(Camera), C.c_int32, P(Settings), C.c_int32,
+                                            C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t, C.c_int64,
+                                            C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     }
     sig["ges_debug_stats"] = (C.c_int, [C.POINTER(C.c_uint64)])
     for name, (res, args) in sig.items():

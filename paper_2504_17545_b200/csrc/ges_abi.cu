@@ -321,43 +321,50 @@ int ges_debug_stats(uint64_t* out16) {
 }
 
 int ges_render_views_host(const ges_scene_t* sc, const ges_camera_t* host_cams, int32_t n_views,
-                          const ges_settings_t* st, float* host_images, void* ws, size_t ws_bytes, int64_t cap_s,
-                          int64_t cap_g, void* image_dev, ges_frame_status_t* status_dev, void* stream,
-                          void* copy_stream) {
-    if (!host_cams || !host_images || !image_dev || n_views < 0 || !copy_stream)
+                          const ges_settings_t* st, int32_t format, void* host_images, int32_t n_lanes,
+                          void* const* workspaces, size_t ws_bytes, int64_t cap_s, int64_t cap_g, void* image_dev,
+                          ges_frame_status_t* status_dev, void* const* streams, void* copy_stream) {
+    if (!host_cams || !host_images || !image_dev || n_views < 0 || !copy_stream || n_lanes < 1 || !workspaces ||
+        !streams)
         return fail(GES_EINVAL, "bad view batch arguments");
+    if (format != GES_IMAGE_F32_RGB && format != GES_IMAGE_RGBA8) return fail(GES_EINVAL, "unknown image format");
     if (n_views == 0) return GES_OK;
     for (int v = 1; v < n_views; ++v)
         if (host_cams[v].width != host_cams[0].width || host_cams[v].height != host_cams[0].height)
             return fail(GES_EINVAL, "all views of a batch must share one resolution");
-    cudaStream_t s = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
+    cudaStream_t cs = (cudaStream_t)copy_stream;
     const size_t px = (size_t)host_cams[0].width * host_cams[0].height;
-    const size_t bytes = px * 3 * sizeof(float);
-    cudaEvent_t rendered[2], copied[2];
-    for (int k = 0; k < 2; ++k) {
+    const size_t bytes = px * (format == GES_IMAGE_RGBA8 ? 4 : 3 * sizeof(float));
+    const int nb = 2 * n_lanes;   // image buffers: two per lane
+    cudaEvent_t rendered[64], copied[64];
+    if (nb > 64) return fail(GES_EINVAL, "at most 32 lanes");
+    for (int k = 0; k < nb; ++k) {
         cudaEventCreateWithFlags(&rendered[k], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
     }
     int rc = GES_OK;
     for (int v = 0; v < n_views && rc == GES_OK; ++v) {
-        const int b = v & 1;
-        float* buf = static_cast<float*>(image_dev) + b * px * 3;
-        if (v >= 2) cudaStreamWaitEvent(s, copied[b], 0);   // buffer b free again
+        const int lane = v % n_lanes;
+        const int b = (v / n_lanes) % 2 * n_lanes + lane;   // buffer of this (lane, parity)
+        cudaStream_t s = (cudaStream_t)streams[lane];
+        char* buf = static_cast<char*>(image_dev) + b * bytes;
+        if (v >= nb) cudaStreamWaitEvent(s, copied[b], 0);   // buffer b free again
         ges_outputs_t out{};
-        out.image = buf;
-        rc = ges_render(sc, &host_cams[v], st, &out, ws, ws_bytes, cap_s, cap_g,
-                        status_dev ? status_dev + v : nullptr, stream);
+        if (format == GES_IMAGE_RGBA8) out.image_rgba8 = reinterpret_cast<uint8_t*>(buf);
+        else out.image = reinterpret_cast<float*>(buf);
+        rc = ges_render(sc, &host_cams[v], st, &out, workspaces[lane], ws_bytes, cap_s, cap_g,
+                        status_dev ? status_dev + v : nullptr, s);
         if (rc) break;
         cudaEventRecord(rendered[b], s);
         cudaStreamWaitEvent(cs, rendered[b], 0);
-        cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(host_images) + v * bytes, buf, bytes,
+        cudaError_t e = cudaMemcpyAsync(static_cast<char*>(host_images) + v * bytes, buf, bytes,
                                         cudaMemcpyDeviceToHost, cs);
         if (e != cudaSuccess) rc = cuda_fail(e, "image copy");
         cudaEventRecord(copied[b], cs);
     }
-    cudaStreamWaitEvent(s, copied[0], 0);   // later work on `stream` may reuse image_dev
-    cudaStreamWaitEvent(s, copied[1], 0);
-    for (int k = 0; k < 2; ++k) {           // destroy is deferred by the driver until complete
+    for (int l = 0; l < n_lanes; ++l)   // later work on the lanes may reuse image_dev
+        for (int k = 0; k < nb; ++k) cudaStreamWaitEvent((cudaStream_t)streams[l], copied[k], 0);
+    for (int k = 0; k < nb; ++k) {      // destroy is deferred by the driver until complete
         cudaEventDestroy(rendered[k]);
         cudaEventDestroy(copied[k]);
     }
