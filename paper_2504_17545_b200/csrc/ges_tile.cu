@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
                             // current best (all multiplied out, den > 0 <=> t > 0); the exact
                             // t > 0.01 and packed-key comparison run only for candidates
                             if (den > pe[s] && r2 <= den * den && A.w <= tb[s] * den) {
-                                const float t = A.w / den;
+                                const float t = __fdividef(A.w, den);   // 2 ulp: ties are flagged
                                 const unsigned long long key =
                                     ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
                                 GES_STAT(4, 1);
