@@ -418,6 +418,10 @@ def run_gpu(args, rank, world, local_rank):
                      "frac": achieved / peak, "traffic": traffic,
                      "unit_of_work": "one frame (ges_render: 5 kernels + 2 memsets)",
                      "b_alg_bytes_per_frame": balg, "frame_ms": frame_ms,
+                     "achieved_pipelined": balg * fps / world / 1e9,
+                     "note": "achieved = B_alg / isolated frame time (single stream, ges_render_profiled); "
+                             "achieved_pipelined = B_alg x frames/s per GPU of the multi-stream step. The tile "
+                             "kernel is issue/latency-bound, not HBM-bound (profiles/README.md)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                      "phase_ms": phase, "dominant": max(phase, key=phase.get)},
         "cpu_baseline": cpu,
