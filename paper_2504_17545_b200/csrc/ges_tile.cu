@@ -44,7 +44,6 @@ __device__ unsigned long long g_stats[16];
 struct __align__(16) TileSmem {
     float4 st[4][NB];           // pass 1: staged surfel coefficients; pass 2: per-warp survivor records
     uint32_t zp[NB];            // surfels: nearest disc depth with the low byte = warp-patch mask
-    uint32_t sp[NB];            // surfels: packed index of the staged primitive
     float wmax[NWARP];          // per-warp max depth (surfels: current hits; Gaussians: final)
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
     uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
@@ -205,8 +204,9 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
         if (gbeg + threadIdx.x < gend) gid = a.g_list[gbeg + threadIdx.x];
     }
 
-    // best[s]: packed (t_bits << 32 | id) of the nearest surfel hit so far;
-    // bp[s]: its packed index (SH address of the deferred colour)
+    // best[s]: packed (t_bits << 32 | source id) of the nearest surfel hit so
+    // far; bp[s]: its packed index (SH address of the deferred colour), looked
+    // up once after pass 1
     unsigned long long best[NS];
     uint32_t bp[NS];
 
@@ -214,22 +214,19 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
     if constexpr (MODE & 1) {
         // tb[s]: the best t inflated by 1e-5 (candidate filter and culling bound;
         // samples outside the image start at 0 so they never take work or block culling)
-        float tb[NS], lxf[G], lyf[G], pe[NS];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            lxf[g] = (float)(G * plx + g);
-            lyf[g] = (float)(G * ply + g);
-        }
+        // pe: the near-parallel threshold 1e-8|d|, one per thread (the max over
+        // its samples: the 2x2 block's |d| differ by < 1e-3 relative, inside the
+        // flagged grazing band of the parity rule)
+        float tb[NS], pe = 0.f;
+        const float lx0 = (float)(G * plx), ly0 = (float)(G * ply);
 #pragma unroll
         for (int gy = 0; gy < G; ++gy)
 #pragma unroll
             for (int gx = 0; gx < G; ++gx) {
                 const int X = bx * SS + gx, Y = by * SS + gy;
-                // |d| of the pixel ray only sets the near-parallel threshold 1e-8|d|
                 const float dxn = ((float)X + 0.5f - a.rcx) * a.rifx, dyn = ((float)Y + 0.5f - a.rcy) * a.rify;
-                pe[gy * G + gx] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
+                pe = fmaxf(pe, PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f));
                 best[gy * G + gx] = ~0ull;
-                bp[gy * G + gx] = 0u;
                 const bool in = bx + gx / SS < a.W && by + gy / SS < a.H;
                 tb[gy * G + gx] = in ? INFINITY : 0.f;
             }
@@ -281,7 +278,6 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
                 sm.st[1][threadIdx.x] = make_float4(u0 * IR, r1.y * IR, r1.z * IR, v0 * IR);
                 sm.st[2][threadIdx.x] = make_float4(r2.y * IR, r2.z * IR, r3.w, r3.x);   // r3.w: source id
                 sm.zp[threadIdx.x] = zkey_mask(r3.x, mask);
-                sm.sp[threadIdx.x] = id;
             }
 #ifdef GES_STATS
             {
@@ -304,27 +300,30 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
                     if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
                     if (lane == 0) GES_STAT(3, 1);
                     const float4 A = sm.st[0][j], B = sm.st[1][j];
+                    // den, U, V at the thread's first sample, then stepped by the
+                    // per-sample increments across its G x G block
+                    const float den0 = fmaf(A.z, ly0, fmaf(A.y, lx0, A.x));
+                    const float U0 = fmaf(B.z, ly0, fmaf(B.y, lx0, B.x));
+                    const float V0 = fmaf(C.y, ly0, fmaf(C.x, lx0, B.w));
 #pragma unroll
                     for (int gy = 0; gy < G; ++gy)
 #pragma unroll
                         for (int gx = 0; gx < G; ++gx) {
                             const int s = gy * G + gx;
-                            const float lx = lxf[gx], ly = lyf[gy];
-                            const float den = fmaf(A.z, ly, fmaf(A.y, lx, A.x));
-                            const float U = fmaf(B.z, ly, fmaf(B.y, lx, B.x));
-                            const float V = fmaf(C.y, ly, fmaf(C.x, lx, B.w));
+                            float den = den0, U = U0, V = V0;
+                            if (gx) { den = fmaf(A.y, (float)gx, den); U = fmaf(B.y, (float)gx, U); V = fmaf(C.x, (float)gx, V); }
+                            if (gy) { den = fmaf(A.z, (float)gy, den); U = fmaf(B.z, (float)gy, U); V = fmaf(C.y, (float)gy, V); }
                             const float r2 = fmaf(U, U, V * V);
                             // coverage u^2+v^2 <= R^2, |n.d| > eps|d| and t no later than the
                             // current best (all multiplied out, den > 0 <=> t > 0); the exact
                             // t > 0.01 and packed-key comparison run only for candidates
-                            if (den > pe[s] && r2 <= den * den && A.w <= tb[s] * den) {
+                            if (den > pe && r2 <= den * den && A.w <= tb[s] * den) {
                                 const float t = __fdividef(A.w, den);   // 2 ulp: ties are flagged
                                 const unsigned long long key =
                                     ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
                                 GES_STAT(4, 1);
                                 if (t > NEAR_F && key < best[s]) {
                                     best[s] = key;
-                                    bp[s] = sm.sp[j];
                                     tb[s] = t * 1.00001f;   // margin-inflated best depth
                                 }
                             }
@@ -335,8 +334,11 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
             if (lane == 0) sm.wmax[warp] = wmx;
             __syncthreads();
         }
-        // the winners' SH blocks are read at the end (deferred colour): start
-        // pulling them into L2 now, overlapping the Gaussian pass
+        // the winners' SH blocks are read at the end (deferred colour): find
+        // their packed indices and start pulling them into L2 now, overlapping
+        // the Gaussian pass
+#pragma unroll
+        for (int s = 0; s < NS; ++s) bp[s] = best[s] != ~0ull ? __ldg(a.s_pack + (uint32_t)best[s]) : 0u;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             if (best[s] != ~0ull) {
