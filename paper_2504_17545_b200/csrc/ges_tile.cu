@@ -148,25 +148,75 @@ static __device__ __noinline__ float3 surfel_color_eval(const float* __restrict_
 }
 
 // Deferred surfel colour (SURVEY 7 "SH only for winning surfels"): after pass
-// 1 each lane knows its winners; lanes of a warp that share a winner elect
-// one lane to evaluate its SH (all elected lanes evaluate in one SIMT pass)
-// and broadcast it.  Must be called by all 32 lanes.
+// 1 each lane knows the winners of its NS samples.  Distinct winners of the
+// whole warp are compacted into a task list in the warp's shared-memory slice
+// (a winner repeated in a lane's own samples or, per sample slot, in other
+// lanes is evaluated once), the list is evaluated 32 tasks per SIMT pass, and
+// every sample reads its colour back.  Must be called by all 32 lanes, with
+// the warp's slice of sm.st free.
 template <int NS>
-__device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, const unsigned long long* best,
-                                                      const uint32_t* bp, int lane, float3* col) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-        const bool cov = best[s] != ~0ull;
-        const unsigned peers = __match_any_sync(0xffffffffu, cov ? bp[s] : 0xffffffffu);
+__device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, TileSmem& sm, const unsigned long long* best,
+                                                      const uint32_t* bp, int lane, int warp, float3* col) {
+    const float3 bg = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+    if constexpr (NS == 1) {
+        const bool cov = best[0] != ~0ull;
+        const unsigned peers = __match_any_sync(0xffffffffu, cov ? bp[0] : 0xffffffffu);
         const int leader = __ffs(peers) - 1;
-        float3 c = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+        float3 c = bg;
         if (cov && lane == leader)
             c = surfel_color_eval(a.s_sh, a.s_pos, a.sh_deg, (float)a.cpos[0], (float)a.cpos[1], (float)a.cpos[2],
-                                  bp[s]);
+                                  bp[0]);
         c.x = __shfl_sync(0xffffffffu, c.x, leader);
         c.y = __shfl_sync(0xffffffffu, c.y, leader);
         c.z = __shfl_sync(0xffffffffu, c.z, leader);
-        col[s] = cov ? c : make_float3(a.bg[0], a.bg[1], a.bg[2]);
+        col[0] = cov ? c : bg;
+    } else {
+        static_assert(NS <= 4, "task slice holds 128 winners per warp");
+        int dup[NS], leader[NS];
+        uint32_t need = 0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const bool cov = best[s] != ~0ull;
+            const uint32_t v = cov ? bp[s] : 0xffffffffu;
+            dup[s] = -1;
+#pragma unroll
+            for (int q = s - 1; q >= 0; --q)
+                if (cov && bp[q] == v && best[q] != ~0ull) dup[s] = q;
+            leader[s] = __ffs(__match_any_sync(0xffffffffu, v)) - 1;
+            if (cov && dup[s] < 0 && lane == leader[s]) need |= 1u << s;
+        }
+        // exclusive prefix of the per-lane task counts
+        const int cnt = __popc(need);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t* tp = reinterpret_cast<uint32_t*>(&sm.st[0][warp * 32]);   // 128 task slots
+        float* tr = reinterpret_cast<float*>(&sm.st[1][warp * 32]);
+        float* tg = reinterpret_cast<float*>(&sm.st[2][warp * 32]);
+        float* tb = reinterpret_cast<float*>(&sm.st[3][warp * 32]);
+        int task[NS];
+        int k = incl - cnt;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            int own = -1;
+            if ((need >> s) & 1u) { own = k++; tp[own] = bp[s]; }
+            else if (dup[s] >= 0) own = task[dup[s]];
+            const int lead = __shfl_sync(0xffffffffu, own, leader[s]);
+            task[s] = best[s] == ~0ull ? -1 : (dup[s] >= 0 || ((need >> s) & 1u)) ? own : lead;
+        }
+        __syncwarp();
+        for (int i = lane; i < total; i += 32) {
+            const float3 c = surfel_color_eval(a.s_sh, a.s_pos, a.sh_deg, (float)a.cpos[0], (float)a.cpos[1],
+                                               (float)a.cpos[2], tp[i]);
+            tr[i] = c.x; tg[i] = c.y; tb[i] = c.z;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < NS; ++s) col[s] = task[s] >= 0 ? make_float3(tr[task[s]], tg[task[s]], tb[task[s]]) : bg;
     }
 }
 
@@ -534,7 +584,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileA
     for (int p = 0; p < NP; ++p) cs[p] = make_float3(a.bg[0], a.bg[1], a.bg[2]);
     if constexpr ((MODE & 1) != 0) {
         float3 col[NS];
-        resolve_surfel_colors<NS>(a, best, bp, lane, col);
+        resolve_surfel_colors<NS>(a, sm, best, bp, lane, warp, col);
         if constexpr (PX == 1) {   // box mean over the sub-samples (forward.py:201-203)
             float3 acc = make_float3(0.f, 0.f, 0.f);
 #pragma unroll
