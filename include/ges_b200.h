@@ -196,6 +196,66 @@ int ges_render_views_host(const ges_scene_t *scene, const ges_camera_t *host_cam
  * library was built with -DGES_STATS (tuning builds only; synchronous). */
 int ges_debug_stats(uint64_t *out16);
 
+/* ------------------------------------------------------------------ training
+ * Joint-stage training step of the reference (training.py:358-392 frozen
+ * surfel pass, :399-544 Gaussian passes, :547-788 backward): the forward is
+ * the deployment kernels above (ges_rasterize_surfels on the supersampled
+ * camera, ges_accumulate_gaussians at base resolution) plus the surfel view
+ * colours below; the backward pushes image cotangents to the Gaussian
+ * parameters (3D EWA and planar 2D) and, through the cached winner map, to
+ * the frozen surfels' SH coefficients and positions.
+ *
+ * Gradients are float64 device arrays in SOURCE order with the layout of the
+ * reference GradientSet (primitives.py:195-209), i.e. w.r.t. exposed values:
+ * position, opacity sigma (not its logit), the unit quaternion (tangent
+ * projected, training.py:890-893), scale (not its log) and SH. */
+typedef struct ges_gauss_grads {
+    double *pos;       /* n_gaussians x 3 */
+    double *opacity;   /* n_gaussians */
+    double *quat;      /* n_gaussians x 4 */
+    double *scale;     /* n_gaussians x gaussian_dim */
+    double *sh;        /* n_gaussians x K x 3 */
+    double *screen;    /* n_gaussians: NDC screen-gradient norm (training.py:896-911) */
+} ges_gauss_grads_t;
+
+/* View colour of every surfel, (n_surfels, 3) float32 in SOURCE order:
+ * _surfel_colors_with_tape (training.py:100-109) / surfel_view_colors
+ * (forward.py:99-103). */
+int ges_surfel_colors(const ges_scene_t *scene, const ges_camera_t *cam, float *rgb, void *stream);
+
+/* Scratch of ges_backward_gaussians: 16 float64 accumulators and two
+ * float4 ray coefficients per Gaussian. */
+size_t ges_backward_scratch_bytes(int64_t n_gaussians);
+
+/* Workspace of ges_backward_gaussians (its own tile binning at 16 px). */
+size_t ges_backward_workspace_bytes(const ges_scene_t *scene, const ges_camera_t *cam,
+                                    const ges_settings_t *st, int64_t gaussian_pair_cap);
+
+/* Gaussian half of training.backward (training.py:547-609 with
+ * _gaussian_backward_3d :646-719 / _gaussian_backward_2d :722-788), given the
+ * cotangents of the Gaussian buffers: g_color = dL/dC_G (H,W,3), g_weight =
+ * dL/dW_G (H,W) and, optional (NULL = zero), g_depth = dL/dD_G (H,W),
+ * g_normal = dL/dN_G (H,W,3), all float32.  surfel_depth (H,W) is the depth
+ * the forward's Gaussian pass was gated with.  `src` must hold the float64
+ * source arrays the scene was packed from (the chain rule runs in float64 on
+ * them).  any_filter: nonzero iff any filter3d entry is nonzero
+ * (primitives.py:113-126 switch the effective scale/opacity on globally). */
+int ges_backward_gaussians(const ges_scene_t *scene, const ges_scene_src_t *src, int32_t any_filter,
+                           const ges_camera_t *cam, const ges_settings_t *st, const float *surfel_depth,
+                           const float *g_color, const float *g_weight, const float *g_depth,
+                           const float *g_normal, const ges_gauss_grads_t *grads, void *scratch,
+                           size_t scratch_bytes, void *workspace, size_t ws_bytes,
+                           int64_t gaussian_pair_cap, ges_frame_status_t *status_dev, void *stream);
+
+/* Frozen-surfel half of training.backward (_surfel_backward_frozen,
+ * training.py:612-629): winner (H*grid, W*grid) int32 source ids (-1 =
+ * uncovered) of the cached opaque z-buffer, g_color = dL/dC_s (H,W,3)
+ * float32.  Writes g_sh (n_surfels x K x 3) and g_pos (n_surfels x 3)
+ * float64; col_scratch holds n_surfels x 3 float64. */
+int ges_backward_surfels_frozen(const ges_scene_src_t *src, const ges_camera_t *cam, int32_t grid,
+                                const int32_t *winner, const float *g_color, double *col_scratch,
+                                double *g_sh, double *g_pos, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

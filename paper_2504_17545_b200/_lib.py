@@ -22,7 +22,9 @@ LAYERS = {"full": 0, "surfels_only": 1, "gaussians_only": 2}
 EXPORTS = ("ges_abi_version", "ges_last_error", "ges_scene_bytes", "ges_scene_pack",
            "ges_workspace_bytes", "ges_render", "ges_render_profiled", "ges_rasterize_surfels",
            "ges_accumulate_gaussians", "ges_composite", "ges_smooth_geometry",
-           "ges_render_views_host", "ges_debug_stats")
+           "ges_render_views_host", "ges_debug_stats", "ges_surfel_colors",
+           "ges_backward_scratch_bytes", "ges_backward_workspace_bytes", "ges_backward_gaussians",
+           "ges_backward_surfels_frozen")
 
 
 class Camera(C.Structure):
@@ -62,6 +64,10 @@ class FrameStatus(C.Structure):
                 ("overflow", C.c_int32), ("pad", C.c_int32)]
 
 
+class GaussGrads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("pos", "opacity", "quat", "scale", "sh", "screen")]
+
+
 _lib = None
 
 
@@ -98,6 +104,14 @@ def lib():
                                             C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     }
     sig["ges_debug_stats"] = (C.c_int, [C.POINTER(C.c_uint64)])
+    sig["ges_surfel_colors"] = (C.c_int, [P(Scene), P(Camera), C.c_void_p, C.c_void_p])
+    sig["ges_backward_scratch_bytes"] = (C.c_size_t, [C.c_int64])
+    sig["ges_backward_workspace_bytes"] = (C.c_size_t, [P(Scene), P(Camera), P(Settings), C.c_int64])
+    sig["ges_backward_gaussians"] = (C.c_int, [P(Scene), P(SceneSrc), C.c_int32, P(Camera), P(Settings)]
+                                     + [C.c_void_p] * 5 + [P(GaussGrads), C.c_void_p, C.c_size_t,
+                                                           C.c_void_p, C.c_size_t, C.c_int64, C.c_void_p,
+                                                           C.c_void_p])
+    sig["ges_backward_surfels_frozen"] = (C.c_int, [P(SceneSrc), P(Camera), C.c_int32] + [C.c_void_p] * 6)
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
         fn.restype = res

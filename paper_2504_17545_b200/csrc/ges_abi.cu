@@ -220,6 +220,17 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     return GES_OK;
 }
 
+size_t backward_scratch_bytes(int64_t ng) { return al((size_t)ng * 16 * sizeof(double)) + al((size_t)ng * 32); }
+
+ges_settings_t backward_settings(const ges_settings_t* st, bool geom) {
+    ges_settings_t s2 = *st;
+    s2.supersample = 1;        // the Gaussian pass runs at base resolution (training.py:315-326)
+    s2.tile_mode = 1;          // 16 px tiles: the training forward's Gaussian pass uses them too
+    s2.layers = GES_LAYERS_FULL;
+    s2.with_geometry = geom;   // normals are only needed for a normal cotangent
+    return s2;
+}
+
 }  // namespace
 
 extern "C" {
@@ -312,6 +323,99 @@ int ges_smooth_geometry(const float* sd, const float* sn, const float* gd, const
         return fail(GES_EINVAL, "bad smooth_geometry arguments");
     cudaError_t e = launch_smooth(sd, sn, gd, gn, gw, d_out, n_out, n, (cudaStream_t)stream);
     return e == cudaSuccess ? GES_OK : cuda_fail(e, "smooth_geometry");
+}
+
+int ges_surfel_colors(const ges_scene_t* sc, const ges_camera_t* cam, float* rgb, void* stream) {
+    int rc;
+    if ((rc = check_scene(sc)) || (rc = check_cam(cam))) return rc;
+    if (sc->n_surfels && !rgb) return fail(GES_EINVAL, "rgb is NULL");
+    cudaError_t e = launch_surfel_colors(*sc, make_cam(*cam, 1), rgb, (cudaStream_t)stream);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "surfel colours");
+}
+
+size_t ges_backward_scratch_bytes(int64_t ng) { return ng < 0 ? 0 : backward_scratch_bytes(ng); }
+
+size_t ges_backward_workspace_bytes(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st,
+                                    int64_t cap_g) {
+    if (check_scene(sc) || check_cam(cam) || check_settings(st) || cap_g < 0) return 0;
+    const ges_settings_t s2 = backward_settings(st, true);
+    return layout(nullptr, sc, cam, &s2, 0, cap_g).bytes;
+}
+
+int ges_backward_gaussians(const ges_scene_t* sc, const ges_scene_src_t* src, int32_t any_filter,
+                           const ges_camera_t* cam, const ges_settings_t* st, const float* surfel_depth,
+                           const float* g_color, const float* g_weight, const float* g_depth, const float* g_normal,
+                           const ges_gauss_grads_t* grads, void* scratch, size_t scratch_bytes, void* ws,
+                           size_t ws_bytes, int64_t cap_g, ges_frame_status_t* status_dev, void* stream) {
+    int rc;
+    if ((rc = check_scene(sc)) || (rc = check_cam(cam)) || (rc = check_settings(st))) return rc;
+    if (!src || !grads) return fail(GES_EINVAL, "NULL argument");
+    if (src->n_gaussians != sc->n_gaussians || src->gaussian_dim != sc->gaussian_dim ||
+        src->sh_degree != sc->sh_degree)
+        return fail(GES_EINVAL, "source arrays do not match the packed scene");
+    const int64_t ng = sc->n_gaussians;
+    if (ng == 0) return GES_OK;
+    if (!surfel_depth || !g_color || !g_weight) return fail(GES_EINVAL, "surfel_depth/g_color/g_weight is NULL");
+    if (!src->g_pos || !src->g_quat || !src->g_log_scale || !src->g_raw_opacity || !src->g_sh)
+        return fail(GES_EINVAL, "source Gaussian arrays are NULL");
+    if (!grads->pos || !grads->opacity || !grads->quat || !grads->scale || !grads->sh)
+        return fail(GES_EINVAL, "gradient outputs are NULL");
+    if (cap_g < 0 || cap_g >= (1ll << 32)) return fail(GES_EINVAL, "pair capacity out of range");
+    if (!scratch || scratch_bytes < backward_scratch_bytes(ng)) return fail(GES_EWORKSPACE, "scratch too small");
+    // a normal cotangent reaches 3D Gaussians only when the frame has their
+    // normals (training.py:661-664); planar ones always carry n_vis (:736-743)
+    const bool geom = g_normal && (sc->gaussian_dim == 2 || st->with_geometry);
+    const ges_settings_t s2 = backward_settings(st, geom);
+    Frame f = layout(ws, sc, cam, &s2, 0, cap_g);
+    if (!ws || ws_bytes < f.bytes) return fail(GES_EWORKSPACE, "workspace too small (see ges_backward_workspace_bytes)");
+    cudaStream_t s = (cudaStream_t)stream;
+    ges_frame_status_t* status = status_dev ? status_dev : f.status;
+    double* acc = static_cast<double*>(scratch);
+    float4* aux = reinterpret_cast<float4*>(static_cast<char*>(scratch) + al((size_t)ng * 16 * sizeof(double)));
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(f.cnt_s, 0, f.zero_bytes, s)) != cudaSuccess) return cuda_fail(e, "memset counts");
+    if ((e = cudaMemsetAsync(status, 0, sizeof(ges_frame_status_t), s)) != cudaSuccess)
+        return cuda_fail(e, "memset status");
+    if ((e = cudaMemsetAsync(acc, 0, (size_t)ng * 16 * sizeof(double), s)) != cudaSuccess)
+        return cuda_fail(e, "memset accumulators");
+    const CamK cg = make_cam(*cam, 1);
+    const SlabMap slabs = slab_map(*sc, cg);
+    Grid gg{cg.W, cg.H, TILE, f.ntx, f.nty, slabs};
+    ges_scene_t scs = *sc;
+    scs.n_surfels = 0;
+    const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, 0, f.ntiles, f.ntx, TILE, 4};
+    const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE, 4};
+    PrepOut po{f.grec, nullptr, f.g_nrm, f.cnt_g, sc->gaussian_dim == 2 ? aux : nullptr};
+    if ((e = launch_gauss_prep(scs, cg, gg, s2, po, s))) return cuda_fail(e, "gaussian preprocess");
+    if ((e = launch_scan(bs, bg, status, s))) return cuda_fail(e, "tile scan");
+    if ((e = launch_fill(f.srec, 0, bs, f.grec, ng, sc->gaussian_dim, bg, slabs, s))) return cuda_fail(e, "tile fill");
+    BwdArgs a{};
+    a.W = cam->width; a.H = cam->height; a.ntx = f.ntx; a.nty = f.nty;
+    a.grec = f.grec; a.aux = aux; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg; a.slabs = slabs;
+    a.ds = surfel_depth; a.g_cg = g_color; a.g_wg = g_weight; a.g_gd = g_depth; a.g_gn = geom ? g_normal : nullptr;
+    a.gcx = (float)cg.cx; a.gcy = (float)cg.cy; a.gifx = (float)(1.0 / cg.fx); a.gify = (float)(1.0 / cg.fy);
+    a.acc = acc;
+    a.status = status;
+    if ((e = launch_gauss_bwd(a, sc->gaussian_dim, geom, s))) return cuda_fail(e, "gaussian backward");
+    if ((e = launch_gauss_finish(*src, any_filter, st->mip, cg, acc, *grads, s)))
+        return cuda_fail(e, "gaussian backward finish");
+    return GES_OK;
+}
+
+int ges_backward_surfels_frozen(const ges_scene_src_t* src, const ges_camera_t* cam, int32_t grid,
+                                const int32_t* winner, const float* g_color, double* col, double* g_sh,
+                                double* g_pos, void* stream) {
+    int rc;
+    if ((rc = check_cam(cam))) return rc;
+    if (!src) return fail(GES_EINVAL, "src is NULL");
+    if (grid != 1 && grid != 2) return fail(GES_EINVAL, "grid must be 1 or 2");
+    if (src->sh_degree < 0 || src->sh_degree > 3) return fail(GES_EDEGREE, "SH degree must be in [0, 3]");
+    if (src->n_surfels == 0) return GES_OK;
+    if (!winner || !g_color || !col || !g_sh || !g_pos || !src->s_pos || !src->s_sh)
+        return fail(GES_EINVAL, "NULL argument");
+    cudaError_t e = launch_frozen_bwd(*src, make_cam(*cam, 1), cam->width, cam->height, grid, winner, g_color, col,
+                                      g_sh, g_pos, (cudaStream_t)stream);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "frozen surfel backward");
 }
 
 int ges_debug_stats(uint64_t* out16) {

@@ -12,6 +12,8 @@ struct PrepOut {
     float4* rgb;            // per-primitive view colour (surfels; Gaussians 3D keep it in rec)
     float4* nrm;            // per-primitive camera-facing normal (surfels; Gaussians if geometry)
     uint32_t* bin_count;    // per-(tile, slab) pair counters (zeroed by the caller)
+    float4* aux;            // 2D Gaussians, training backward only: (a1/s1).d and (a2/s2).d
+                            // as affine functions of the pixel (2 per Gaussian), or NULL
 };
 
 // Tile grid for the pass: ntx x nty tiles of `tile_px` pixels at resolution W x H.
@@ -69,5 +71,28 @@ cudaError_t launch_composite(const float* sc, const float* gc, const float* gw, 
                              int64_t n, cudaStream_t s);
 cudaError_t launch_smooth(const float* sd, const float* sn, const float* gd, const float* gn,
                           const float* gw, float* d_out, float* n_out, int64_t n, cudaStream_t s);
+
+// ---------------------------------------------------------------- training (ges_train.cu)
+struct BwdArgs {
+    int W, H, ntx, nty;           // base resolution, 16x16 tiles
+    const void* grec;
+    const float4* aux;            // 2D: (k1, k2) affine coefficients per Gaussian
+    const float4* g_nrm;          // normal cotangent given: camera-facing normals
+    const uint32_t* g_list;
+    BinPass gbin;
+    SlabMap slabs;
+    const float *ds, *g_cg, *g_wg, *g_gd, *g_gn;   // gd, gn may be NULL
+    float gcx, gcy, gifx, gify;
+    double* acc;                  // 16 float64 partial sums per packed Gaussian
+    const ges_frame_status_t* status;
+};
+
+cudaError_t launch_surfel_colors(const ges_scene_t& sc, const CamK& cam, float* rgb, cudaStream_t s);
+cudaError_t launch_gauss_bwd(const BwdArgs& a, int g_kind, bool geom, cudaStream_t s);
+cudaError_t launch_gauss_finish(const ges_scene_src_t& src, int any_filter, int mip, const CamK& cam,
+                                const double* acc, const ges_gauss_grads_t& out, cudaStream_t s);
+cudaError_t launch_frozen_bwd(const ges_scene_src_t& src, const CamK& cam, int W, int H, int grid,
+                              const int32_t* winner, const float* g_cs, double* col, double* g_sh, double* g_pos,
+                              cudaStream_t s);
 
 }  // namespace ges

@@ -393,6 +393,11 @@ __global__ void __launch_bounds__(256, 4) k_gauss2_prep(ges_scene_t sc, CamK cam
                                    (float)(dv.y * inv), (float)(dv.z * inv));
         rec.r3 = make_float4((float)sig, (float)m2max * 1.0001f + 1e-4f, 0.f, 0.f);
         rec.r4 = make_float4(col.x, col.y, col.z, 0.f);
+        if (o.aux) {   // k1 = a1.d/s1, k2 = a2.d/s2 of ray_splat_backward (geometry.py:229-252)
+            const int xr = (int)rec.r1.w, yr = (int)rec.r2.w;
+            o.aux[2 * i] = affine_of(scl(a1, 1.0 / s1), cam, xr, yr, 0.f);
+            o.aux[2 * i + 1] = affine_of(scl(a2, 1.0 / s2), cam, xr, yr, 0.f);
+        }
         if (cfg.geom) {
             double sgn = dot(n, q) < 0.0 ? 1.0 : -1.0;   // forward.py:337
             o.nrm[i] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);

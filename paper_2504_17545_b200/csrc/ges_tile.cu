@@ -220,13 +220,17 @@ __device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, TileSme
     }
 }
 
+#ifndef GES_TILE_MINB2
+#define GES_TILE_MINB2 4   // resident CTAs per SM for the 4-sample variants (64 registers)
+#endif
+
 // SS: supersampling of the surfel pass (1, or 2 = the 2x2 grid of ss=4);
 // PX: base pixels per thread per axis (1: 16x16-pixel tiles; 2: 32x32-pixel
 // tiles, each thread a 2x2 pixel block, so every staged surfel and every
 // list step is shared by 4 pixels).  A thread owns G x G = (SS*PX)^2 samples
 // in pass 1 and PX x PX pixels in pass 2.
 template <int SS, int PX, int MODE, int GK, bool GEOM>
-__global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? 4 : 6) k_tile(TileArgs a) {
+__global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6) k_tile(TileArgs a) {
     constexpr int G = SS * PX, NS = G * G, NP = PX * PX, TP = TILE * PX;
     __shared__ TileSmem sm;
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders

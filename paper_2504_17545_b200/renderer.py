@@ -103,10 +103,12 @@ class DeviceScene:
     """A scene packed once into float32 SoA on the device (kernel K0).
 
     Built from any object with the reference's ``Scene`` fields; the source
-    float64 arrays are uploaded, packed by ``ges_scene_pack`` and dropped.
+    float64 arrays are uploaded, packed by ``ges_scene_pack`` and dropped --
+    unless ``keep_source`` (the training backward runs its float64 chain rule
+    on them: ``self.src`` then holds their device pointers).
     """
 
-    def __init__(self, scene, device=None, *, spatial_order: bool = True):
+    def __init__(self, scene, device=None, *, spatial_order: bool = True, keep_source: bool = False):
         self.device = torch.device(device or "cuda")
         s, g = scene.surfels, scene.gaussians
         ns, ng = int(np.asarray(s.pos).shape[0]), int(np.asarray(g.pos).shape[0])
@@ -158,9 +160,14 @@ class DeviceScene:
         stream = torch.cuda.current_stream(dev).cuda_stream
         _lib.check(L.ges_scene_pack(C.byref(src), C.c_void_p(self.blob.data_ptr()), nbytes,
                                     C.byref(self.c), C.c_void_p(stream)), "ges_scene_pack")
-        self._src = keep   # freed by the caching allocator in stream order
-        torch.cuda.current_stream(dev).synchronize()
-        self._src = None
+        self.any_filter = bool(ng and np.any(np.asarray(getattr(g, "filter3d", None) if
+                                                        getattr(g, "filter3d", None) is not None else 0.0)))
+        if keep_source:
+            self.src, self._src = src, keep
+        else:
+            self._src = keep   # freed by the caching allocator in stream order
+            torch.cuda.current_stream(dev).synchronize()
+            self._src, self.src = None, None
 
     @property
     def nbytes(self) -> int:

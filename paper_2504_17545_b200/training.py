@@ -1,0 +1,295 @@
+"""Drop-in for the reference training renderer's joint stage
+(``ges.training``, /root/reference/pkg/src/ges/training.py).
+
+The joint stage of the reference trainer (optim.py:715-735) renders every
+iteration with frozen, fully opaque surfels (``frozen_cache`` set, all
+``w == 255``) and trainable Gaussians, then calls :func:`backward`.  This
+module runs that step on the GPU:
+
+* forward -- the deployment kernels: the cached opaque z-buffer of the
+  supersampled camera (``ges_rasterize_surfels``, training.py:358-392), the
+  surfel view colours (``ges_surfel_colors``) and the Gaussian pass
+  (``ges_accumulate_gaussians`` on 16 px tiles, training.py:399-544);
+* backward -- ``ges_backward_gaussians`` (training.py:646-788: a per-tile
+  replay of the Gaussian pass with warp-reduced float64 partial sums, then a
+  per-Gaussian float64 chain rule) and ``ges_backward_surfels_frozen``
+  (training.py:612-629).
+
+Same names and arguments as the reference (``TrainSettings``,
+``TrainFrame``, ``render_training``, ``backward``, ``GradientSet``).
+Deliberate differences, documented in DESIGN.md:
+
+* the translucent surfel pass of the surfel stage (training.py:145-292,
+  ``w < 255`` or no ``frozen_cache``) is not on the GPU path and raises
+  ``NotImplementedError``; surfels may also be disabled
+  (``surfels_enabled=False``);
+* per-pixel arithmetic is float32 (``settings.dtype`` only sets the dtype of
+  the returned NumPy arrays); gradients are float64;
+* the frame carries no per-fragment tape; ``frame.tape`` holds the device
+  state :func:`backward` needs.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from types import SimpleNamespace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .renderer import DeviceScene, camera_struct, default_renderer, settings_struct
+from .types import GaussianKind, GradientSet
+
+W_ADJUST_THRESHOLD = 30.0
+W_OPAQUE = 255.0
+
+
+@dataclass
+class TrainSettings:
+    """Training-path knobs (training.py:36-63); ``None`` = from the schedule state."""
+    supersample: int | None = None
+    adjust_order: bool | None = None
+    background: tuple = (0.0, 0.0, 0.0)
+    epsilon_mode: str = "adaptive"
+    epsilon_value: float = 0.0
+    mip: bool = False
+    with_geometry: bool = False
+    gaussians_enabled: bool = True
+    surfels_enabled: bool = True
+    dtype: type = np.float64
+    frozen_cache: dict | None = None
+    gaussian_only_norm: bool = False
+
+    def resolve(self, scene):
+        w = np.asarray(scene.surfels.w)
+        wmin = w.min() if w.size else np.inf
+        late = wmin >= W_ADJUST_THRESHOLD
+        ss = self.supersample if self.supersample is not None else (4 if late else 1)
+        adj = self.adjust_order if self.adjust_order is not None else late
+        return ss, adj, late
+
+
+@dataclass
+class TrainFrame:
+    """Forward buffers plus the device state :func:`backward` needs (training.py:66-78)."""
+    image: object
+    surfel_color: object
+    surfel_depth: object
+    gauss_color: object
+    gauss_weight: object
+    blend_depth: object = None
+    blend_normal: object = None
+    gauss_depth: object = None
+    gauss_normal: object = None
+    tape: dict = field(default_factory=dict)
+
+
+def _count(a) -> int:
+    return int(np.asarray(a).shape[0])
+
+
+def _pass_settings(st: TrainSettings, **kw):
+    ns = SimpleNamespace(supersample=1, layers="full", mip=st.mip, epsilon_mode=st.epsilon_mode,
+                         epsilon_value=st.epsilon_value, with_geometry=st.with_geometry,
+                         background=tuple(st.background), tile_mode=1)
+    for k, v in kw.items():
+        setattr(ns, k, v)
+    return ns
+
+
+def _out(t, to_numpy, dtype):
+    if t is None or not to_numpy:
+        return t
+    return t.detach().cpu().numpy().astype(dtype, copy=False)
+
+
+def _as_dev(a, dev, dtype=torch.float32):
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=dev).contiguous()
+
+
+def _frozen_entry(ds, scene, rc, settings, cache_key, dev):
+    """Cached opaque z-buffer of the (supersampled) camera (training.py:367-381)."""
+    cache = settings.frozen_cache
+    entry = cache.get(cache_key) if cache_key is not None else None
+    if entry is not None and not entry.get("_gpu"):   # written by the reference: adopt it
+        entry = {"winner": _as_dev(np.asarray(entry["winner"]).reshape(-1), dev, torch.int32),
+                 "depth": _as_dev(np.asarray(entry["depth"]).reshape(-1), dev),
+                 "normal": _as_dev(np.asarray(entry["normal"]).reshape(-1, 3), dev), "_gpu": True}
+    if entry is None:
+        fr = default_renderer(dev).render(ds, rc, _pass_settings(settings, with_geometry=False), mode=1,
+                                          want=("s_depth", "s_normal", "s_winner"))
+        entry = {"winner": fr.s_winner.reshape(-1), "depth": fr.s_depth.reshape(-1),
+                 "normal": fr.s_normal.reshape(-1, 3), "_gpu": True}
+        if cache_key is not None:
+            cache[cache_key] = entry
+    return entry
+
+
+def render_training(scene, cam, settings: TrainSettings | None = None, cache_key=None, *,
+                    to_numpy: bool = True, device=None) -> TrainFrame:
+    """training.py:295-355 for the joint stage (frozen surfels or none) on the GPU."""
+    settings = settings or TrainSettings()
+    dev = torch.device(device or "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    ns, ng = _count(scene.surfels.pos), _count(scene.gaussians.pos)
+    ss, _adjust, late = settings.resolve(scene)
+    grid = 2 if ss == 4 else 1
+    H, W = int(cam.height), int(cam.width)
+    bg = torch.tensor([float(v) for v in settings.background], dtype=torch.float32, device=dev)
+    use_surfels = settings.surfels_enabled and ns > 0
+    fast = (use_surfels and settings.frozen_cache is not None
+            and bool(np.all(np.asarray(scene.surfels.w) == W_OPAQUE)))
+    if use_surfels and not fast:
+        raise NotImplementedError(
+            "the translucent surfel pass (training.py:145-292) is not on the GPU path: the GPU training "
+            "step needs frozen surfels (w == 255 and settings.frozen_cache) or surfels_enabled=False")
+    ds = DeviceScene(scene, dev, keep_source=True)
+    L = _lib.lib()
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    geom = bool(settings.with_geometry)
+    blend_depth = blend_normal = None
+    winner = None
+    if fast:
+        rc = cam.scaled(grid) if grid > 1 else cam
+        entry = _frozen_entry(ds, scene, rc, settings, cache_key, dev)
+        winner = entry["winner"]
+        colors = torch.empty((ns, 3), dtype=torch.float32, device=dev)
+        _lib.check(L.ges_surfel_colors(C.byref(ds.c), C.byref(camera_struct(cam)), C.c_void_p(colors.data_ptr()),
+                                       stream), "surfel colours")
+        covered = winner >= 0
+        chi = bg.expand(H * grid * W * grid, 3).clone()
+        chi[covered] = colors[winner[covered].long()]
+        surfel_color = chi.view(H, grid, W, grid, 3).mean(dim=(1, 3))
+        # late phase (all w = 255 >= 30): the Gaussian gate uses the front hit depth
+        surfel_depth = entry["depth"].view(H * grid, W * grid)[::grid, ::grid].contiguous()
+        if geom:
+            zero = torch.zeros((), dtype=torch.float32, device=dev)
+            bd = torch.where(covered, entry["depth"], zero)
+            bn = torch.where(covered[:, None], entry["normal"], zero)
+            blend_depth = bd.view(H, grid, W, grid).mean(dim=(1, 3))
+            blend_normal = bn.view(H, grid, W, grid, 3).mean(dim=(1, 3))
+    else:
+        surfel_color = bg.expand(H, W, 3).clone()
+        surfel_depth = torch.full((H, W), float("inf"), dtype=torch.float32, device=dev)
+        if geom and use_surfels:
+            blend_depth = torch.zeros((H, W), dtype=torch.float32, device=dev)
+            blend_normal = torch.zeros((H, W, 3), dtype=torch.float32, device=dev)
+    gaussians = settings.gaussians_enabled and ng > 0
+    gd = gn = None
+    if gaussians:
+        fr = default_renderer(dev).render(ds, cam, _pass_settings(settings), mode=2, surfel_depth=surfel_depth,
+                                          want=("g_color", "g_weight", "g_depth", "g_normal"))
+        gc, gw = fr.g_color, fr.g_weight
+        if geom:
+            gd, gn = fr.g_depth, fr.g_normal
+    else:
+        gc = torch.zeros((H, W, 3), dtype=torch.float32, device=dev)
+        gw = torch.zeros((H, W), dtype=torch.float32, device=dev)
+        if geom:
+            gd = torch.zeros((H, W), dtype=torch.float32, device=dev)
+            gn = torch.zeros((H, W, 3), dtype=torch.float32, device=dev)
+    gaussian_only = settings.gaussian_only_norm and not use_surfels
+    if gaussian_only:   # training.py:329-332
+        image = torch.where(gw[..., None] > 0, gc / gw.clamp_min(1e-12)[..., None], bg)
+    else:
+        image = (surfel_color + gc) / (1.0 + gw)[..., None]
+    dt = settings.dtype
+    frame = TrainFrame(image=_out(image, to_numpy, dt), surfel_color=_out(surfel_color, to_numpy, dt),
+                       surfel_depth=_out(surfel_depth, to_numpy, dt), gauss_color=_out(gc, to_numpy, dt),
+                       gauss_weight=_out(gw, to_numpy, dt), blend_depth=_out(blend_depth, to_numpy, dt),
+                       blend_normal=_out(blend_normal, to_numpy, dt), gauss_depth=_out(gd, to_numpy, dt),
+                       gauss_normal=_out(gn, to_numpy, dt))
+    frame.tape = {"scene": scene, "cam": cam, "settings": settings, "grid": grid, "late": late,
+                  "device_scene": ds, "device": dev, "image": image, "gauss_weight": gw,
+                  "surfel_depth": surfel_depth, "winner": winner, "use_surfels": use_surfels,
+                  "frozen": fast, "gaussians": gaussians, "gaussian_only": gaussian_only}
+    return frame
+
+
+def backward(frame: TrainFrame, g_image, *, g_blend_depth=None, g_blend_normal=None,
+             g_gauss_depth=None, g_gauss_normal=None, g_gauss_weight=None) -> GradientSet:
+    """training.py:547-609 on the GPU.  ``g_image`` is dL/dC (H, W, 3); the
+    optional cotangents feed the geometry buffers.  Returns float64 NumPy
+    gradients w.r.t. exposed parameter values."""
+    tape = frame.tape
+    if not tape:
+        raise ValueError("frame carries no tape; re-render with render_training")
+    scene, cam, settings = tape["scene"], tape["cam"], tape["settings"]
+    dev, ds = tape["device"], tape["device_scene"]
+    H, W = int(cam.height), int(cam.width)
+    g_img = _as_dev(g_image, dev)
+    image, gw = tape["image"], tape["gauss_weight"]
+    if tape["gaussian_only"]:
+        wsafe = gw.clamp_min(1e-12)
+        cov = gw > 0
+        g_cg = torch.where(cov[..., None], g_img / wsafe[..., None], torch.zeros((), device=dev))
+        g_wg = torch.where(cov, -(g_img * image).sum(-1) / wsafe, torch.zeros((), device=dev))
+        g_cs = torch.zeros_like(g_img)
+    else:
+        denom = 1.0 + gw
+        g_cs = g_img / denom[..., None]
+        g_cg = g_cs
+        g_wg = -(g_img * image).sum(-1) / denom
+    if g_gauss_weight is not None:
+        g_wg = g_wg + _as_dev(g_gauss_weight, dev)
+    g_cg, g_wg = g_cg.contiguous(), g_wg.contiguous()
+
+    ns, ng = _count(scene.surfels.pos), _count(scene.gaussians.pos)
+    K = (ds.sh_degree + 1) ** 2
+    dim = ds.dim if ng else (3 if getattr(scene.gaussians, "kind", GaussianKind.THREE_D) is GaussianKind.THREE_D
+                            else 2)
+    f64 = dict(dtype=torch.float64, device=dev)
+    out = {k: torch.zeros(shape, **f64) for k, shape in (
+        ("surfel_pos", (ns, 3)), ("surfel_quat", (ns, 4)), ("surfel_scale", (ns, 2)),
+        ("surfel_sh", (ns, K, 3)), ("surfel_w", (ns,)), ("gaussian_pos", (ng, 3)),
+        ("gaussian_opacity", (ng,)), ("gaussian_quat", (ng, 4)), ("gaussian_scale", (ng, dim)),
+        ("gaussian_sh", (ng, K, 3)), ("surfel_screen_grad", (ns,)), ("gaussian_screen_grad", (ng,)))}
+    L = _lib.lib()
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    cam_c = camera_struct(cam)
+    if tape["gaussians"]:
+        gg = _lib.GaussGrads()
+        gg.pos, gg.opacity = out["gaussian_pos"].data_ptr(), out["gaussian_opacity"].data_ptr()
+        gg.quat, gg.scale = out["gaussian_quat"].data_ptr(), out["gaussian_scale"].data_ptr()
+        gg.sh, gg.screen = out["gaussian_sh"].data_ptr(), out["gaussian_screen_grad"].data_ptr()
+        st_c = settings_struct(_pass_settings(settings))
+        g_gd = _as_dev(g_gauss_depth, dev)
+        g_gn = _as_dev(g_gauss_normal, dev)
+        scratch = torch.empty(L.ges_backward_scratch_bytes(ng), dtype=torch.uint8, device=dev)
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        cap = max(1 << 20, 8 * ng)
+        status = torch.zeros(3, dtype=torch.int64, device=dev)
+        for _ in range(3):
+            nbytes = L.ges_backward_workspace_bytes(C.byref(ds.c), C.byref(cam_c), C.byref(st_c), cap)
+            if nbytes == 0:
+                _lib.check(_lib.GES_EINVAL, "ges_backward_workspace_bytes")
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            rc = L.ges_backward_gaussians(C.byref(ds.c), C.byref(ds.src), int(ds.any_filter), C.byref(cam_c),
+                                          C.byref(st_c), ptr(tape["surfel_depth"]), ptr(g_cg), ptr(g_wg),
+                                          ptr(g_gd), ptr(g_gn), C.byref(gg), ptr(scratch), scratch.numel(),
+                                          ptr(ws), nbytes, cap, ptr(status), stream)
+            _lib.check(rc, "gaussian backward")
+            st = status.cpu()
+            if not int(st[2] & 0xFFFFFFFF):
+                break
+            cap = max(cap, int(int(st[1]) * 1.25) + 1024)
+        else:
+            raise RuntimeError("tile pair lists overflowed repeatedly")
+    if tape["frozen"] and bool((tape["winner"] >= 0).any()):
+        col = torch.empty((ns, 3), **f64)
+        _lib.check(L.ges_backward_surfels_frozen(C.byref(ds.src), C.byref(cam_c), int(tape["grid"]),
+                                                 C.c_void_p(tape["winner"].data_ptr()),
+                                                 C.c_void_p(g_cs.contiguous().data_ptr()),
+                                                 C.c_void_p(col.data_ptr()),
+                                                 C.c_void_p(out["surfel_sh"].data_ptr()),
+                                                 C.c_void_p(out["surfel_pos"].data_ptr()), stream),
+                   "frozen surfel backward")
+    host = {k: v.cpu().numpy() for k, v in out.items()}
+    return GradientSet(**host)

@@ -12,6 +12,7 @@ follow the reference:
 * ``GaussianSet``   -- ``ges/primitives.py:82-161`` (pos, raw_opacity logit,
                        quat, log_scale (N,3|2), sh, kind, filter3d)
 * ``Scene``         -- ``ges/primitives.py:166-191``
+* ``GradientSet``   -- ``ges/primitives.py:194-214``
 """
 
 from __future__ import annotations
@@ -185,3 +186,25 @@ class Scene:
     gaussians: GaussianSet
     sh_degree: int
     stage: Stage = Stage.FROZEN
+
+
+@dataclass
+class GradientSet:
+    """Gradients w.r.t. exposed parameter values (primitives.py:194-214)."""
+    surfel_pos: np.ndarray
+    surfel_quat: np.ndarray
+    surfel_scale: np.ndarray
+    surfel_sh: np.ndarray
+    surfel_w: np.ndarray
+    gaussian_pos: np.ndarray
+    gaussian_opacity: np.ndarray
+    gaussian_quat: np.ndarray
+    gaussian_scale: np.ndarray
+    gaussian_sh: np.ndarray
+    surfel_screen_grad: np.ndarray = None
+    gaussian_screen_grad: np.ndarray = None
+
+    def check_finite(self):
+        for name, arr in self.__dict__.items():
+            if arr is not None and arr.size and not np.all(np.isfinite(arr)):
+                raise FloatingPointError(f"non-finite gradient in {name}")

@@ -19,7 +19,41 @@ GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 def names():
     """Render golden cases (the .ges fixtures have their own *_load.npz)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
-                  if not os.path.basename(p).startswith("ges_"))
+                  if not os.path.basename(p).startswith(("ges_", "train_")))
+
+
+def train_names():
+    """Training-step cases written by ``tests/golden/make_train_golden.py``."""
+    return sorted(os.path.basename(p)[6:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "train_*.npz")))
+
+
+TRAIN_GRADS = ("surfel_pos", "surfel_quat", "surfel_scale", "surfel_sh", "surfel_w", "gaussian_pos",
+               "gaussian_opacity", "gaussian_quat", "gaussian_scale", "gaussian_sh", "surfel_screen_grad",
+               "gaussian_screen_grad")
+
+
+def train_settings(d, settings_cls=None):
+    """TrainSettings of a case (the package's own class unless given)."""
+    if settings_cls is None:
+        from paper_2504_17545_b200.training import TrainSettings as settings_cls
+    kw = {k: (tuple(v) if isinstance(v, list) else v) for k, v in d.items()}
+    return settings_cls(frozen_cache={}, **kw)
+
+
+def load_train(name):
+    z = np.load(os.path.join(GOLDEN_DIR, f"train_{name}.npz"))
+    cam = Camera(float(z["fx"]), float(z["fy"]), float(z["cx"]), float(z["cy"]),
+                 int(z["width"]), int(z["height"]), z["w2c"])
+    kind = GaussianKind.TWO_D if str(z["kind"]) == "2d" else GaussianKind.THREE_D
+    scene = Scene(SurfelSet(z["sp"], z["sq"], z["sl"], z["ssh"], z["sw"]),
+                  GaussianSet(z["gp"], z["go"], z["gq"], z["gl"], z["gsh"], kind, z["gf"]),
+                  int(z["sh_degree"]), Stage.FROZEN)
+    st = json.loads(str(z["settings"]))
+    cot = {k: z[k] for k in ("g_gauss_depth", "g_gauss_normal", "g_gauss_weight") if k in z.files}
+    fwd = {k: z[k] for k in ("image", "surfel_color", "surfel_depth", "gauss_color", "gauss_weight",
+                             "blend_depth", "blend_normal", "gauss_depth", "gauss_normal") if k in z.files}
+    grads = {k: z["grad_" + k] for k in TRAIN_GRADS}
+    return scene, cam, st, z["g_image"], cot, fwd, grads
 
 
 def settings_ns(d, dtype=np.float64):
