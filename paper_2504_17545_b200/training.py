@@ -132,8 +132,12 @@ def _frozen_entry(ds, scene, rc, settings, cache_key, dev):
 
 
 def render_training(scene, cam, settings: TrainSettings | None = None, cache_key=None, *,
-                    to_numpy: bool = True, device=None) -> TrainFrame:
-    """training.py:295-355 for the joint stage (frozen surfels or none) on the GPU."""
+                    to_numpy: bool = True, device=None, device_scene: DeviceScene | None = None) -> TrainFrame:
+    """training.py:295-355 for the joint stage (frozen surfels or none) on the GPU.
+
+    ``device_scene``: a ``DeviceScene(scene, keep_source=True)`` packed from
+    the CURRENT parameter values, to skip the per-call upload and pack (the
+    caller re-packs after every parameter update)."""
     settings = settings or TrainSettings()
     dev = torch.device(device or "cuda")
     if dev.index is None:
@@ -150,7 +154,12 @@ def render_training(scene, cam, settings: TrainSettings | None = None, cache_key
         raise NotImplementedError(
             "the translucent surfel pass (training.py:145-292) is not on the GPU path: the GPU training "
             "step needs frozen surfels (w == 255 and settings.frozen_cache) or surfels_enabled=False")
-    ds = DeviceScene(scene, dev, keep_source=True)
+    if device_scene is not None:
+        if device_scene.src is None:
+            raise ValueError("device_scene must be built with keep_source=True")
+        ds = device_scene
+    else:
+        ds = DeviceScene(scene, dev, keep_source=True)
     L = _lib.lib()
     stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
     geom = bool(settings.with_geometry)
@@ -214,10 +223,13 @@ def render_training(scene, cam, settings: TrainSettings | None = None, cache_key
 
 
 def backward(frame: TrainFrame, g_image, *, g_blend_depth=None, g_blend_normal=None,
-             g_gauss_depth=None, g_gauss_normal=None, g_gauss_weight=None) -> GradientSet:
+             g_gauss_depth=None, g_gauss_normal=None, g_gauss_weight=None, to_numpy: bool = True) -> GradientSet:
     """training.py:547-609 on the GPU.  ``g_image`` is dL/dC (H, W, 3); the
-    optional cotangents feed the geometry buffers.  Returns float64 NumPy
-    gradients w.r.t. exposed parameter values."""
+    optional cotangents feed the geometry buffers.  Returns float64 gradients
+    w.r.t. exposed parameter values (NumPy, or torch CUDA tensors with
+    ``to_numpy=False``).  ``g_blend_*`` are accepted like the reference's and,
+    as in its frozen-surfel path (training.py:612-629), do not reach any
+    parameter."""
     tape = frame.tape
     if not tape:
         raise ValueError("frame carries no tape; re-render with render_training")
@@ -291,5 +303,6 @@ def backward(frame: TrainFrame, g_image, *, g_blend_depth=None, g_blend_normal=N
                                                  C.c_void_p(out["surfel_sh"].data_ptr()),
                                                  C.c_void_p(out["surfel_pos"].data_ptr()), stream),
                    "frozen surfel backward")
-    host = {k: v.cpu().numpy() for k, v in out.items()}
-    return GradientSet(**host)
+    if not to_numpy:
+        return GradientSet(**out)
+    return GradientSet(**{k: v.cpu().numpy() for k, v in out.items()})
