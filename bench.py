@@ -36,12 +36,12 @@ def parse():
     p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     p.add_argument("--views", type=int, default=None, help="views per rank per step")
     p.add_argument("--ss", type=int, default=1, choices=[1, 4])
-    p.add_argument("--streams", type=int, default=4, help="CUDA streams pipelining the views of a step")
+    p.add_argument("--streams", type=int, default=8, help="CUDA streams pipelining the views of a step")
     p.add_argument("--layers", default="full", choices=["full", "surfels_only", "gaussians_only"])
     p.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    p.add_argument("--cpu-tiles", type=int, default=64, help="tiles in the CPU sample")
+    p.add_argument("--cpu-tiles", type=int, default=512, help="tiles in the CPU sample (about 10 s of CPU work)")
     p.add_argument("--profile-only", action="store_true", help="render a few frames, no JSON (for ncu)")
     return p.parse_args()
 
@@ -64,7 +64,7 @@ WORKLOADS = {
     4: "config4 (Mip): 1M surfels + 300k filtered Gaussians, SH3, 3840x2160, mip=True",
     5: "config5: 3M surfels + 1M Gaussians, SH3, 3840x2160 orbit views",
 }
-DEFAULT_VIEWS = {1: 32, 2: 8, 3: 8, 4: 4, 5: 8}
+DEFAULT_VIEWS = {1: 32, 2: 32, 3: 32, 4: 4, 5: 8}
 
 
 def views_for(cfg, rank, world, per_rank):
