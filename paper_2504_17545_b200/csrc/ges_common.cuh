@@ -59,8 +59,24 @@ struct __align__(16) Gauss2Rec {
 
 // Depth slabs of the (tile, slab) bins: NSLAB equal slabs over the view's
 // depth range [zlo, zlo + NSLAB/inv_dz); keys outside clamp to the end slabs.
-constexpr int NSLAB = 32;   // multiple of 4
+#ifndef GES_NSLAB
+#define GES_NSLAB 48
+#endif
+constexpr int NSLAB = GES_NSLAB;   // multiple of 4
 static_assert(NSLAB % 4 == 0, "scan reads slab counters as uint4");
+
+// Slab index of relative list position `rel` of a tile: the number of slab
+// ends <= rel (ends are non-decreasing).  One vote per 32 slabs; every lane
+// of the warp gets the same answer.
+__device__ __forceinline__ int slab_of_pos(const uint32_t* ends, uint32_t rel, int lane) {
+    int n = 0;
+#pragma unroll
+    for (int k = 0; k < NSLAB; k += 32) {
+        const bool le = lane + k < NSLAB - 1 && ends[lane + k] <= rel;
+        n += __popc(__ballot_sync(0xffffffffu, le));
+    }
+    return n;
+}
 
 struct SlabMap {
     float zlo, inv_dz;

@@ -54,8 +54,7 @@ struct __align__(16) TileSmem {
 // one vote per warp) and the CTA-wide max of the per-warp depths in sm.wmax.
 // Both read shared memory only, so every warp gets the same answer.
 __device__ __forceinline__ float slab_floor(const uint32_t* ends, const SlabMap& m, uint32_t rel, int lane) {
-    const bool le = lane < NSLAB - 1 && ends[lane] <= rel;
-    return m.lower(__popc(__ballot_sync(0xffffffffu, le)));
+    return m.lower(slab_of_pos(ends, rel, lane));
 }
 __device__ __forceinline__ float tile_max(const TileSmem& sm) {
     float m = sm.wmax[0];
@@ -513,6 +512,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 sm.st[3][slot] = make_float4(v[12], v[13], v[14], v[15]);
             }
             uint32_t vote = __ballot_sync(0xffffffffu, live);
+            if (lane == 0) { GES_STAT(6, min(32u, gend - base)); GES_STAT(7, __popc(vote)); }
             __syncwarp();
             while (vote) {
                 const int j = __ffs(vote) - 1;

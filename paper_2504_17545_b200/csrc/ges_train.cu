@@ -273,8 +273,7 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
     const float lx = (float)plx, ly = (float)ply;
     for (uint32_t base = gbeg; base < gend; base += 32) {
         {   // near-to-far slabs: stop once the rest fail every gate of the patch
-            const bool le = lane < NSLAB - 1 && gslab_end[lane] <= base - gbeg;
-            if (a.slabs.lower(__popc(__ballot_sync(0xffffffffu, le))) > wdmax) break;
+            if (a.slabs.lower(slab_of_pos(gslab_end, base - gbeg, lane)) > wdmax) break;
         }
         const uint32_t e = base + lane;
         bool live = false;

@@ -16,7 +16,7 @@ import paper_2504_17545_b200 as G  # noqa: E402
 from paper_2504_17545_b200 import _lib, scenes as S  # noqa: E402
 
 NAMES = ["surfel batches", "surfel entries staged", "  with live mask", "surfel warp tests",
-         "candidate lanes", "gauss batches", "gauss entries staged", "  with live mask",
+         "candidate lanes", "gauss batches", "gauss entries walked (x warps)", "  surviving the warp cull",
          "gauss warp tests", "contributing lanes", "tiles", "tiles with uncovered px"]
 
 ap = argparse.ArgumentParser()
