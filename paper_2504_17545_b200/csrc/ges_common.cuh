@@ -22,6 +22,7 @@ constexpr float ALPHA_CUTOFF_F = 1.0f / 255.0f;   // forward.py:26
 // Camera in the form the kernels use (double for per-primitive math).
 struct CamK {
     double fx, fy, cx, cy;
+    double ifx, ify;    // 1/fx, 1/fy
     double R[9];
     double t[3];
     double pos[3];      // world-space camera centre -R^T t (cameras.py:38)

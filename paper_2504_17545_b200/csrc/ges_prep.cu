@@ -14,6 +14,7 @@ namespace ges {
 CamK make_cam(const ges_camera_t& c, int scale) {
     CamK k{};
     k.fx = c.fx * scale; k.fy = c.fy * scale; k.cx = c.cx * scale; k.cy = c.cy * scale;
+    k.ifx = 1.0 / k.fx; k.ify = 1.0 / k.fy;
     for (int i = 0; i < 3; ++i) {
         for (int j = 0; j < 3; ++j) k.R[3 * i + j] = c.w2c[4 * i + j];
         k.t[i] = c.w2c[4 * i + 3];
@@ -38,7 +39,7 @@ __device__ __forceinline__ d3 rot(const CamK& c, d3 v) {   // W v
 // Columns of the rotation of quaternion (w,x,y,z), renormalised (geometry.py:18-36).
 __device__ __forceinline__ void quat_cols(float4 qf, d3& c0, d3& c1, d3& c2) {
     double w = qf.x, x = qf.y, y = qf.z, z = qf.w;
-    double inv = 1.0 / sqrt(w * w + x * x + y * y + z * z);
+    double inv = rsqrt(w * w + x * x + y * y + z * z);
     w *= inv; x *= inv; y *= inv; z *= inv;
     c0 = mk(1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y));
     c1 = mk(2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x));
@@ -61,8 +62,9 @@ __device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1,
         double c1 = -2.0 * (A2 * B2 - (A0 * B0 + A1 * B1));
         double c0 = A2 * A2 - (A0 * A0 + A1 * A1);
         double root = sqrt(fmax(c1 * c1 - 4.0 * c2s * c0, 0.0));
-        lo[ax] = (-c1 - root) / (2.0 * c2s);
-        hi[ax] = (-c1 + root) / (2.0 * c2s);
+        const double i2 = 0.5 / c2s;   // bounds only cull: a 1-ulp change moves no pixel centre in or out
+        lo[ax] = (-c1 - root) * i2;
+        hi[ax] = (-c1 + root) * i2;
     }
     auto clampi = [](double v, int n) -> int {
         if (!(v >= 0.0)) return 0;          // also NaN -> 0 like np.clip of NaN cast (never alive)
@@ -105,7 +107,7 @@ __device__ __forceinline__ void count_tiles(uint32_t* cnt, const Grid& g, bool l
 // Ray-plane homography of a planar primitive relative to pixel (xr, yr):
 // n.d, U and V as affine functions of the pixel offset (see SurfRec).
 __device__ __forceinline__ float4 affine_of(d3 v, const CamK& c, int xr, int yr, float last) {
-    double cx = v.x / c.fx, cy = v.y / c.fy;
+    double cx = v.x * c.ifx, cy = v.y * c.ify;
     double c0 = cx * (xr + 0.5 - c.cx) + cy * (yr + 0.5 - c.cy) + v.z;
     return make_float4((float)c0, (float)cx, (float)cy, last);
 }
@@ -118,7 +120,8 @@ __device__ __forceinline__ void planar_coeffs(d3 q, d3 a1, d3 a2, d3 n, double s
     d3 cv = scl(sub(scl(a2, nq), scl(n, dot(a2, q))), 1.0 / s2);
     int xr = x0, yr = y0;
     if (q.z > 0.0) {
-        double mx = c.fx * q.x / q.z + c.cx, my = c.fy * q.y / q.z + c.cy;
+        const double iz = 1.0 / q.z;   // reference pixel of the coefficients: any pixel works
+        double mx = c.fx * q.x * iz + c.cx, my = c.fy * q.y * iz + c.cy;
         xr = (int)fmin(fmax(floor(mx), (double)x0), (double)x1);
         yr = (int)fmin(fmax(floor(my), (double)y0), (double)y1);
     }
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(256, 4) k_gauss3_prep(ges_scene_t sc, CamK cam
     double m2max = 2.0 * log(fmax(255.0 * sig, 1e-12));
     valid = valid && m2max > 0.0;
     double rx = sqrt(fmax(m2max * c00, 0.0)), ry = sqrt(fmax(m2max * c11, 0.0));
-    double mx = cam.fx * ts.x / ts.z + cam.cx, my = cam.fy * ts.y / ts.z + cam.cy;
+    double mx = cam.fx * ts.x * iz + cam.cx, my = cam.fy * ts.y * iz + cam.cy;
     GaussRec rec;
     int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
     if (valid) {
