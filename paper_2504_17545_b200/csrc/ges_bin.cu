@@ -112,13 +112,18 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
     const unsigned lt = (1u << lane) - 1u;
     uint32_t base_r[FILL_R], toff_r[FILL_R], peers_r[FILL_R];
     bool act_r[FILL_R];
+    // rounds this warp needs (most primitives touch 1-4 tiles): the unrolled
+    // batches below stop at the warp's largest tile count
+    int ntl = more ? (tx1 - tx0 + 1) * (ty1 - (y0 >> sh) + 1) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ntl = max(ntl, __shfl_xor_sync(0xffffffffu, ntl, o));
 #pragma unroll
     for (int r = 0; r < FILL_R; ++r) {
         act_r[r] = more;
         peers_r[r] = 0u;
         base_r[r] = 0u;
         toff_r[r] = 0u;
-        if (__any_sync(0xffffffffu, more)) {
+        if (r < ntl) {
             const int tile = ty * p.ntx + tx;
             const int key = more ? tile * NSLAB + slab : -1;
             const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -133,6 +138,7 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
     }
 #pragma unroll
     for (int r = 0; r < FILL_R; ++r) {
+        if (r >= ntl) break;
         // every lane of a group takes its leader's base (inactive lanes form their own groups)
         const int leader = act_r[r] ? __ffs(peers_r[r]) - 1 : (int)lane;
         const uint32_t b = __shfl_sync(0xffffffffu, base_r[r], leader);
