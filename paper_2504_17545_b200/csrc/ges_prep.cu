@@ -46,39 +46,52 @@ __device__ __forceinline__ void quat_cols(float4 qf, d3& c0, d3& c1, d3& c2) {
     c2 = mk(2 * (x * z + w * y), 2 * (y * z - w * x), 1 - 2 * (x * x + y * y));
 }
 
-// Exact screen AABB of the projected disc {a m1 + b m2 : a^2+b^2<=1}
+// Screen AABB of the projected disc {q + a m1 + b m2 : a^2+b^2<=1}
 // (geometry.py:273-302) -> inclusive pixel ranges with 0.5 px padding
 // (forward.py:85-96).  Returns false if the range is empty.
+//
+// The ranges only cull (every pixel in them still gets the exact coverage
+// test), so they need to contain the reference's, not to equal them.  The
+// tangent condition is solved relative to the projected centre s0 = q_a/q_z,
+// s = s0 + delta: with w = m_a - s0 m_z (per disc axis),
+//   delta^2 (q_z^2 - |m_z|^2) + 2 delta (w.m_z) - |w|^2 = 0,
+// whose coefficients are of the disc's size, so float32 is accurate to
+// ~1e-6 of the disc extent; the bounds are widened by PAD_PX to cover that.
+// q_z^2 <= |m_z|^2 (the disc reaches the focal plane) is the reference's
+// whole-screen case; it is taken with a relative margin (superset).
 __device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1, int& y0, int& y1) {
-    double B0 = m1.z, B1 = m2.z, B2 = q.z;
-    double c2 = B2 * B2 - (B0 * B0 + B1 * B1);
-    bool whole = c2 <= 0.0;
-    double c2s = whole ? 1.0 : c2;
-    double lo[2], hi[2];
-    for (int ax = 0; ax < 2; ++ax) {
-        double f = ax ? c.fy : c.fx, cc = ax ? c.cy : c.cx;
-        double m1a = ax ? m1.y : m1.x, m2a = ax ? m2.y : m2.x, qa = ax ? q.y : q.x;
-        double A0 = f * m1a + cc * m1.z, A1 = f * m2a + cc * m2.z, A2 = f * qa + cc * q.z;
-        double c1 = -2.0 * (A2 * B2 - (A0 * B0 + A1 * B1));
-        double c0 = A2 * A2 - (A0 * A0 + A1 * A1);
-        double root = sqrt(fmax(c1 * c1 - 4.0 * c2s * c0, 0.0));
-        const double i2 = 0.5 / c2s;   // bounds only cull: a 1-ulp change moves no pixel centre in or out
-        lo[ax] = (-c1 - root) * i2;
-        hi[ax] = (-c1 + root) * i2;
-    }
-    auto clampi = [](double v, int n) -> int {
-        if (!(v >= 0.0)) return 0;          // also NaN -> 0 like np.clip of NaN cast (never alive)
-        if (v > n - 1.0) return n - 1;
+    constexpr float PAD_PX = 0.01f;
+    const float qz = (float)q.z, m1z = (float)m1.z, m2z = (float)m2.z;
+    const float A = fmaf(qz, qz, -(m1z * m1z + m2z * m2z));
+    const bool whole = !(A > 1e-5f * qz * qz);
+    auto clampi = [](float v, int n) -> int {
+        if (!(v >= 0.f)) return 0;
+        if (v > n - 1.f) return n - 1;
         return (int)v;
     };
     if (whole) {
         x0 = 0; x1 = c.W - 1; y0 = 0; y1 = c.H - 1;
-    } else {
-        x0 = clampi(ceil(lo[0] - 0.5 - 0.5), c.W);
-        x1 = clampi(floor(hi[0] + 0.5 - 0.5), c.W);
-        y0 = clampi(ceil(lo[1] - 0.5 - 0.5), c.H);
-        y1 = clampi(floor(hi[1] + 0.5 - 0.5), c.H);
+        return c.W > 0 && c.H > 0;
     }
+    const float iA = 1.0f / A, iz = 1.0f / qz;
+    float lo[2], hi[2];
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+        const float f = (float)(ax ? c.fy : c.fx), cc = (float)(ax ? c.cy : c.cx);
+        const float s0 = (float)(ax ? q.y : q.x) * iz;
+        const float w1 = fmaf(-s0, m1z, (float)(ax ? m1.y : m1.x)), w2 = fmaf(-s0, m2z, (float)(ax ? m2.y : m2.x));
+        const float B = fmaf(w1, m1z, w2 * m2z), Cw = fmaf(w1, w1, w2 * w2);
+        const float root = sqrtf(fmaxf(fmaf(B, B, A * Cw), 0.f));
+        const float dlo = (-B - root) * iA, dhi = (-B + root) * iA;
+        const float clo = fmaf(f, s0 + dlo, cc), chi = fmaf(f, s0 + dhi, cc);
+        const float pad = PAD_PX + 1e-6f * (fabsf(clo) + fabsf(chi));
+        lo[ax] = clo - pad;
+        hi[ax] = chi + pad;
+    }
+    x0 = clampi(ceilf(lo[0] - 0.5f - 0.5f), c.W);
+    x1 = clampi(floorf(hi[0] + 0.5f - 0.5f), c.W);
+    y0 = clampi(ceilf(lo[1] - 0.5f - 0.5f), c.H);
+    y1 = clampi(floorf(hi[1] + 0.5f - 0.5f), c.H);
     return x1 >= x0 && y1 >= y0;
 }
 
