@@ -19,6 +19,17 @@ constexpr float PARALLEL_EPS_F = 1e-8f;           // geometry.py:15
 constexpr double SCREEN_VAR = 0.3;                // filters.py:21
 constexpr float ALPHA_CUTOFF_F = 1.0f / 255.0f;   // forward.py:26
 
+constexpr float LOG2E_F = 1.4426950408889634f;
+constexpr float LN2_F = 0.6931471805599453f;
+
+// 2^x on the SFU, flush-to-zero (results below 2^-126 only ever fail the
+// 1/255 alpha cutoff)
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Camera in the form the kernels use (double for per-primitive math).
 struct CamK {
     double fx, fy, cx, cy;
@@ -45,8 +56,9 @@ struct __align__(16) SurfRec {
 // 3D EWA, 64 B:
 //   c  = (depth, eps, rect_x, rect_y)
 //   r0 = (mx_int, mx_frac, my_int, my_frac)       mean2d split for precision
-//   r1 = (pa, pb, pc, sigma)  power = pa dx^2 + pb dx dy + pc dy^2
-//   r2 = (pmin, r, g, b)      pmin: power below which alpha < 1/255
+//   r1 = (pa, pb, pc, sigma)  log2(e) * power = pa dx^2 + pb dx dy + pc dy^2,
+//                             alpha = sigma * 2^(pa dx^2 + ...)
+//   r2 = (pmin, r, g, b)      pmin: log2(e) * power below which alpha < 1/255
 struct __align__(16) GaussRec {
     float4 c, r0, r1, r2;
 };

@@ -330,8 +330,10 @@ __global__ void __launch_bounds__(256, 4) k_gauss3_prep(ges_scene_t sc, CamK cam
         double mxi = floor(mx), myi = floor(my);
         rec.c = make_float4(depf, epsf, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)));
         rec.r0 = make_float4((float)mxi, (float)(mx - mxi), (float)myi, (float)(my - myi));
-        rec.r1 = make_float4((float)(-0.5 * la), (float)(-lb), (float)(-0.5 * lc), (float)sig);
-        const float pmin = (float)(-0.5 * m2max) - 1e-4f;
+        // conic pre-scaled by log2(e): the tile kernel evaluates exp as one ex2
+        const double L2E = 1.4426950408889634;
+        rec.r1 = make_float4((float)(-0.5 * L2E * la), (float)(-L2E * lb), (float)(-0.5 * L2E * lc), (float)sig);
+        const float pmin = (float)(-0.5 * L2E * m2max) - 1e-4f;
         d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
         double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
         float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),

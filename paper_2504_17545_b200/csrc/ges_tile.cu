@@ -154,11 +154,11 @@ static __device__ __noinline__ float3 surfel_color_eval(const float* __restrict_
 // every sample reads its colour back.  Must be called by all 32 lanes, with
 // the warp's slice of sm.st free.
 template <int NS>
-__device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, TileSmem& sm, const unsigned long long* best,
+__device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, TileSmem& sm, uint32_t covm,
                                                       const uint32_t* bp, int lane, int warp, float3* col) {
     const float3 bg = make_float3(a.bg[0], a.bg[1], a.bg[2]);
     if constexpr (NS == 1) {
-        const bool cov = best[0] != ~0ull;
+        const bool cov = covm & 1u;
         const unsigned peers = __match_any_sync(0xffffffffu, cov ? bp[0] : 0xffffffffu);
         const int leader = __ffs(peers) - 1;
         float3 c = bg;
@@ -175,12 +175,12 @@ __device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, TileSme
         uint32_t need = 0;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-            const bool cov = best[s] != ~0ull;
+            const bool cov = (covm >> s) & 1u;
             const uint32_t v = cov ? bp[s] : 0xffffffffu;
             dup[s] = -1;
 #pragma unroll
             for (int q = s - 1; q >= 0; --q)
-                if (cov && bp[q] == v && best[q] != ~0ull) dup[s] = q;
+                if (cov && bp[q] == v && ((covm >> q) & 1u)) dup[s] = q;
             leader[s] = __ffs(__match_any_sync(0xffffffffu, v)) - 1;
             if (cov && dup[s] < 0 && lane == leader[s]) need |= 1u << s;
         }
@@ -205,7 +205,7 @@ __device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, TileSme
             if ((need >> s) & 1u) { own = k++; tp[own] = bp[s]; }
             else if (dup[s] >= 0) own = task[dup[s]];
             const int lead = __shfl_sync(0xffffffffu, own, leader[s]);
-            task[s] = best[s] == ~0ull ? -1 : (dup[s] >= 0 || ((need >> s) & 1u)) ? own : lead;
+            task[s] = !((covm >> s) & 1u) ? -1 : (dup[s] >= 0 || ((need >> s) & 1u)) ? own : lead;
         }
         __syncwarp();
         for (int i = lane; i < total; i += 32) {
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
     // up once after pass 1
     unsigned long long best[NS];
     uint32_t bp[NS];
+    uint32_t covm = 0;   // bit s: sample s covered (best[] is dead after pass 1)
 
     // ------------------------------------------------------------ pass 1
     if constexpr (MODE & 1) {
@@ -391,7 +392,10 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
         // their packed indices and start pulling them into L2 now, overlapping
         // the Gaussian pass
 #pragma unroll
-        for (int s = 0; s < NS; ++s) bp[s] = best[s] != ~0ull ? __ldg(a.s_pack + (uint32_t)best[s]) : 0u;
+        for (int s = 0; s < NS; ++s) {
+            bp[s] = best[s] != ~0ull ? __ldg(a.s_pack + (uint32_t)best[s]) : 0u;
+            covm |= (best[s] != ~0ull ? 1u : 0u) << s;
+        }
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             if (best[s] != ~0ull) {
@@ -457,6 +461,9 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
         }
         const int ox = tx * TP, oy = ty * TP;
         const int px0 = (warp & 1) * 8 * PX, py0 = (warp >> 1) * 4 * PX;   // this warp's patch
+        float lxs[PX], lys[PX];   // this thread's pixel coordinates in the tile
+#pragma unroll
+        for (int i = 0; i < PX; ++i) { lxs[i] = (float)(PX * plx + i); lys[i] = (float)(PX * ply + i); }
         for (uint32_t base = gbeg; base < gend; base += 32) {
             // keys (depth - eps) are binned near-to-far: the rest fail every gate of the patch
             if (slab_floor(sm.gslab_end, a.slabs, base - gbeg, lane) > wdmax) break;
@@ -532,13 +539,14 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 }
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
-                    const float lx = (float)(PX * plx + p % PX), ly = (float)(PX * ply + p / PX);
+                    const float lx = lxs[p % PX], ly = lys[p / PX];
                     if constexpr (GK == 3) {
-                        // forward.py:301-311
+                        // forward.py:301-311; the conic is pre-scaled by log2(e), so
+                        // exp is one ex2 (branch-free: most survivors' pixels pass)
                         const float dx = lx - w[0], dy = ly - w[1];
                         const float pw = fmaf(w[2] * dx, dx, fmaf(w[4] * dy, dy, w[3] * dx * dy));
-                        if (pw >= w[8]) {
-                            const float al = w[5] * __expf(pw);
+                        {
+                            const float al = w[5] * ex2_ftz(pw);
                             if (al >= ALPHA_CUTOFF_F && w[6] < ds[p] + w[7]) {
                                 GES_STAT(9, 1);
                                 wsum[p] += al;
@@ -561,7 +569,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                             const float inv = __fdividef(1.0f, den);
                             const float t = w[3] * inv;
                             const float q2 = r2u * inv * inv;
-                            const float al = w[10] * __expf(-0.5f * q2);
+                            const float al = w[10] * ex2_ftz(q2 * (-0.5f * LOG2E_F));
                             if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds[p] + w[11]) {
                                 wsum[p] += al;
                                 cr[p] = fmaf(al, w[13], cr[p]); cg[p] = fmaf(al, w[14], cg[p]);
@@ -588,7 +596,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
     for (int p = 0; p < NP; ++p) cs[p] = make_float3(a.bg[0], a.bg[1], a.bg[2]);
     if constexpr ((MODE & 1) != 0) {
         float3 col[NS];
-        resolve_surfel_colors<NS>(a, sm, best, bp, lane, warp, col);
+        resolve_surfel_colors<NS>(a, sm, covm, bp, lane, warp, col);
         if constexpr (PX == 1) {   // box mean over the sub-samples (forward.py:201-203)
             float3 acc = make_float3(0.f, 0.f, 0.f);
 #pragma unroll

@@ -300,9 +300,9 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                 const float mx = (r0.x - (float)ox) + (r0.y - 0.5f), my = (r0.z - (float)oy) + (r0.w - 0.5f);
                 // identical to the forward tile kernel (forward.py:301-311)
                 const float dx = lx - mx, dy = ly - my;
-                const float pw = fmaf(r1.x * dx, dx, fmaf(r1.z * dy, dy, r1.y * dx * dy));
-                if (inside && pw >= r2.x) {
-                    const float al = r1.w * __expf(pw);
+                const float pw = fmaf(r1.x * dx, dx, fmaf(r1.z * dy, dy, r1.y * dx * dy));   // log2(e) * power
+                if (inside) {
+                    const float al = r1.w * ex2_ftz(pw);
                     if (al >= ALPHA_CUTOFF_F && c.x < ds + c.y) {
                         contrib = true;
                         // training.py:652-690: g_alpha, then alpha = amp exp(power)
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                             ga = fmaf(nv.x, gnx, fmaf(nv.y, gny, fmaf(nv.z, gnz, ga)));
                         }
                         const float gp = ga * al;
-                        const float la = -2.f * r1.x, lb = -r1.y, lc = -2.f * r1.z;
+                        const float la = -2.f * LN2_F * r1.x, lb = -LN2_F * r1.y, lc = -2.f * LN2_F * r1.z;
                         v[0] = gp;
                         v[1] = gp * fmaf(la, dx, lb * dy);
                         v[2] = gp * fmaf(lb, dx, lc * dy);
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                     const float inv = __fdividef(1.0f, den);
                     const float t = r0.w * inv;
                     const float q2 = r2u * inv * inv;
-                    const float G = __expf(-0.5f * q2);
+                    const float G = ex2_ftz(q2 * (-0.5f * LOG2E_F));
                     const float al = r3.x * G;
                     if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds + c.y) {
                         contrib = true;
