@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
             bp[s] = best[s] != ~0ull ? __ldg(a.s_pack + (uint32_t)best[s]) : 0u;
             covm |= (best[s] != ~0ull ? 1u : 0u) << s;
         }
+        asm volatile("" : "+r"(covm));   // materialise now so best[] dies before pass 2
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             if (best[s] != ~0ull) {
@@ -410,6 +411,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
             const int s0 = (p / PX) * SS * G + (p % PX) * SS;
             const bool cov = best[s0] != ~0ull;
             ds[p] = cov ? __uint_as_float((uint32_t)(best[s0] >> 32)) : INFINITY;
+            asm volatile("" : "+f"(ds[p]));   // (not rematerialised from best[] in pass 2)
             if (inside_px(p)) {
                 const int64_t pix = pix_of(p);
                 if (a.out.s_depth) a.out.s_depth[pix] = ds[p];
@@ -463,7 +465,10 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
         const int px0 = (warp & 1) * 8 * PX, py0 = (warp >> 1) * 4 * PX;   // this warp's patch
         float lxs[PX], lys[PX];   // this thread's pixel coordinates in the tile
 #pragma unroll
-        for (int i = 0; i < PX; ++i) { lxs[i] = (float)(PX * plx + i); lys[i] = (float)(PX * ply + i); }
+        for (int i = 0; i < PX; ++i) {
+            lxs[i] = (float)(PX * plx + i); lys[i] = (float)(PX * ply + i);
+            asm volatile("" : "+f"(lxs[i]), "+f"(lys[i]));
+        }
         for (uint32_t base = gbeg; base < gend; base += 32) {
             // keys (depth - eps) are binned near-to-far: the rest fail every gate of the patch
             if (slab_floor(sm.gslab_end, a.slabs, base - gbeg, lane) > wdmax) break;
