@@ -30,6 +30,13 @@ __device__ __forceinline__ float ex2_ftz(float x) {
     return y;
 }
 
+// 1/x on the SFU (approximate, ~1 ulp), flush-to-zero; callers guarantee |x| >= 1e-8
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Camera in the form the kernels use (double for per-primitive math).
 struct CamK {
     double fx, fy, cx, cy;

@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                             // current best (all multiplied out, den > 0 <=> t > 0); the exact
                             // t > 0.01 and packed-key comparison run only for candidates
                             if (den > pe && r2 <= den * den && A.w <= tb[s] * den) {
-                                const float t = __fdividef(A.w, den);   // 2 ulp: ties are flagged
+                                const float t = A.w * rcp_ftz(den);   // den > 1e-8|d|; 2 ulp: ties are flagged
                                 const unsigned long long key =
                                     ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
                                 GES_STAT(4, 1);
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                         const float V = fmaf(w[9], ly, fmaf(w[8], lx, w[7]));
                         const float r2u = fmaf(U, U, V * V);
                         if (r2u <= w[12] * den * den && fabsf(den) > pe[p]) {
-                            const float inv = __fdividef(1.0f, den);
+                            const float inv = rcp_ftz(den);   // |den| > 1e-8|d|
                             const float t = w[3] * inv;
                             const float q2 = r2u * inv * inv;
                             const float al = w[10] * ex2_ftz(q2 * (-0.5f * LOG2E_F));

@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                 const float V = fmaf(r2.z, ly, fmaf(r2.y, lx, v0));
                 const float r2u = fmaf(U, U, V * V);
                 if (inside && r2u <= r3.y * den * den && fabsf(den) > pe) {
-                    const float inv = __fdividef(1.0f, den);
+                    const float inv = rcp_ftz(den);   // |den| > 1e-8|d|
                     const float t = r0.w * inv;
                     const float q2 = r2u * inv * inv;
                     const float G = ex2_ftz(q2 * (-0.5f * LOG2E_F));
