@@ -239,9 +239,9 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.synchronize()
     upload_ms = (time.perf_counter() - t0) * 1e3
     rend = G.Renderer(dev)
-    # B_alg outputs (image fp32, depth, winner) + the RGBA8 send buffer for the gather
-    vb = ViewBatchRenderer(rend, ds, cams, settings, want=("image", "s_depth", "s_winner", "image_rgba8"),
-                           streams=args.streams)
+    # B_alg outputs (image fp32, depth, winner) + the RGBA8 send buffer of the gather (N > 1)
+    want = ("image", "s_depth", "s_winner") + (("image_rgba8",) if world > 1 else ())
+    vb = ViewBatchRenderer(rend, ds, cams, settings, want=want, streams=args.streams)
     # size every workspace's pair lists from a checked frame of every view
     for r in vb.pool:
         for c, fr in zip(vb.cams, vb.frames):

@@ -104,7 +104,7 @@ __device__ __forceinline__ float3 im_of(const TileArgs& a, float3 cs, float w, f
         }
         return make_float3(a.bg[0], a.bg[1], a.bg[2]);
     }
-    const float r = 1.0f / (1.0f + w);
+    const float r = __frcp_rn(1.0f + w);
     return make_float3((cs.x + cr) * r, (cs.y + cg) * r, (cs.z + cb) * r);
 }
 
@@ -279,11 +279,12 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
             for (int gx = 0; gx < G; ++gx) {
                 const int X = bx * SS + gx, Y = by * SS + gy;
                 const float dxn = ((float)X + 0.5f - a.rcx) * a.rifx, dyn = ((float)Y + 0.5f - a.rcy) * a.rify;
-                pe = fmaxf(pe, PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f));
+                pe = fmaxf(pe, fmaf(dxn, dxn, dyn * dyn));
                 best[gy * G + gx] = ~0ull;
                 const bool in = bx + gx / SS < a.W && by + gy / SS < a.H;
                 tb[gy * G + gx] = in ? INFINITY : 0.f;
             }
+        pe = PARALLEL_EPS_F * sqrtf(pe + 1.0f);   // max over the samples of 1e-8 |d|
         auto patch_depth = [&]() {
             float m = tb[0];
 #pragma unroll
