@@ -247,6 +247,18 @@ int ges_backward_gaussians(const ges_scene_t *scene, const ges_scene_src_t *src,
                            size_t scratch_bytes, void *workspace, size_t ws_bytes,
                            int64_t gaussian_pair_cap, ges_frame_status_t *status_dev, void *stream);
 
+/* Per-Gaussian contribution score of one view (optim.py:519-533, the joint
+ * stage's pruning statistic): scores[j] = max(scores[j], max over the
+ * Gaussian's fragments of max_c(colour) * alpha / (1 + W_G)), for source
+ * Gaussian j (order from src->g_order; src may be NULL = identity).
+ * g_weight = W_G (H,W) of the same view and settings, float32; scores
+ * (n_gaussians) float32 >= 0, accumulated across calls.  Workspace as
+ * ges_backward_workspace_bytes. */
+int ges_gaussian_contributions(const ges_scene_t *scene, const ges_scene_src_t *src, const ges_camera_t *cam,
+                               const ges_settings_t *st, const float *surfel_depth, const float *g_weight,
+                               float *scores, void *workspace, size_t ws_bytes, int64_t gaussian_pair_cap,
+                               ges_frame_status_t *status_dev, void *stream);
+
 /* Frozen-surfel half of training.backward (_surfel_backward_frozen,
  * training.py:612-629): winner (H*grid, W*grid) int32 source ids (-1 =
  * uncovered) of the cached opaque z-buffer, g_color = dL/dC_s (H,W,3)

@@ -232,7 +232,7 @@ def _screen(pos, g_pos, c):
     return np.hypot(gcam[:, 0] * z / c.fx * (c.width / 2.0), gcam[:, 1] * z / c.fy * (c.height / 2.0))
 
 
-def _backward_3d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn):
+def _backward_3d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn, wg):
     g = scene.gaussians
     n = int(np.asarray(g.pos).shape[0])
     H, W = c.height, c.width
@@ -278,6 +278,7 @@ def _backward_3d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn):
     S_L = np.zeros((n, 2, 2))
     S_col = np.zeros((n, 3))
     S_d = np.zeros(n)
+    S_con = np.zeros(n)
     for i, win in _windows(x0, x1, y0, y1, W):
         if win is None or not valid[i]:
             continue
@@ -289,6 +290,7 @@ def _backward_3d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn):
         if not np.any(ok):
             continue
         X, Y, dlt, a = X[ok], Y[ok], dlt[ok], a[ok]
+        S_con[i] = np.max(cols[i].max() * a / (1.0 + wg[Y, X]))   # optim.py:526-533
         ga = g_cg[Y, X] @ cols[i] + g_wg[Y, X]
         if g_gd is not None:
             ga = ga + z[i] * g_gd[Y, X]
@@ -330,10 +332,12 @@ def _backward_3d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn):
     g_pos = g_pos + g_pos_sh
     g_scale, g_sigma = _chain_eff(s, sig, lam, anyf, es, sig_e, g_es, g_sig_e)
     touched = (S_gp != 0) | np.any(S_col != 0, axis=1) | (S_d != 0) | np.any(S_m != 0, axis=1)
-    return _pack(touched, qn, pos, g_pos, g_quat_u, g_scale, g_sigma, g_sh, c)
+    out = _pack(touched, qn, pos, g_pos, g_quat_u, g_scale, g_sigma, g_sh, c)
+    out["contrib"] = S_con
+    return out
 
 
-def _backward_2d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn):
+def _backward_2d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn, wg):
     g = scene.gaussians
     n = int(np.asarray(g.pos).shape[0])
     H, W = c.height, c.width
@@ -362,6 +366,7 @@ def _backward_2d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn):
     Gsig = np.zeros(n)
     S_col = np.zeros((n, 3))
     S_nv = np.zeros((n, 3))
+    S_con = np.zeros(n)
     for i, win in _windows(x0, x1, y0, y1, W):
         if win is None or not valid[i]:
             continue
@@ -380,6 +385,7 @@ def _backward_2d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn):
         if not np.any(keep):
             continue
         X, Y, d, nd, t, h, u, v, G, a = (w[keep] for w in (X, Y, d, nd, t, h, u, v, G, a))
+        S_con[i] = np.max(cols[i].max() * a / (1.0 + wg[Y, X]))   # optim.py:526-533
         ga = g_cg[Y, X] @ cols[i] + g_wg[Y, X]
         gt_direct = np.zeros_like(t)
         if g_gd is not None:
@@ -408,7 +414,9 @@ def _backward_2d(scene, c, settings, ds, g_cg, g_wg, g_gd, g_gn):
     g_pos = g_pos + g_pos_sh
     g_scale, g_sigma = _chain_eff(s, sig, lam, anyf, es, sig_e, Gs * smul, Gsig * omul)
     touched = (Gsig != 0) | np.any(S_col != 0, axis=1) | np.any(Gq != 0, axis=1)
-    return _pack(touched, qn, pos, g_pos, g_quat_u, g_scale, g_sigma, g_sh, c)
+    out = _pack(touched, qn, pos, g_pos, g_quat_u, g_scale, g_sigma, g_sh, c)
+    out["contrib"] = S_con
+    return out
 
 
 def _pack(touched, qn, pos, g_pos, g_quat_u, g_scale, g_sigma, g_sh, c):
@@ -422,7 +430,8 @@ def _pack(touched, qn, pos, g_pos, g_quat_u, g_scale, g_sigma, g_sh, c):
 
 def backward(scene, cam, settings, frame, g_image, *, g_gauss_depth=None, g_gauss_normal=None,
              g_gauss_weight=None):
-    """training.py:547-609 for the joint stage; returns a dict of float64 arrays."""
+    """training.py:547-609 for the joint stage; returns a dict of float64 arrays
+    (plus ``contrib``: this view's contribution scores, optim.py:519-533)."""
     c = O.as_cam(cam)
     g_img = np.asarray(g_image, dtype=np.float64)
     gw, image = frame["gauss_weight"], frame["image"]
@@ -447,12 +456,12 @@ def backward(scene, cam, settings, frame, g_image, *, g_gauss_depth=None, g_gaus
                surfel_sh=np.zeros((ns, K, 3)), surfel_w=np.zeros(ns), gaussian_pos=np.zeros((ng, 3)),
                gaussian_opacity=np.zeros(ng), gaussian_quat=np.zeros((ng, 4)), gaussian_scale=np.zeros((ng, D)),
                gaussian_sh=np.zeros((ng, K, 3)), surfel_screen_grad=np.zeros(ns),
-               gaussian_screen_grad=np.zeros(ng))
+               gaussian_screen_grad=np.zeros(ng), contrib=np.zeros(ng))
     if frame["gaussians"]:
         gd = None if g_gauss_depth is None else np.asarray(g_gauss_depth, dtype=np.float64)
         gn = None if g_gauss_normal is None else np.asarray(g_gauss_normal, dtype=np.float64)
         fn = _backward_2d if O._is_2d(scene.gaussians.kind) else _backward_3d
-        out.update(fn(scene, c, settings, frame["surfel_depth"], g_cg, g_wg, gd, gn))
+        out.update(fn(scene, c, settings, frame["surfel_depth"], g_cg, g_wg, gd, gn, frame["gauss_weight"]))
     win = frame["winner"]
     if win is not None and np.any(win >= 0):
         grid = frame["grid"]

@@ -402,6 +402,49 @@ int ges_backward_gaussians(const ges_scene_t* sc, const ges_scene_src_t* src, in
     return GES_OK;
 }
 
+int ges_gaussian_contributions(const ges_scene_t* sc, const ges_scene_src_t* src, const ges_camera_t* cam,
+                               const ges_settings_t* st, const float* surfel_depth, const float* g_weight,
+                               float* scores, void* ws, size_t ws_bytes, int64_t cap_g,
+                               ges_frame_status_t* status_dev, void* stream) {
+    int rc;
+    if ((rc = check_scene(sc)) || (rc = check_cam(cam)) || (rc = check_settings(st))) return rc;
+    const int64_t ng = sc->n_gaussians;
+    if (ng == 0) return GES_OK;
+    if (!surfel_depth || !g_weight || !scores) return fail(GES_EINVAL, "surfel_depth/g_weight/scores is NULL");
+    if (src && src->n_gaussians != ng) return fail(GES_EINVAL, "source arrays do not match the packed scene");
+    if (cap_g < 0 || cap_g >= (1ll << 32)) return fail(GES_EINVAL, "pair capacity out of range");
+    const ges_settings_t s2 = backward_settings(st, false);
+    Frame f = layout(ws, sc, cam, &s2, 0, cap_g);
+    if (!ws || ws_bytes < f.bytes) return fail(GES_EWORKSPACE, "workspace too small (see ges_backward_workspace_bytes)");
+    cudaStream_t s = (cudaStream_t)stream;
+    ges_frame_status_t* status = status_dev ? status_dev : f.status;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(f.cnt_s, 0, f.zero_bytes, s)) != cudaSuccess) return cuda_fail(e, "memset counts");
+    if ((e = cudaMemsetAsync(status, 0, sizeof(ges_frame_status_t), s)) != cudaSuccess)
+        return cuda_fail(e, "memset status");
+    const CamK cg = make_cam(*cam, 1);
+    const SlabMap slabs = slab_map(*sc, cg);
+    Grid gg{cg.W, cg.H, TILE, f.ntx, f.nty, slabs};
+    ges_scene_t scs = *sc;
+    scs.n_surfels = 0;
+    const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, 0, f.ntiles, f.ntx, TILE, 4};
+    const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE, 4};
+    PrepOut po{f.grec, nullptr, f.g_nrm, f.cnt_g, nullptr};
+    if ((e = launch_gauss_prep(scs, cg, gg, s2, po, s))) return cuda_fail(e, "gaussian preprocess");
+    if ((e = launch_scan(bs, bg, status, s))) return cuda_fail(e, "tile scan");
+    if ((e = launch_fill(f.srec, 0, bs, f.grec, ng, sc->gaussian_dim, bg, slabs, s))) return cuda_fail(e, "tile fill");
+    BwdArgs a{};
+    a.W = cam->width; a.H = cam->height; a.ntx = f.ntx; a.nty = f.nty;
+    a.grec = f.grec; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg; a.slabs = slabs;
+    a.ds = surfel_depth; a.g_wg = g_weight;
+    a.gcx = (float)cg.cx; a.gcy = (float)cg.cy; a.gifx = (float)(1.0 / cg.fx); a.gify = (float)(1.0 / cg.fy);
+    a.scores = scores;
+    a.order = src ? src->g_order : nullptr;
+    a.status = status;
+    if ((e = launch_gauss_contrib(a, sc->gaussian_dim, s))) return cuda_fail(e, "gaussian contributions");
+    return GES_OK;
+}
+
 int ges_backward_surfels_frozen(const ges_scene_src_t* src, const ges_camera_t* cam, int32_t grid,
                                 const int32_t* winner, const float* g_color, double* col, double* g_sh,
                                 double* g_pos, void* stream) {

@@ -84,11 +84,14 @@ struct BwdArgs {
     const float *ds, *g_cg, *g_wg, *g_gd, *g_gn;   // gd, gn may be NULL
     float gcx, gcy, gifx, gify;
     double* acc;                  // 16 float64 partial sums per packed Gaussian
+    float* scores;                // contribution mode: per-source-Gaussian max
+    const int32_t* order;         // packed -> source index (NULL = identity)
     const ges_frame_status_t* status;
 };
 
 cudaError_t launch_surfel_colors(const ges_scene_t& sc, const CamK& cam, float* rgb, cudaStream_t s);
 cudaError_t launch_gauss_bwd(const BwdArgs& a, int g_kind, bool geom, cudaStream_t s);
+cudaError_t launch_gauss_contrib(const BwdArgs& a, int g_kind, cudaStream_t s);
 cudaError_t launch_gauss_finish(const ges_scene_src_t& src, int any_filter, int mip, const CamK& cam,
                                 const double* acc, const ges_gauss_grads_t& out, cudaStream_t s);
 cudaError_t launch_frozen_bwd(const ges_scene_src_t& src, const CamK& cam, int W, int H, int grid,

@@ -241,7 +241,10 @@ __global__ void k_surfel_colors(ges_scene_t sc, CamK cam, float* rgb) {
 }
 
 // ---------------------------------------------------------------- tile replay
-template <int GK, bool GEOM>
+// CONTRIB: instead of gradients, the per-Gaussian max over its fragments of
+// max_c(colour) * alpha / (1 + W_G) (optim.py:526-533; g_wg = W_G then),
+// atomically max-ed into a.scores[source id].
+template <int GK, bool GEOM, bool CONTRIB = false>
 __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
     __shared__ uint32_t gslab_end[NSLAB];
     if (a.status->overflow) return;
@@ -254,11 +257,12 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
     float ds = INFINITY, gcr = 0.f, gcg = 0.f, gcb = 0.f, gw = 0.f, gd = 0.f, gnx = 0.f, gny = 0.f, gnz = 0.f;
     if (inside) {
         ds = a.ds[pix];
-        gcr = a.g_cg[3 * pix]; gcg = a.g_cg[3 * pix + 1]; gcb = a.g_cg[3 * pix + 2];
+        if (!CONTRIB) { gcr = a.g_cg[3 * pix]; gcg = a.g_cg[3 * pix + 1]; gcb = a.g_cg[3 * pix + 2]; }
         gw = a.g_wg[pix];
         if (a.g_gd) gd = a.g_gd[pix];
         if (a.g_gn) { gnx = a.g_gn[3 * pix]; gny = a.g_gn[3 * pix + 1]; gnz = a.g_gn[3 * pix + 2]; }
     }
+    const float cden = CONTRIB ? 1.0f / (1.0f + gw) : 0.f;   // gw = W_G in CONTRIB mode
     if (threadIdx.x < NSLAB) gslab_end[threadIdx.x] = a.gbin.cnt[tile * NSLAB + threadIdx.x];
     const uint32_t gbeg = a.gbin.tile_off(tile), gend = gbeg + a.gbin.cnt[tile * NSLAB + NSLAB - 1];
     __syncthreads();
@@ -305,6 +309,9 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                     const float al = r1.w * ex2_ftz(pw);
                     if (al >= ALPHA_CUTOFF_F && c.x < ds + c.y) {
                         contrib = true;
+                        if constexpr (CONTRIB) {
+                            v[0] = fmaxf(r2.y, fmaxf(r2.z, r2.w)) * al * cden;
+                        } else {
                         // training.py:652-690: g_alpha, then alpha = amp exp(power)
                         float ga = fmaf(r2.y, gcr, fmaf(r2.z, gcg, fmaf(r2.w, gcb, gw)));
                         ga = fmaf(c.x, gd, ga);
@@ -322,12 +329,14 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                         v[5] = -0.5f * gp * dy * dy;
                         v[6] = al * gcr; v[7] = al * gcg; v[8] = al * gcb;
                         v[9] = al * gd;
+                        }
                     }
                 }
             } else {
                 const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + gid;
                 const float4 c = r->c, r0 = r->r0, r1 = r->r1, r2 = r->r2, r3 = r->r3, r4 = r->r4;
-                const float4 k1c = a.aux[2 * (size_t)gid], k2c = a.aux[2 * (size_t)gid + 1];
+                const float4 k1c = CONTRIB ? float4{} : a.aux[2 * (size_t)gid];
+                const float4 k2c = CONTRIB ? float4{} : a.aux[2 * (size_t)gid + 1];
                 const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
                 const float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
                 const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
@@ -345,6 +354,9 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                     const float al = r3.x * G;
                     if (t > NEAR_F && al >= ALPHA_CUTOFF_F && t < ds + c.y) {
                         contrib = true;
+                        if constexpr (CONTRIB) {
+                            v[0] = fmaxf(r4.x, fmaxf(r4.y, r4.z)) * al * cden;
+                        } else {
                         // training.py:731-754: g_alpha, g_sigma', g_G, g_u, g_v, g_t
                         float ga = fmaf(r4.x, gcr, fmaf(r4.y, gcg, fmaf(r4.z, gcb, gw)));
                         ga = fmaf(t, gd, ga);
@@ -369,10 +381,18 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                         v[9] = ga * G;
                         v[10] = al * gcr; v[11] = al * gcg; v[12] = al * gcb;
                         v[13] = al * gnx; v[14] = al * gny; v[15] = al * gnz;
+                        }
                     }
                 }
             }
             if (!__any_sync(0xffffffffu, contrib)) continue;
+            if constexpr (CONTRIB) {
+                const float m = warp_maxf(v[0]);
+                if (lane == 0 && m > 0.f)
+                    atomicMax(reinterpret_cast<unsigned int*>(a.scores) + (a.order ? a.order[gid] : (int32_t)gid),
+                              __float_as_uint(m));   // non-negative floats order like their bits
+                continue;
+            }
             constexpr int NV = GK == 3 ? 10 : NACC;
             float mine = 0.f;
 #pragma unroll
@@ -673,6 +693,13 @@ cudaError_t launch_gauss_bwd(const BwdArgs& a, int g_kind, bool geom, cudaStream
         if (geom) k_gauss_bwd<3, true><<<nt, 256, 0, s>>>(a);
         else k_gauss_bwd<3, false><<<nt, 256, 0, s>>>(a);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gauss_contrib(const BwdArgs& a, int g_kind, cudaStream_t s) {
+    const dim3 nt((unsigned)a.ntx, (unsigned)a.nty);
+    if (g_kind == 2) k_gauss_bwd<2, false, true><<<nt, 256, 0, s>>>(a);
+    else k_gauss_bwd<3, false, true><<<nt, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

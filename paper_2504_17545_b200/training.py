@@ -306,3 +306,47 @@ def backward(frame: TrainFrame, g_image, *, g_blend_depth=None, g_blend_normal=N
     if not to_numpy:
         return GradientSet(**out)
     return GradientSet(**{k: v.cpu().numpy() for k, v in out.items()})
+
+
+def contribution_scores(scene, cams, settings: TrainSettings | None = None, cache_keys=None, *,
+                        device=None) -> np.ndarray:
+    """Per-Gaussian pruning statistic of the joint stage (optim.py:519-533):
+    max over views and fragments of ``max_c(colour) * alpha / (1 + W_G)``.
+    ``cache_keys[i]`` is the frozen-cache key of ``cams[i]`` (the trainer
+    passes the view index).  Returns float64 NumPy scores (n_gaussians,)."""
+    settings = settings or TrainSettings()
+    dev = torch.device(device or "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    ng = _count(scene.gaussians.pos)
+    if ng == 0 or not settings.gaussians_enabled:
+        return np.zeros(ng)
+    ds = DeviceScene(scene, dev, keep_source=True)
+    L = _lib.lib()
+    scores = torch.zeros(ng, dtype=torch.float32, device=dev)
+    st_c = settings_struct(_pass_settings(settings, with_geometry=False))
+    status = torch.zeros(3, dtype=torch.int64, device=dev)
+    cap = max(1 << 20, 8 * ng)
+    for i, cam in enumerate(cams):
+        key = cache_keys[i] if cache_keys is not None else None
+        fr = render_training(scene, cam, settings, cache_key=key, to_numpy=False, device=dev, device_scene=ds)
+        cam_c = camera_struct(cam)
+        stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        for _ in range(3):
+            nbytes = L.ges_backward_workspace_bytes(C.byref(ds.c), C.byref(cam_c), C.byref(st_c), cap)
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            trial = scores.clone()
+            _lib.check(L.ges_gaussian_contributions(C.byref(ds.c), C.byref(ds.src), C.byref(cam_c), C.byref(st_c),
+                                                    C.c_void_p(fr.tape["surfel_depth"].data_ptr()),
+                                                    C.c_void_p(fr.gauss_weight.contiguous().data_ptr()),
+                                                    C.c_void_p(trial.data_ptr()), C.c_void_p(ws.data_ptr()), nbytes,
+                                                    cap, C.c_void_p(status.data_ptr()), stream),
+                       "gaussian contributions")
+            st = status.cpu()
+            if not int(st[2] & 0xFFFFFFFF):
+                scores = trial
+                break
+            cap = max(cap, int(int(st[1]) * 1.25) + 1024)
+        else:
+            raise RuntimeError("tile pair lists overflowed repeatedly")
+    return scores.double().cpu().numpy()

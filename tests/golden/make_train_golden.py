@@ -100,6 +100,15 @@ def main():
                 d[k] = getattr(frame, k)
         for k in GRAD_FIELDS:
             d["grad_" + k] = getattr(grads, k)
+        # optim.py:526-533 (Trainer.contribution_scores) for this one view,
+        # from the reference's own fragment tape
+        gt = frame.tape["gauss"]
+        contrib = np.zeros(g.count)
+        if gt.get("count"):
+            denom = (1.0 + frame.gauss_weight).reshape(-1)
+            cmax = gt["colors"].max(axis=1)
+            np.maximum.at(contrib, gt["gid"], cmax[gt["gid"]] * gt["alpha"] / denom[gt["pix"]])
+        d["contrib"] = contrib
         np.savez_compressed(os.path.join(HERE, f"train_{name}.npz"), **d)
         print(name, "gauss frags:", frame.tape["gauss"].get("count", 0),
               "|g_pos|:", float(np.abs(grads.gaussian_pos).max()) if g.count else 0.0)

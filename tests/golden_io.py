@@ -53,6 +53,7 @@ def load_train(name):
     fwd = {k: z[k] for k in ("image", "surfel_color", "surfel_depth", "gauss_color", "gauss_weight",
                              "blend_depth", "blend_normal", "gauss_depth", "gauss_normal") if k in z.files}
     grads = {k: z["grad_" + k] for k in TRAIN_GRADS}
+    grads["contrib"] = z["contrib"]
     return scene, cam, st, z["g_image"], cot, fwd, grads
 
 

@@ -65,6 +65,9 @@ def test_training_step_matches_reference(name):
     for k in TRAIN_GRADS:
         _grad_close(k, getattr(out, k), grads[k])
     out.check_finite()
+    # the joint stage's pruning statistic for this view (optim.py:519-533)
+    sc = TR.contribution_scores(scene, [cam], train_settings(st, TR.TrainSettings), cache_keys=[0])
+    _grad_close("contrib", sc, grads["contrib"], rel=1e-4)
 
 
 def _random_case(seed, kind, ns=60, ng=150, deg=2, res=(96, 80), mip=False):
@@ -98,6 +101,8 @@ def test_training_step_matches_oracle_random(kind, mip, geom):
     out = TR.backward(frame, g_img, **cot)
     for k in TRAIN_GRADS:
         _grad_close(k, getattr(out, k), rout[k])
+    sc = TR.contribution_scores(scene, [cam], train_settings(st, TR.TrainSettings), cache_keys=[1])
+    _grad_close("contrib", sc, rout["contrib"], rel=1e-4)
 
 
 def test_frozen_cache_is_reused_and_translucent_pass_raises():
@@ -136,3 +141,17 @@ def test_training_gradient_descends_loss():
                      gs.sh - lr * 10 * g.gaussian_sh, gs.kind, gs.filter3d)
     l1, _ = loss_and_grad(Scene(scene.surfels, new_g, scene.sh_degree, scene.stage))
     assert l1 < l0
+
+
+def test_contribution_scores_max_over_views():
+    scene, cam0 = _random_case(13, GaussianKind.THREE_D, ns=50, ng=120)
+    cams = [cam0, S.make_camera(96, 80, azim=1.1), S.make_camera(96, 80, azim=2.3, elev=0.5)]
+    so = TR.TrainSettings(frozen_cache={})
+    ref = np.zeros(scene.gaussians.count)
+    for k, c in enumerate(cams):
+        fr = TO.render_training(scene, c, so, cache=so.frozen_cache, cache_key=k)
+        out = TO.backward(scene, c, so, fr, np.zeros((c.height, c.width, 3)))
+        ref = np.maximum(ref, out["contrib"])
+    got = TR.contribution_scores(scene, cams, TR.TrainSettings(frozen_cache={}), cache_keys=[0, 1, 2])
+    assert got.shape == ref.shape and np.count_nonzero(ref) > 10
+    _grad_close("contrib", got, ref, rel=1e-4)

@@ -33,7 +33,7 @@ def test_train_oracle_matches_reference(name):
     for k, v in fwd.items():
         _close_fwd(np.asarray(frame[k]), v)
     out = T.backward(scene, cam, settings, frame, g_img, **cot)
-    for k in TRAIN_GRADS:
+    for k in TRAIN_GRADS + ("contrib",):
         _close_grad(k, out[k], grads[k])
 
 
