@@ -223,6 +223,20 @@ typedef struct ges_gauss_grads {
  * (forward.py:99-103). */
 int ges_surfel_colors(const ges_scene_t *scene, const ges_camera_t *cam, float *rgb, void *stream);
 
+/* Surfel buffers of the frozen pass from the cached z-buffer of the
+ * supersampled camera (training.py:380-392 and :334-346): winner / depth /
+ * normal are (H*grid, W*grid[,3]) device arrays (winner: source ids, -1
+ * uncovered), colors (n_surfels, 3) the view colours (ges_surfel_colors),
+ * background 3 floats on the HOST.  Writes s_color (H,W,3) = box mean of the
+ * sub-samples' colour (background where uncovered), s_depth (H,W) = the
+ * depth of sub-sample (0,0) (the Gaussian gate depth of the late phase) and,
+ * if non-NULL, the blended geometry b_depth (H,W) / b_normal (H,W,3) = box
+ * means of the covered sub-samples' depth / normal. */
+int ges_frozen_surfel_buffers(const int32_t *winner, const float *depth, const float *normal,
+                              const float *colors, int32_t width, int32_t height, int32_t grid,
+                              const float *background, float *s_color, float *s_depth, float *b_depth,
+                              float *b_normal, void *stream);
+
 /* Scratch of ges_backward_gaussians: 16 float64 accumulators and two
  * float4 ray coefficients per Gaussian. */
 size_t ges_backward_scratch_bytes(int64_t n_gaussians);
@@ -239,7 +253,9 @@ size_t ges_backward_workspace_bytes(const ges_scene_t *scene, const ges_camera_t
  * the forward's Gaussian pass was gated with.  `src` must hold the float64
  * source arrays the scene was packed from (the chain rule runs in float64 on
  * them).  any_filter: nonzero iff any filter3d entry is nonzero
- * (primitives.py:113-126 switch the effective scale/opacity on globally). */
+ * (primitives.py:113-126 switch the effective scale/opacity on globally).
+ * The gradient outputs must be zero-initialised: Gaussians without any
+ * contributing fragment are not written. */
 int ges_backward_gaussians(const ges_scene_t *scene, const ges_scene_src_t *src, int32_t any_filter,
                            const ges_camera_t *cam, const ges_settings_t *st, const float *surfel_depth,
                            const float *g_color, const float *g_weight, const float *g_depth,
@@ -263,7 +279,9 @@ int ges_gaussian_contributions(const ges_scene_t *scene, const ges_scene_src_t *
  * training.py:612-629): winner (H*grid, W*grid) int32 source ids (-1 =
  * uncovered) of the cached opaque z-buffer, g_color = dL/dC_s (H,W,3)
  * float32.  Writes g_sh (n_surfels x K x 3) and g_pos (n_surfels x 3)
- * float64; col_scratch holds n_surfels x 3 float64. */
+ * float64 for the surfels that received a colour cotangent (the outputs must
+ * be zero-initialised; others are not written); col_scratch holds
+ * n_surfels x 3 float64. */
 int ges_backward_surfels_frozen(const ges_scene_src_t *src, const ges_camera_t *cam, int32_t grid,
                                 const int32_t *winner, const float *g_color, double *col_scratch,
                                 double *g_sh, double *g_pos, void *stream);

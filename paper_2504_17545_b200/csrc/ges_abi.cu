@@ -402,6 +402,18 @@ int ges_backward_gaussians(const ges_scene_t* sc, const ges_scene_src_t* src, in
     return GES_OK;
 }
 
+int ges_frozen_surfel_buffers(const int32_t* winner, const float* depth, const float* normal, const float* colors,
+                              int32_t width, int32_t height, int32_t grid, const float* background, float* s_color,
+                              float* s_depth, float* b_depth, float* b_normal, void* stream) {
+    if (grid != 1 && grid != 2) return fail(GES_EINVAL, "grid must be 1 or 2");
+    if (width <= 0 || height <= 0) return fail(GES_EINVAL, "image size out of range");
+    if (!winner || !depth || !colors || !background || !s_color || !s_depth || (b_normal && !normal))
+        return fail(GES_EINVAL, "NULL argument");
+    cudaError_t e = launch_frozen_resolve(winner, depth, normal, colors, width, height, grid, background, s_color,
+                                          s_depth, b_depth, b_normal, (cudaStream_t)stream);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "frozen surfel buffers");
+}
+
 int ges_gaussian_contributions(const ges_scene_t* sc, const ges_scene_src_t* src, const ges_camera_t* cam,
                                const ges_settings_t* st, const float* surfel_depth, const float* g_weight,
                                float* scores, void* ws, size_t ws_bytes, int64_t cap_g,

@@ -91,6 +91,9 @@ struct BwdArgs {
 
 cudaError_t launch_surfel_colors(const ges_scene_t& sc, const CamK& cam, float* rgb, cudaStream_t s);
 cudaError_t launch_gauss_bwd(const BwdArgs& a, int g_kind, bool geom, cudaStream_t s);
+cudaError_t launch_frozen_resolve(const int32_t* winner, const float* depth, const float* normal, const float* colors,
+                                  int W, int H, int grid, const float* bg, float* s_color, float* s_depth,
+                                  float* b_depth, float* b_normal, cudaStream_t s);
 cudaError_t launch_gauss_contrib(const BwdArgs& a, int g_kind, cudaStream_t s);
 cudaError_t launch_gauss_finish(const ges_scene_src_t& src, int any_filter, int mip, const CamK& cam,
                                 const double* acc, const ges_gauss_grads_t& out, cudaStream_t s);

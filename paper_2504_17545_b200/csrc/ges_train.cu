@@ -215,15 +215,6 @@ __device__ void write_gauss_grads(const ges_gauss_grads_t& out, int64_t o, int D
     }
 }
 
-__device__ void zero_gauss_grads(const ges_gauss_grads_t& out, int64_t o, int D, int K) {
-    for (int j = 0; j < 3; ++j) out.pos[3 * o + j] = 0.0;
-    for (int j = 0; j < 4; ++j) out.quat[4 * o + j] = 0.0;
-    for (int k = 0; k < D; ++k) out.scale[D * o + k] = 0.0;
-    out.opacity[o] = 0.0;
-    for (int j = 0; j < K * 3; ++j) out.sh[(int64_t)K * 3 * o + j] = 0.0;
-    if (out.screen) out.screen[o] = 0.0;
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- colours
@@ -417,7 +408,7 @@ __global__ void k_gauss3_finish(ges_scene_src_t src, int any_filter, int mip, Ca
     double A[10];
     bool any = false;
     for (int k = 0; k < 10; ++k) { A[k] = acc[i * NACC + k]; any |= A[k] != 0.0; }
-    if (!any) { zero_gauss_grads(out, o, 3, K); return; }
+    if (!any) return;   // no fragments: the (zero-initialised) outputs stay zero
     GSrc g;
     load_gsrc(src, o, any_filter, g);
     const double* W = cam.R;
@@ -572,7 +563,7 @@ __global__ void k_gauss2_finish(ges_scene_src_t src, int any_filter, int mip, Ca
     double B[NACC];
     bool any = false;
     for (int k = 0; k < NACC; ++k) { B[k] = acc[i * NACC + k]; any |= B[k] != 0.0; }
-    if (!any) { zero_gauss_grads(out, o, 2, K); return; }
+    if (!any) return;   // no fragments: the (zero-initialised) outputs stay zero
     GSrc g;
     load_gsrc(src, o, any_filter, g);
     const double* W = cam.R;
@@ -630,16 +621,82 @@ __global__ void k_gauss2_finish(ges_scene_src_t src, int any_filter, int mip, Ca
 }
 
 // ---------------------------------------------------------------- frozen surfels
+// dL/dC_s (base pixel) * 1/grid^2 to every covered sub-sample's winner
+// (training.py:617-625).  One thread per BASE pixel: its grid^2 sub-samples
+// usually share one winner, and so do neighbouring pixels, so equal
+// (winner, value) contributions are first summed per thread, then across the
+// warp's lanes with the same single winner (one float64 atomic per group).
 __global__ void k_frozen_scatter(const int32_t* __restrict__ winner, const float* __restrict__ g_cs, int W, int H,
                                  int grid, double* col) {
-    const int64_t n = (int64_t)W * grid * H * grid;
+    const int64_t n = (int64_t)W * H;
+    const int WW = W * grid;
     const double share = 1.0 / (grid * grid);
-    for (int64_t P = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; P < n; P += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t w = winner[P];
-        if (w < 0) continue;
-        const int64_t X = P % ((int64_t)W * grid), Y = P / ((int64_t)W * grid);
-        const int64_t b = (Y / grid) * W + X / grid;
-        for (int c = 0; c < 3; ++c) atomicAdd(col + 3 * (int64_t)w + c, (double)g_cs[3 * b + c] * share);
+    const unsigned lane = threadIdx.x & 31;
+    for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = b0 + threadIdx.x;
+        int32_t w[4] = {-1, -1, -1, -1};
+        double g[3] = {0.0, 0.0, 0.0};
+        if (b < n) {
+            const int64_t X = b % W, Y = b / W;
+            for (int k = 0; k < grid * grid; ++k)
+                w[k] = winner[(Y * grid + k / grid) * (int64_t)WW + X * grid + k % grid];
+            for (int c = 0; c < 3; ++c) g[c] = (double)g_cs[3 * b + c] * share;
+        }
+        const bool uni = w[0] >= 0 && (grid == 1 || (w[1] == w[0] && w[2] == w[0] && w[3] == w[0]));
+        // lanes whose sub-samples all share one winner: aggregate over the warp
+        const unsigned peers = __match_any_sync(0xffffffffu, uni ? w[0] : -2 - (int)lane);
+        const int leader = __ffs(peers) - 1;
+        double tot[3] = {0.0, 0.0, 0.0};
+        const double m = (double)(grid * grid);
+        for (int src = 0; src < 32; ++src) {
+            const bool mine = (peers >> src) & 1u;
+            for (int c = 0; c < 3; ++c) {
+                const double x = __shfl_sync(0xffffffffu, g[c], src);
+                if (mine) tot[c] += x * m;
+            }
+        }
+        if (uni) {
+            if ((int)lane == leader)
+                for (int c = 0; c < 3; ++c) atomicAdd(col + 3 * (int64_t)w[0] + c, tot[c]);
+        } else {
+            for (int k = 0; k < grid * grid; ++k)
+                if (w[k] >= 0)
+                    for (int c = 0; c < 3; ++c) atomicAdd(col + 3 * (int64_t)w[k] + c, g[c]);
+        }
+    }
+}
+
+// Forward of the frozen surfel pass on the cached z-buffer
+// (training.py:380-392, :334-346): per base pixel the box mean over its
+// grid^2 sub-samples of (winner colour or background), the Gaussian gate depth
+// = sub-sample (0,0) depth, and with geometry the box means of the covered
+// sub-samples' depth and normal (0 where uncovered).
+__global__ void k_frozen_resolve(const int32_t* __restrict__ winner, const float* __restrict__ depth,
+                                 const float* __restrict__ normal, const float* __restrict__ colors, int W, int H,
+                                 int grid, float bg0, float bg1, float bg2, float* s_color, float* s_depth,
+                                 float* b_depth, float* b_normal) {
+    const int64_t n = (int64_t)W * H;
+    const int WW = W * grid;
+    const float inv = 1.0f / (float)(grid * grid);
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t X = b % W, Y = b / W;
+        float c[3] = {0.f, 0.f, 0.f}, d = 0.f, nn[3] = {0.f, 0.f, 0.f};
+        for (int k = 0; k < grid * grid; ++k) {
+            const int64_t P = (Y * grid + k / grid) * (int64_t)WW + X * grid + k % grid;
+            const int32_t w = winner[P];
+            if (w >= 0) {
+                c[0] += __ldg(colors + 3 * (int64_t)w); c[1] += __ldg(colors + 3 * (int64_t)w + 1);
+                c[2] += __ldg(colors + 3 * (int64_t)w + 2);
+                if (b_depth) d += depth[P];
+                if (b_normal) { nn[0] += normal[3 * P]; nn[1] += normal[3 * P + 1]; nn[2] += normal[3 * P + 2]; }
+            } else {
+                c[0] += bg0; c[1] += bg1; c[2] += bg2;
+            }
+            if (k == 0) s_depth[b] = depth[P];
+        }
+        s_color[3 * b] = c[0] * inv; s_color[3 * b + 1] = c[1] * inv; s_color[3 * b + 2] = c[2] * inv;
+        if (b_depth) b_depth[b] = d * inv;
+        if (b_normal) { b_normal[3 * b] = nn[0] * inv; b_normal[3 * b + 1] = nn[1] * inv; b_normal[3 * b + 2] = nn[2] * inv; }
     }
 }
 
@@ -650,11 +707,7 @@ __global__ void k_surfel_sh_bwd(ges_scene_src_t src, CamK cam, const double* __r
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= src.n_surfels) return;
     const double gc[3] = {col[3 * j], col[3 * j + 1], col[3 * j + 2]};
-    if (gc[0] == 0.0 && gc[1] == 0.0 && gc[2] == 0.0) {
-        for (int k = 0; k < K * 3; ++k) g_sh[(int64_t)K * 3 * j + k] = 0.0;
-        for (int k = 0; k < 3; ++k) g_pos[3 * j + k] = 0.0;
-        return;
-    }
+    if (gc[0] == 0.0 && gc[1] == 0.0 && gc[2] == 0.0) return;   // not visible: outputs stay zero
     double p[3] = {src.s_pos[3 * j], src.s_pos[3 * j + 1], src.s_pos[3 * j + 2]};
     double shs[K * 3], gs[K * 3], gp[3];
     for (int k = 0; k < K * 3; ++k) shs[k] = src.s_sh[(int64_t)K * 3 * j + k];
@@ -731,7 +784,7 @@ cudaError_t launch_frozen_bwd(const ges_scene_src_t& src, const CamK& cam, int W
     if (src.n_surfels == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(col, 0, sizeof(double) * 3 * src.n_surfels, s);
     if (e != cudaSuccess) return e;
-    k_frozen_scatter<<<148 * 8, 256, 0, s>>>(winner, g_cs, W, H, grid, col);
+    k_frozen_scatter<<<148 * 16, 256, 0, s>>>(winner, g_cs, W, H, grid, col);
     const unsigned nb = (unsigned)((src.n_surfels + 127) / 128);
     switch (src.sh_degree) {
         case 0: k_surfel_sh_bwd<0><<<nb, 128, 0, s>>>(src, cam, col, g_sh, g_pos); break;
@@ -739,6 +792,14 @@ cudaError_t launch_frozen_bwd(const ges_scene_src_t& src, const CamK& cam, int W
         case 2: k_surfel_sh_bwd<2><<<nb, 128, 0, s>>>(src, cam, col, g_sh, g_pos); break;
         default: k_surfel_sh_bwd<3><<<nb, 128, 0, s>>>(src, cam, col, g_sh, g_pos); break;
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_frozen_resolve(const int32_t* winner, const float* depth, const float* normal, const float* colors,
+                                  int W, int H, int grid, const float* bg, float* s_color, float* s_depth,
+                                  float* b_depth, float* b_normal, cudaStream_t s) {
+    k_frozen_resolve<<<148 * 16, 256, 0, s>>>(winner, depth, normal, colors, W, H, grid, bg[0], bg[1], bg[2], s_color,
+                                              s_depth, b_depth, b_normal);
     return cudaGetLastError();
 }
 

@@ -172,18 +172,19 @@ def render_training(scene, cam, settings: TrainSettings | None = None, cache_key
         colors = torch.empty((ns, 3), dtype=torch.float32, device=dev)
         _lib.check(L.ges_surfel_colors(C.byref(ds.c), C.byref(camera_struct(cam)), C.c_void_p(colors.data_ptr()),
                                        stream), "surfel colours")
-        covered = winner >= 0
-        chi = bg.expand(H * grid * W * grid, 3).clone()
-        chi[covered] = colors[winner[covered].long()]
-        surfel_color = chi.view(H, grid, W, grid, 3).mean(dim=(1, 3))
-        # late phase (all w = 255 >= 30): the Gaussian gate uses the front hit depth
-        surfel_depth = entry["depth"].view(H * grid, W * grid)[::grid, ::grid].contiguous()
+        # box-mean colour, gate depth (late phase, all w = 255 >= 30: the front
+        # hit of sub-sample 0) and blended geometry in one kernel
+        f32 = dict(dtype=torch.float32, device=dev)
+        surfel_color = torch.empty((H, W, 3), **f32)
+        surfel_depth = torch.empty((H, W), **f32)
         if geom:
-            zero = torch.zeros((), dtype=torch.float32, device=dev)
-            bd = torch.where(covered, entry["depth"], zero)
-            bn = torch.where(covered[:, None], entry["normal"], zero)
-            blend_depth = bd.view(H, grid, W, grid).mean(dim=(1, 3))
-            blend_normal = bn.view(H, grid, W, grid, 3).mean(dim=(1, 3))
+            blend_depth = torch.empty((H, W), **f32)
+            blend_normal = torch.empty((H, W, 3), **f32)
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        bgh = (C.c_float * 3)(*[float(v) for v in settings.background])
+        _lib.check(L.ges_frozen_surfel_buffers(ptr(winner), ptr(entry["depth"]), ptr(entry["normal"]), ptr(colors),
+                                               W, H, grid, C.cast(bgh, C.c_void_p), ptr(surfel_color), ptr(surfel_depth),
+                                               ptr(blend_depth), ptr(blend_normal), stream), "frozen surfel buffers")
     else:
         surfel_color = bg.expand(H, W, 3).clone()
         surfel_depth = torch.full((H, W), float("inf"), dtype=torch.float32, device=dev)
