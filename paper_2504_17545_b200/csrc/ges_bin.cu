@@ -168,14 +168,14 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
 __global__ void __launch_bounds__(256) k_fill(const SurfRec* __restrict__ srec, int64_t ns, BinPass ps,
                                               const float4* __restrict__ grec, int64_t ng, int g_kind, BinPass pg,
                                               SlabMap sm) {
-    const int64_t sblocks = (ns + blockDim.x - 1) / blockDim.x;
+    const unsigned sblocks = (unsigned)((ns + 255) >> 8);   // blockDim.x == 256
     if (blockIdx.x < sblocks) {
         const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
         const bool live = i < ns;
         const float4 r3 = live ? __ldg(&srec[i].r3) : make_float4(0.f, 0.f, 0.f, 0.f);
         fill_one(live, (uint32_t)i, __float_as_uint(r3.y), __float_as_uint(r3.z), sm.slab(r3.x), ps);
     } else {
-        const int64_t j = (blockIdx.x - sblocks) * (int64_t)blockDim.x + threadIdx.x;
+        const int64_t j = (int64_t)(blockIdx.x - sblocks) * 256 + threadIdx.x;
         const bool live = j < ng;
         uint32_t sx = 0, sy = 0;
         float key = 0.f;
