@@ -99,7 +99,10 @@ cudaError_t launch_scan(const BinPass& s, const BinPass& g, ges_frame_status_t* 
 // atomic.  The atomics of up to FILL_R rounds are issued back to back (their
 // results parked in registers) before any slot is written, so their L2 round
 // trips overlap instead of serialising; longer ranges finish in a plain loop.
-constexpr int FILL_R = 8;
+#ifndef GES_FILL_R
+#define GES_FILL_R 4
+#endif
+constexpr int FILL_R = GES_FILL_R;
 
 __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, uint32_t sy, int slab,
                                          const BinPass& p) {
