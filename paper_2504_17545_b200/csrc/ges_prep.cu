@@ -9,6 +9,10 @@
 #include "ges_launch.h"
 #include "ges_sh.cuh"
 
+#ifndef GES_PREP_MINB
+#define GES_PREP_MINB 3   // resident 256-thread blocks per SM of the preprocess kernels
+#endif
+
 namespace ges {
 
 CamK make_cam(const ges_camera_t& c, int scale) {
@@ -210,7 +214,7 @@ cudaError_t launch_pack(const ges_scene_src_t& src, const ges_scene_t& dst, cuda
 // ---------------------------------------------------------------- K1 surfels
 // forward.py:148-158 (frames, colour, n_vis, cull, bounds, ranges) for one surfel.
 template <int DEG>
-__global__ void __launch_bounds__(256, 4) k_surfel_prep(ges_scene_t sc, CamK cam, Grid g, PrepOut o) {
+__global__ void __launch_bounds__(256, GES_PREP_MINB) k_surfel_prep(ges_scene_t sc, CamK cam, Grid g, PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_surfels;
     if (!valid_thread) i = sc.n_surfels - 1;   // idle lanes still join the warp-wide count
@@ -270,7 +274,7 @@ struct GaussCfg {
 
 // 3D EWA: geometry.py:114-132 + forward.py:252-290.
 template <int DEG>
-__global__ void __launch_bounds__(256, 4) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+__global__ void __launch_bounds__(256, GES_PREP_MINB) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_gaussians;
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(256, 4) k_gauss3_prep(ges_scene_t sc, CamK cam
 
 // Planar 2D Gaussians: forward.py:324-351 (+ filters.py:84-109 when mip).
 template <int DEG>
-__global__ void __launch_bounds__(256, 4) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+__global__ void __launch_bounds__(256, GES_PREP_MINB) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_gaussians;
