@@ -38,6 +38,8 @@ def parse():
     p.add_argument("--ss", type=int, default=1, choices=[1, 4])
     p.add_argument("--streams", type=int, default=8, help="CUDA streams pipelining the views of a step")
     p.add_argument("--layers", default="full", choices=["full", "surfels_only", "gaussians_only"])
+    p.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                   help="N > 1: frames to rank 0 through peer memory written by the tile kernel, or NCCL gather")
     p.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
@@ -99,6 +101,9 @@ def base_config(cfg, per_rank, world, ss):
             "resolution": [w, h] if cfg != 4 else "480x270, 960x540, 1920x1080, 3840x2160",
             "supersample": ss, "parallelism": f"views x{world}", "streams_per_gpu": ARGS.streams,
             "cuda_graph": not ARGS.no_graph, "layers": ARGS.layers,
+            "frame_gather": ("none (N=1)" if world == 1 else
+                             "peer: tile kernel writes RGBA8 frames into rank 0 over NVLink (CUDA IPC)"
+                             if ARGS.gather == "peer" else "NCCL gather of RGBA8 frames"),
             "scene": "seeded synthetic (SURVEY 8(d), seed 0)", "l2": l2}
 
 
@@ -223,7 +228,7 @@ def run_gpu(args, rank, world, local_rank):
 
     import paper_2504_17545_b200 as G
     from paper_2504_17545_b200 import _lib
-    from paper_2504_17545_b200.multiview import ViewBatchRenderer, gather_frames
+    from paper_2504_17545_b200.multiview import PeerFrameGather, ViewBatchRenderer, gather_frames
     from paper_2504_17545_b200.renderer import camera_struct, settings_struct
 
     dev = torch.device("cuda", local_rank)
@@ -239,9 +244,15 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.synchronize()
     upload_ms = (time.perf_counter() - t0) * 1e3
     rend = G.Renderer(dev)
-    # B_alg outputs (image fp32, depth, winner) + the RGBA8 send buffer of the gather (N > 1)
-    want = ("image", "s_depth", "s_winner") + (("image_rgba8",) if world > 1 else ())
-    vb = ViewBatchRenderer(rend, ds, cams, settings, want=want, streams=args.streams)
+    # B_alg outputs (image fp32, depth, winner) + the RGBA8 frames of the gather (N > 1): with
+    # --gather peer the tile kernel writes them straight into rank 0's batch over NVLink
+    same_res = len({(int(c.height), int(c.width)) for c in cams}) == 1
+    sink = None
+    if world > 1 and args.gather == "peer" and same_res:
+        sink = PeerFrameGather(per_rank, int(cams[0].height), int(cams[0].width), dst=0, device=dev)
+    want = ("image", "s_depth", "s_winner") + (("image_rgba8",) if world > 1 and sink is None else ())
+    vb = ViewBatchRenderer(rend, ds, cams, settings, want=want, streams=args.streams,
+                           rgba_out=sink.slots if sink is not None else None)
     # size every workspace's pair lists from a checked frame of every view
     for r in vb.pool:
         for c, fr in zip(vb.cams, vb.frames):
@@ -251,7 +262,9 @@ def run_gpu(args, rank, world, local_rank):
 
     def step():
         vb.render(check=False)
-        if world > 1 and torch.is_tensor(vb.rgba):
+        if sink is not None:
+            sink.fence()
+        elif world > 1 and torch.is_tensor(vb.rgba):
             gather_frames(vb.rgba, dst=0)
 
     if args.profile_only:

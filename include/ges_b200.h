@@ -192,6 +192,19 @@ int ges_render_views_host(const ges_scene_t *scene, const ges_camera_t *host_cam
                           void *image_dev, ges_frame_status_t *status_dev, void *const *streams,
                           void *copy_stream);
 
+/* Peer frame buffers for the multi-GPU frame gather without a collective
+ * (SURVEY 8(e)): the destination rank allocates one device buffer and
+ * exports a CUDA IPC handle (64 bytes, written to ipc_handle); every other
+ * rank maps it on its own device (peer access over NVLink enabled) and
+ * passes slices of it as ges_outputs_t::image_rgba8, so the tile kernel's
+ * RGBA8 stores land in the destination GPU's memory while it renders.
+ * ges_peer_open must run on the device given (the caller's current device
+ * is restored). */
+int ges_peer_alloc(size_t bytes, void **dev_ptr, void *ipc_handle);
+int ges_peer_free(void *dev_ptr);
+int ges_peer_open(const void *ipc_handle, int32_t device, void **dev_ptr);
+int ges_peer_close(void *dev_ptr);
+
 /* Tile-kernel work counters (16 x u64), then reset.  All zero unless the
  * library was built with -DGES_STATS (tuning builds only; synchronous). */
 int ges_debug_stats(uint64_t *out16);

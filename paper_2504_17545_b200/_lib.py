@@ -25,7 +25,7 @@ EXPORTS = ("ges_abi_version", "ges_last_error", "ges_scene_bytes", "ges_scene_pa
            "ges_render_views_host", "ges_debug_stats", "ges_surfel_colors",
            "ges_backward_scratch_bytes", "ges_backward_workspace_bytes", "ges_backward_gaussians",
            "ges_backward_surfels_frozen", "ges_gaussian_contributions",
-           "ges_frozen_surfel_buffers")
+           "ges_frozen_surfel_buffers", "ges_peer_alloc", "ges_peer_free", "ges_peer_open", "ges_peer_close")
 
 
 class Camera(C.Structure):
@@ -113,6 +113,10 @@ def lib():
                                                            C.c_void_p, C.c_size_t, C.c_int64, C.c_void_p,
                                                            C.c_void_p])
     sig["ges_backward_surfels_frozen"] = (C.c_int, [P(SceneSrc), P(Camera), C.c_int32] + [C.c_void_p] * 6)
+    sig["ges_peer_alloc"] = (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p), C.c_void_p])
+    sig["ges_peer_free"] = (C.c_int, [C.c_void_p])
+    sig["ges_peer_open"] = (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)])
+    sig["ges_peer_close"] = (C.c_int, [C.c_void_p])
     sig["ges_frozen_surfel_buffers"] = (C.c_int, [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p] * 6)
     sig["ges_gaussian_contributions"] = (C.c_int, [P(Scene), P(SceneSrc), P(Camera), P(Settings)] + [C.c_void_p] * 4
                                          + [C.c_size_t, C.c_int64, C.c_void_p, C.c_void_p])

@@ -3,6 +3,7 @@
 //   memset -> K1 surfel prep(+count) -> K4 Gaussian prep(+count) -> scan -> fill -> fused tile kernel
 // Every call is stream-ordered and capturable in a CUDA graph (no host sync).
 #include <stdio.h>
+#include <string.h>
 
 #include <string>
 
@@ -471,6 +472,44 @@ int ges_backward_surfels_frozen(const ges_scene_src_t* src, const ges_camera_t* 
     cudaError_t e = launch_frozen_bwd(*src, make_cam(*cam, 1), cam->width, cam->height, grid, winner, g_color, col,
                                       g_sh, g_pos, (cudaStream_t)stream);
     return e == cudaSuccess ? GES_OK : cuda_fail(e, "frozen surfel backward");
+}
+
+int ges_peer_alloc(size_t bytes, void** dev_ptr, void* ipc_handle) {
+    if (!dev_ptr || !ipc_handle || bytes == 0) return fail(GES_EINVAL, "bad peer_alloc arguments");
+    cudaError_t e = cudaMalloc(dev_ptr, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "peer buffer cudaMalloc");
+    cudaIpcMemHandle_t h;
+    if ((e = cudaIpcGetMemHandle(&h, *dev_ptr)) != cudaSuccess) {
+        cudaFree(*dev_ptr);
+        *dev_ptr = nullptr;
+        return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    memcpy(ipc_handle, &h, sizeof(h));
+    return GES_OK;
+}
+
+int ges_peer_free(void* dev_ptr) {
+    cudaError_t e = cudaFree(dev_ptr);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "peer buffer cudaFree");
+}
+
+int ges_peer_open(const void* ipc_handle, int32_t device, void** dev_ptr) {
+    if (!ipc_handle || !dev_ptr) return fail(GES_EINVAL, "bad peer_open arguments");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    cudaSetDevice(prev);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+int ges_peer_close(void* dev_ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
 int ges_debug_stats(uint64_t* out16) {

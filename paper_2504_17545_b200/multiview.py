@@ -4,12 +4,21 @@ Views are independent units (``render`` is a pure function of scene and
 camera, forward.py:403); the reference's multi-view callers loop over them
 (metrics.py:60-66, cli.py:165-168).  Here each rank holds a full scene
 replica, renders a contiguous block of views, and the only inter-GPU
-traffic is one frame gather to the destination rank over NCCL (NVLink),
-of RGBA8 frames the tile kernel writes straight into the send buffer.
+traffic is the frame gather to the destination rank.  Two forms:
+
+* ``PeerFrameGather`` (default for the multi-GPU bench): the destination
+  rank exports one device buffer through CUDA IPC; every rank's tile kernel
+  writes its RGBA8 frames straight into its slice of that buffer over NVLink
+  while it renders, so the transfer overlaps the tile work and no collective
+  moves frames; a one-word all-reduce per step orders the writes before the
+  destination reads them.
+* ``gather_frames``: the plain NCCL ``gather`` of per-rank send buffers
+  (baseline, also used on CPU/gloo).
 """
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 
 import torch
@@ -38,6 +47,93 @@ def gather_frames(local: torch.Tensor, dst: int = 0, group=None):
     return None
 
 
+class DevicePointer:
+    """A raw device address with the ``data_ptr()`` the renderer's output
+    binding reads (slices of a peer buffer are not torch allocations)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr, self.nbytes = int(ptr), int(nbytes)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
+class _CudaArray:
+    """``__cuda_array_interface__`` view of a device buffer (torch.as_tensor)."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class PeerFrameGather:
+    """Frame gather through peer memory (SURVEY 8(e) exchange step, fused with
+    the rendering): ``dst`` allocates the (world * V, H, W, 4) RGBA8 batch and
+    shares it by CUDA IPC; rank r's views go to rows [r*V, (r+1)*V).  Pass
+    ``slots`` to ``ViewBatchRenderer(rgba_out=...)``; after each step call
+    ``fence()`` on every rank; ``frames`` (dst only) is the gathered batch."""
+
+    def __init__(self, frames_per_rank: int, height: int, width: int, *, dst: int = 0, group=None, device=None):
+        from . import _lib
+        self.L = _lib.lib()
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.dst = dst
+        self.device = torch.device(device or "cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.frame_bytes = height * width * 4
+        V = frames_per_rank
+        total = self.world * V * self.frame_bytes
+        handle = None
+        self._owned = self._opened = None
+        if self.rank == dst:
+            ptr = C.c_void_p()
+            hbuf = (C.c_char * 64)()
+            _lib.check(self.L.ges_peer_alloc(total, C.byref(ptr), hbuf), "peer buffer")
+            self._owned = ptr.value
+            handle = bytes(hbuf)
+        if self.world > 1:
+            obj = [handle]
+            dist.broadcast_object_list(obj, src=dst, group=group)
+            handle = obj[0]
+        if self.rank == dst:
+            base = self._owned
+        else:
+            ptr = C.c_void_p()
+            _lib.check(self.L.ges_peer_open(handle, self.device.index, C.byref(ptr)), "peer buffer open")
+            self._opened = base = ptr.value
+        self.base = base
+        first = self.rank * V * self.frame_bytes
+        self.slots = [DevicePointer(base + first + k * self.frame_bytes, self.frame_bytes) for k in range(V)]
+        self.frames = (torch.as_tensor(_CudaArray(base, (self.world * V, height, width, 4)), device=self.device)
+                       if self.rank == dst else None)
+        self._flag = torch.zeros(1, device=self.device) if self.world > 1 else None
+
+    def fence(self):
+        """Order every rank's frame writes of this step before the
+        destination's later work: one stream-ordered one-word all-reduce with
+        NCCL (a rank's all-reduce starts only after its render kernels have
+        finished); host synchronisation + barrier with other backends."""
+        if self.world == 1:
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.current_stream(self.device).synchronize()
+            dist.barrier(group=self.group)
+
+    def close(self):
+        if self._opened:
+            self.L.ges_peer_close(C.c_void_p(self._opened))
+            self._opened = None
+        if self._owned:
+            torch.cuda.synchronize(self.device)
+            self.frames = None
+            self.L.ges_peer_free(C.c_void_p(self._owned))
+            self._owned = None
+
+
 class ViewBatchRenderer:
     """Renders a batch of views of one packed scene, asynchronously on the
     current stream, into preallocated outputs: a (V, H, W, 4) RGBA8 send
@@ -45,10 +141,13 @@ class ViewBatchRenderer:
     otherwise, e.g. the multi-scale Mip views), plus any other requested
     buffers (fp32 image, depth, winner ...)."""
 
-    def __init__(self, renderer, scene, cams, settings, *, want=("image_rgba8",), streams: int = 1):
+    def __init__(self, renderer, scene, cams, settings, *, want=("image_rgba8",), streams: int = 1,
+                 rgba_out=None):
         """``streams`` > 1 pipelines consecutive views on that many CUDA
         streams, each with its own frame workspace, so one view's
-        preprocessing/binning overlaps another view's tile kernel."""
+        preprocessing/binning overlaps another view's tile kernel.
+        ``rgba_out``: per-view RGBA8 destinations (e.g.
+        ``PeerFrameGather.slots``) instead of a local send buffer."""
         self.r = renderer
         self.pool = [renderer] + [type(renderer)(renderer.device) for _ in range(max(streams, 1) - 1)]
         self.streams = [None] + [torch.cuda.Stream(renderer.device) for _ in range(max(streams, 1) - 1)]
@@ -58,7 +157,11 @@ class ViewBatchRenderer:
         shapes = {(int(c.height), int(c.width)) for c in self.cams}
         dev = renderer.device
         self.frames = []
-        if len(shapes) == 1:
+        if rgba_out is not None:
+            if len(rgba_out) != len(self.cams):
+                raise ValueError("one RGBA8 destination per view")
+            self.rgba = bufs = list(rgba_out)
+        elif len(shapes) == 1:
             H, W = shapes.pop()
             self.rgba = torch.empty((len(self.cams), H, W, 4), dtype=torch.uint8, device=dev)
             bufs = list(self.rgba.unbind(0))
