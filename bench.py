@@ -380,8 +380,11 @@ def run_gpu(args, rank, world, local_rank):
             else:
                 # fp32 Gaussian sums may differ in the last bit between renders (atomic list
                 # order), which can move an 8-bit rounding by one step
-                dif = (host[0].int() - vb.rgba[0].cpu().int()).abs().max().item()
-                assert dif <= 1, f"e2e RGBA8 frame differs from device render by {dif}"
+                dev_rgba = (vb.rgba[0] if torch.is_tensor(vb.rgba[0]) else
+                            sink.frames[0] if sink is not None and sink.frames is not None else None)
+                if dev_rgba is not None:   # (ranks > 0 of the peer gather hold no local frame copy)
+                    dif = (host[0].int() - dev_rgba.cpu().int()).abs().max().item()
+                    assert dif <= 1, f"e2e RGBA8 frame differs from device render by {dif}"
             return per_rank * world * args.steps / e_el, host[0].numel() * host.element_size() * per_rank
 
         # fp32 frames saturate PCIe with one render stream (more streams only contend)
@@ -459,9 +462,17 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    if "GES_BENCH_DEVICE" in os.environ:
+        # functional test of the N > 1 code path on a one-GPU box (all ranks on one
+        # device, gloo): not a measurement
+        local_rank = int(os.environ["GES_BENCH_DEVICE"])
     if world > 1:
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("GES_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_gpu(args, rank, world, local_rank)
     finally:
