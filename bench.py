@@ -422,9 +422,21 @@ def run_gpu(args, rank, world, local_rank):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = balg / (frame_ms / 1e3) / 1e9
     traffic = None
+    issue = None
     tp = os.path.join(ROOT, "profiles", f"traffic_config{cfg}.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_frame")
+    if os.path.exists(tp) and args.ss == 1 and args.layers == "full":
+        prof = json.load(open(tp))
+        traffic = prof.get("dram_bytes_per_frame")
+        wi = prof.get("warp_instructions_per_frame")
+        if wi:
+            # instruction-issue view of the same frame: warp-instructions per frame (ncu, profiles/)
+            # x frames/s per GPU against 148 SMs x 4 schedulers x the SM clock
+            sm_mhz = clk.summary().get("sm_mhz")
+            issue_peak = 148 * 4 * sm_mhz * 1e6 if sm_mhz else None
+            if issue_peak:
+                ach = wi * fps / world
+                issue = {"warp_instructions_per_frame": wi, "achieved_per_s": ach, "peak_per_s": issue_peak,
+                         "frac": ach / issue_peak, "source": "profiles/" + os.path.basename(tp)}
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -438,6 +450,7 @@ def run_gpu(args, rank, world, local_rank):
                      "note": "achieved = B_alg / isolated frame time (single stream, ges_render_profiled); "
                              "achieved_pipelined = B_alg x frames/s per GPU of the multi-stream step. The tile "
                              "kernel is issue/latency-bound, not HBM-bound (profiles/README.md)",
+                     "issue": issue,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                      "phase_ms": phase, "dominant": max(phase, key=phase.get)},
         "cpu_baseline": cpu,
