@@ -9,14 +9,20 @@ device-native engine is :class:`Renderer` / :class:`DeviceScene`.
 from .forward import (GaussianBuffers, RenderResult, RenderSettings, SurfelBuffers,
                       accumulate_gaussians, composite, rasterize_surfels, render,
                       smooth_geometry)
-from .renderer import DeviceScene, Frame, Renderer, default_renderer
+from .renderer import SCENE_CACHE, DeviceScene, Frame, Renderer, default_renderer
 from .types import (Camera, GaussianKind, GaussianSet, Scene, Stage, SurfelSet, look_at,
                     orbit_cameras)
 
 __version__ = "0.1.0"
 
+
+def invalidate(scene) -> None:
+    """Forget the device copy of ``scene`` after editing its arrays in place
+    (replaced arrays are detected automatically)."""
+    SCENE_CACHE.invalidate(scene)
+
 __all__ = ["render", "rasterize_surfels", "accumulate_gaussians", "composite",
            "smooth_geometry", "RenderSettings", "SurfelBuffers", "GaussianBuffers",
            "RenderResult", "Renderer", "DeviceScene", "Frame", "default_renderer",
            "Camera", "GaussianKind", "GaussianSet", "Scene", "Stage", "SurfelSet",
-           "look_at", "orbit_cameras"]
+           "look_at", "orbit_cameras", "invalidate"]

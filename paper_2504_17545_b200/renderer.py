@@ -175,7 +175,11 @@ class DeviceScene:
 
 
 class _SceneCache:
-    """LRU of packed scenes keyed by the identity of the source arrays."""
+    """LRU of packed scenes keyed by the identity (object, data pointer,
+    shape) of the source arrays.  Replacing an array (``s.pos = new``, as the
+    reference's optimiser does, optim.py:126-135) re-packs automatically;
+    writing INTO a cached array in place is not detected: call
+    ``invalidate(scene)`` (or ``clear()``) after such an edit."""
 
     def __init__(self, size=4):
         self.size = size
@@ -208,6 +212,12 @@ class _SceneCache:
 
     def clear(self):
         self.d.clear()
+
+    def invalidate(self, scene):
+        """Drop the packed copies of ``scene`` (after in-place edits of its arrays)."""
+        key, _ = self._key(scene, None)
+        for k in [k for k in self.d if k[1:] == key[1:]]:
+            del self.d[k]
 
 
 SCENE_CACHE = _SceneCache()

@@ -85,3 +85,19 @@ def test_covering_counts_match_oracle_winners():
         slack += np.bincount(tw[tw >= 0], minlength=60) + int(o.tie.sum())
     assert np.all(np.abs(got - best) <= slack)
     assert got.sum() > 0
+
+
+def test_scene_cache_replaced_and_invalidated_arrays():
+    """Replacing an array re-packs the scene; in-place edits need invalidate()."""
+    rng = np.random.default_rng(8)
+    scene = S.random_scene(rng, 40, 30, degree=1)
+    cam = S.make_camera(48, 40)
+    a = G.render(scene, cam).image
+    scene.surfels.pos = scene.surfels.pos + np.array([0.05, 0.0, 0.0])   # new array: detected
+    b = G.render(scene, cam).image
+    assert not np.array_equal(a, b)
+    np.testing.assert_allclose(b, O.render(scene, cam, None).image, atol=1e-4)
+    scene.gaussians.sh[...] *= 0.0                                        # in place: needs invalidate
+    G.invalidate(scene)
+    c = G.render(scene, cam).image
+    np.testing.assert_allclose(c, O.render(scene, cam, None).image, atol=1e-4)
