@@ -114,6 +114,36 @@ __device__ __forceinline__ void store_rgba8(uint8_t* dst, int64_t pix, float3 c)
     reinterpret_cast<uint32_t*>(dst)[pix] = q(c.x) | (q(c.y) << 8) | (q(c.z) << 16) | (255u << 24);
 }
 
+// Row-pair stores of a thread's two horizontally adjacent pixels (PX = 2):
+// one 8-byte store per pair of words when the first pixel index is even (and
+// both pixels are inside the image), plain stores otherwise.
+__device__ __forceinline__ void put1_pair(float* dst, int64_t pix, float v0, float v1, bool in1) {
+    if (in1 && !(pix & 1)) {
+        *reinterpret_cast<float2*>(dst + pix) = make_float2(v0, v1);
+    } else {
+        dst[pix] = v0;
+        if (in1) dst[pix + 1] = v1;
+    }
+}
+__device__ __forceinline__ void put1_pair(int32_t* dst, int64_t pix, int32_t v0, int32_t v1, bool in1) {
+    if (in1 && !(pix & 1)) {
+        *reinterpret_cast<int2*>(dst + pix) = make_int2(v0, v1);
+    } else {
+        dst[pix] = v0;
+        if (in1) dst[pix + 1] = v1;
+    }
+}
+__device__ __forceinline__ void put3_pair(float* dst, int64_t pix, float3 v0, float3 v1, bool in1) {
+    float* d = dst + 3 * pix;
+    if (in1 && !(pix & 1)) {   // 3 * pix even: the 6 floats start 8-byte aligned
+        float2* d2 = reinterpret_cast<float2*>(d);
+        d2[0] = make_float2(v0.x, v0.y); d2[1] = make_float2(v0.z, v1.x); d2[2] = make_float2(v1.y, v1.z);
+    } else {
+        d[0] = v0.x; d[1] = v0.y; d[2] = v0.z;
+        if (in1) { d[3] = v1.x; d[4] = v1.y; d[5] = v1.z; }
+    }
+}
+
 // Camera-facing plane normal of source surfel `sid` (forward.py:148, :152),
 // from the packed quaternion in float64 like the reference's frames.
 __device__ __forceinline__ float3 surfel_nvis(const TileArgs& a, uint32_t sid) {
@@ -415,8 +445,20 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
             asm volatile("" : "+f"(ds[p]));   // (not rematerialised from best[] in pass 2)
             if (inside_px(p)) {
                 const int64_t pix = pix_of(p);
-                if (a.out.s_depth) a.out.s_depth[pix] = ds[p];
-                if (a.out.s_winner) a.out.s_winner[pix] = cov ? (int32_t)(uint32_t)best[s0] : -1;
+                if constexpr (PX == 2) {   // depth and winner of the row pair in one store each
+                    if (p % 2 == 0) {
+                        const int s1 = s0 + SS;
+                        const bool in1 = inside_px(p + 1), cov1 = best[s1] != ~0ull;
+                        const float d1 = cov1 ? __uint_as_float((uint32_t)(best[s1] >> 32)) : INFINITY;
+                        if (a.out.s_depth) put1_pair(a.out.s_depth, pix, ds[p], d1, in1);
+                        if (a.out.s_winner)
+                            put1_pair(a.out.s_winner, pix, cov ? (int32_t)(uint32_t)best[s0] : -1,
+                                      cov1 ? (int32_t)(uint32_t)best[s1] : -1, in1);
+                    }
+                } else {
+                    if (a.out.s_depth) a.out.s_depth[pix] = ds[p];
+                    if (a.out.s_winner) a.out.s_winner[pix] = cov ? (int32_t)(uint32_t)best[s0] : -1;
+                }
                 if (a.out.s_normal) {
                     const float3 n = cov ? surfel_nvis(a, (uint32_t)best[s0]) : make_float3(0.f, 0.f, 0.f);
                     a.out.s_normal[3 * pix] = n.x; a.out.s_normal[3 * pix + 1] = n.y;
@@ -613,6 +655,37 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
 #pragma unroll
             for (int p = 0; p < NP; ++p) cs[p] = col[p];   // SS == 1: one sample per pixel
         }
+    }
+    if constexpr (PX == 2 && !GEOM) {
+        // row pairs: 8-byte stores (image, colours, weight)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int p0 = 2 * r, p1 = 2 * r + 1;
+            if (!inside_px(p0)) continue;
+            const bool in1 = inside_px(p1);
+            const int64_t pix = pix_of(p0);
+            if constexpr ((MODE & 1) != 0)
+                if (a.out.s_color) put3_pair(a.out.s_color, pix, cs[p0], cs[p1], in1);
+            float3 i0 = cs[p0], i1 = cs[p1];
+            if constexpr ((MODE & 2) != 0) {
+                if (a.out.g_weight) put1_pair(a.out.g_weight, pix, wsum[p0], wsum[p1], in1);
+                if (a.out.g_color)
+                    put3_pair(a.out.g_color, pix, make_float3(cr[p0], cg[p0], cb[p0]),
+                              make_float3(cr[p1], cg[p1], cb[p1]), in1);
+                i0 = im_of(a, cs[p0], wsum[p0], cr[p0], cg[p0], cb[p0]);
+                i1 = im_of(a, cs[p1], wsum[p1], cr[p1], cg[p1], cb[p1]);
+            } else {   // surfels_only (forward.py:407-410): empty Gaussian buffers
+                if (a.out.g_weight) put1_pair(a.out.g_weight, pix, 0.f, 0.f, in1);
+                if (a.out.g_color)
+                    put3_pair(a.out.g_color, pix, make_float3(0.f, 0.f, 0.f), make_float3(0.f, 0.f, 0.f), in1);
+            }
+            if (a.out.image) put3_pair(a.out.image, pix, i0, i1, in1);
+            if (a.out.image_rgba8) {
+                store_rgba8(a.out.image_rgba8, pix, i0);
+                if (in1) store_rgba8(a.out.image_rgba8, pix + 1, i1);
+            }
+        }
+        return;
     }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
