@@ -685,8 +685,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 if (in1) store_rgba8(a.out.image_rgba8, pix + 1, i1);
             }
         }
-        return;
-    }
+    } else {
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         if (!inside_px(p)) continue;
@@ -728,6 +727,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 a.out.g_color[3 * pix] = 0.f; a.out.g_color[3 * pix + 1] = 0.f; a.out.g_color[3 * pix + 2] = 0.f;
             }
         }
+    }
     }
 }
 
