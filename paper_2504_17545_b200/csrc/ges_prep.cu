@@ -272,9 +272,24 @@ struct GaussCfg {
     float eps_value;
 };
 
+// Gaussian preprocess blocks: 128 threads (4 warps) so the warps' shared
+// coefficient slices of sh_color_warp fit the static shared-memory limit.
+constexpr int GPREP_T = 128;
+
+// View colour of this lane's Gaussian (forward.py:99-109) with the warp's
+// coefficient blocks loaded coalesced (sh_color_warp); all lanes call it.
+template <int DEG>
+__device__ __forceinline__ float3 gauss_view_colour(const ges_scene_t& sc, const CamK& cam, d3 p, float* shw) {
+    const d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
+    const double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31u);
+    return sh_color_warp<DEG>(sc.g_sh, i0, sc.n_gaussians, shw + (threadIdx.x >> 5) * sh_warp_floats<DEG>(),
+                              (float)(dv.x * inv), (float)(dv.y * inv), (float)(dv.z * inv));
+}
+
 // 3D EWA: geometry.py:114-132 + forward.py:252-290.
 template <int DEG>
-__global__ void __launch_bounds__(256, GES_PREP_MINB) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+__global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_gaussians;
@@ -327,6 +342,8 @@ __global__ void __launch_bounds__(256, GES_PREP_MINB) k_gauss3_prep(ges_scene_t 
         y1 = clampi(floor(my + ry + 0.5 - 0.5), cam.H);
         valid = x1 >= x0 && y1 >= y0;
     }
+    __shared__ float shw[(GPREP_T / 32) * sh_warp_floats<DEG>()];
+    const float3 col = gauss_view_colour<DEG>(sc, cam, p, shw);
     const float depf = (float)t.z, epsf = cfg.eps_const ? cfg.eps_value : se.w;
     count_tiles(o.bin_count, g, valid, x0, x1, y0, y1, gauss_key(depf, epsf));
     if (!valid_thread) return;
@@ -338,10 +355,6 @@ __global__ void __launch_bounds__(256, GES_PREP_MINB) k_gauss3_prep(ges_scene_t 
         const double L2E = 1.4426950408889634;
         rec.r1 = make_float4((float)(-0.5 * L2E * la), (float)(-L2E * lb), (float)(-0.5 * L2E * lc), (float)sig);
         const float pmin = (float)(-0.5 * L2E * m2max) - 1e-4f;
-        d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
-        double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
-        float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
-                                   (float)(dv.y * inv), (float)(dv.z * inv));
         rec.r2 = make_float4(pmin, col.x, col.y, col.z);
         if (cfg.geom) {   // forward.py:277-284: shortest eff_scale axis, camera-facing
             int k = 0;
@@ -361,7 +374,7 @@ __global__ void __launch_bounds__(256, GES_PREP_MINB) k_gauss3_prep(ges_scene_t 
 
 // Planar 2D Gaussians: forward.py:324-351 (+ filters.py:84-109 when mip).
 template <int DEG>
-__global__ void __launch_bounds__(256, GES_PREP_MINB) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+__global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_gaussians;
@@ -403,16 +416,14 @@ __global__ void __launch_bounds__(256, GES_PREP_MINB) k_gauss2_prep(ges_scene_t 
     double zsup = q.z - rmax * sqrt(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z);
     zsup -= 1e-5 * fabs(zsup) + 1e-6;
     const float gkey = (float)zsup - epsf;
+    __shared__ float shw[(GPREP_T / 32) * sh_warp_floats<DEG>()];
+    const float3 col = gauss_view_colour<DEG>(sc, cam, p, shw);
     count_tiles(o.bin_count, g, valid, x0, x1, y0, y1, gkey);
     if (!valid_thread) return;
     Gauss2Rec rec;
     if (valid) {
         planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
         rec.c = make_float4(gkey, epsf, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)));
-        d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
-        double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
-        float3 col = sh_color<DEG>(sc.g_sh + i * (DEG + 1) * (DEG + 1) * 3, (float)(dv.x * inv),
-                                   (float)(dv.y * inv), (float)(dv.z * inv));
         rec.r3 = make_float4((float)sig, (float)m2max * 1.0001f + 1e-4f, 0.f, 0.f);
         rec.r4 = make_float4(col.x, col.y, col.z, 0.f);
         if (o.aux) {   // k1 = a1.d/s1, k2 = a2.d/s2 of ray_splat_backward (geometry.py:229-252)
@@ -435,13 +446,13 @@ cudaError_t launch_gauss_prep(const ges_scene_t& sc, const CamK& cam, const Grid
                               const ges_settings_t& st, const PrepOut& o, cudaStream_t s) {
     if (sc.n_gaussians == 0) return cudaSuccess;
     GaussCfg cfg{st.mip, st.epsilon_mode == 1, st.with_geometry, st.epsilon_value};
-    unsigned nb = (unsigned)((sc.n_gaussians + 255) / 256);
-#define GES_G(KER)                                                          \
-    switch (sc.sh_degree) {                                                 \
-        case 0: KER<0><<<nb, 256, 0, s>>>(sc, cam, g, cfg, o); break;      \
-        case 1: KER<1><<<nb, 256, 0, s>>>(sc, cam, g, cfg, o); break;      \
-        case 2: KER<2><<<nb, 256, 0, s>>>(sc, cam, g, cfg, o); break;      \
-        default: KER<3><<<nb, 256, 0, s>>>(sc, cam, g, cfg, o); break;     \
+    unsigned nb = (unsigned)((sc.n_gaussians + GPREP_T - 1) / GPREP_T);
+#define GES_G(KER)                                                              \
+    switch (sc.sh_degree) {                                                     \
+        case 0: KER<0><<<nb, GPREP_T, 0, s>>>(sc, cam, g, cfg, o); break;      \
+        case 1: KER<1><<<nb, GPREP_T, 0, s>>>(sc, cam, g, cfg, o); break;      \
+        case 2: KER<2><<<nb, GPREP_T, 0, s>>>(sc, cam, g, cfg, o); break;      \
+        default: KER<3><<<nb, GPREP_T, 0, s>>>(sc, cam, g, cfg, o); break;     \
     }
     if (sc.gaussian_dim == 2) {
         GES_G(k_gauss2_prep)

@@ -6,22 +6,10 @@
 
 namespace ges {
 
-// sh: K x 3 floats, coefficient-major (DC first), for ONE primitive.
+// Colour from the K x 3 coefficients of ONE primitive already in registers.
 template <int DEG>
-__device__ __forceinline__ float3 sh_color(const float* __restrict__ sh, float x, float y, float z) {
+__device__ __forceinline__ float3 sh_color_regs(const float* c, float x, float y, float z) {
     constexpr int K = (DEG + 1) * (DEG + 1);
-    float c[K * 3];
-    if constexpr ((K * 3) % 4 == 0) {
-        const float4* s4 = reinterpret_cast<const float4*>(sh);
-#pragma unroll
-        for (int j = 0; j < K * 3 / 4; ++j) {
-            float4 v = __ldg(s4 + j);
-            c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < K * 3; ++j) c[j] = __ldg(sh + j);
-    }
     float b[K];
     b[0] = 0.28209479177387814f;
     if constexpr (DEG >= 1) {
@@ -54,6 +42,67 @@ __device__ __forceinline__ float3 sh_color(const float* __restrict__ sh, float x
     }
     return make_float3(fminf(fmaxf(0.5f + r, 0.f), 1.f), fminf(fmaxf(0.5f + g, 0.f), 1.f),
                        fminf(fmaxf(0.5f + bl, 0.f), 1.f));
+}
+
+// sh: K x 3 floats, coefficient-major (DC first), for ONE primitive.
+template <int DEG>
+__device__ __forceinline__ float3 sh_color(const float* __restrict__ sh, float x, float y, float z) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    float c[K * 3];
+    if constexpr ((K * 3) % 4 == 0) {
+        const float4* s4 = reinterpret_cast<const float4*>(sh);
+#pragma unroll
+        for (int j = 0; j < K * 3 / 4; ++j) {
+            float4 v = __ldg(s4 + j);
+            c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < K * 3; ++j) c[j] = __ldg(sh + j);
+    }
+    return sh_color_regs<DEG>(c, x, y, z);
+}
+
+// Shared floats per warp for sh_color_warp<DEG>.
+template <int DEG>
+__host__ __device__ constexpr int sh_warp_floats() { return 32 * ((3 * (DEG + 1) * (DEG + 1)) | 1); }
+
+// Warp-cooperative sh_color for the warp's 32 consecutive primitives
+// i0 .. i0+31 (< n): their coefficient blocks are contiguous, so the warp
+// loads them coalesced into its shared slice smw (row stride K*3 | 1 floats:
+// conflict-free column reads), then every lane evaluates its own primitive.
+// Must be called by all 32 lanes.
+template <int DEG>
+__device__ __forceinline__ float3 sh_color_warp(const float* __restrict__ sh, int64_t i0, int64_t n, float* smw,
+                                                float x, float y, float z) {
+    constexpr int K3 = 3 * (DEG + 1) * (DEG + 1), STR = K3 | 1;
+    const int lane = threadIdx.x & 31;
+    const int cnt = n - i0 < 32 ? (int)(n - i0) : 32;
+    const float* base = sh + i0 * K3;
+    if constexpr (K3 % 4 == 0) {   // float4 loads never straddle two primitives
+        const float4* b4 = reinterpret_cast<const float4*>(base);
+#pragma unroll
+        for (int t = lane; t < 8 * K3; t += 32) {
+            const int g = (4 * t) / K3, f = 4 * t - g * K3;
+            if (g < cnt) {
+                const float4 v = __ldg(b4 + t);
+                float* d = smw + g * STR + f;
+                d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int t = lane; t < 32 * K3; t += 32) {
+            const int g = t / K3;
+            if (g < cnt) smw[g * STR + t - g * K3] = __ldg(base + t);
+        }
+    }
+    __syncwarp();
+    float c[K3];
+#pragma unroll
+    for (int j = 0; j < K3; ++j) c[j] = smw[lane * STR + j];
+    __syncwarp();
+    return sh_color_regs<DEG>(c, x, y, z);
 }
 
 __device__ __forceinline__ float3 sh_color_dyn(int deg, const float* __restrict__ sh, float x, float y,
