@@ -686,48 +686,48 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
             }
         }
     } else {
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        if (!inside_px(p)) continue;
-        const int64_t pix = pix_of(p);
-        if constexpr ((MODE & 1) != 0) {
-            if (a.out.s_color) {
-                a.out.s_color[3 * pix] = cs[p].x; a.out.s_color[3 * pix + 1] = cs[p].y;
-                a.out.s_color[3 * pix + 2] = cs[p].z;
-            }
-        }
-        if constexpr ((MODE & 2) != 0) {
-            if (a.out.g_weight) a.out.g_weight[pix] = wsum[p];
-            if (a.out.g_color) {
-                a.out.g_color[3 * pix] = cr[p]; a.out.g_color[3 * pix + 1] = cg[p];
-                a.out.g_color[3 * pix + 2] = cb[p];
-            }
-            if constexpr (GEOM) {
-                if (a.out.g_depth) a.out.g_depth[pix] = dsum[p];
-                if (a.out.g_normal) {
-                    a.out.g_normal[3 * pix] = nx[p]; a.out.g_normal[3 * pix + 1] = ny[p];
-                    a.out.g_normal[3 * pix + 2] = nz[p];
+    #pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            if (!inside_px(p)) continue;
+            const int64_t pix = pix_of(p);
+            if constexpr ((MODE & 1) != 0) {
+                if (a.out.s_color) {
+                    a.out.s_color[3 * pix] = cs[p].x; a.out.s_color[3 * pix + 1] = cs[p].y;
+                    a.out.s_color[3 * pix + 2] = cs[p].z;
                 }
             }
-            if (a.out.image || a.out.image_rgba8) {
-                const float3 im = im_of(a, cs[p], wsum[p], cr[p], cg[p], cb[p]);
+            if constexpr ((MODE & 2) != 0) {
+                if (a.out.g_weight) a.out.g_weight[pix] = wsum[p];
+                if (a.out.g_color) {
+                    a.out.g_color[3 * pix] = cr[p]; a.out.g_color[3 * pix + 1] = cg[p];
+                    a.out.g_color[3 * pix + 2] = cb[p];
+                }
+                if constexpr (GEOM) {
+                    if (a.out.g_depth) a.out.g_depth[pix] = dsum[p];
+                    if (a.out.g_normal) {
+                        a.out.g_normal[3 * pix] = nx[p]; a.out.g_normal[3 * pix + 1] = ny[p];
+                        a.out.g_normal[3 * pix + 2] = nz[p];
+                    }
+                }
+                if (a.out.image || a.out.image_rgba8) {
+                    const float3 im = im_of(a, cs[p], wsum[p], cr[p], cg[p], cb[p]);
+                    if (a.out.image) {
+                        a.out.image[3 * pix] = im.x; a.out.image[3 * pix + 1] = im.y; a.out.image[3 * pix + 2] = im.z;
+                    }
+                    if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, im);
+                }
+            } else {   // surfels_only (forward.py:407-410): empty Gaussian buffers
+                if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, cs[p]);
                 if (a.out.image) {
-                    a.out.image[3 * pix] = im.x; a.out.image[3 * pix + 1] = im.y; a.out.image[3 * pix + 2] = im.z;
+                    a.out.image[3 * pix] = cs[p].x; a.out.image[3 * pix + 1] = cs[p].y;
+                    a.out.image[3 * pix + 2] = cs[p].z;
                 }
-                if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, im);
-            }
-        } else {   // surfels_only (forward.py:407-410): empty Gaussian buffers
-            if (a.out.image_rgba8) store_rgba8(a.out.image_rgba8, pix, cs[p]);
-            if (a.out.image) {
-                a.out.image[3 * pix] = cs[p].x; a.out.image[3 * pix + 1] = cs[p].y;
-                a.out.image[3 * pix + 2] = cs[p].z;
-            }
-            if (a.out.g_weight) a.out.g_weight[pix] = 0.f;
-            if (a.out.g_color) {
-                a.out.g_color[3 * pix] = 0.f; a.out.g_color[3 * pix + 1] = 0.f; a.out.g_color[3 * pix + 2] = 0.f;
+                if (a.out.g_weight) a.out.g_weight[pix] = 0.f;
+                if (a.out.g_color) {
+                    a.out.g_color[3 * pix] = 0.f; a.out.g_color[3 * pix + 1] = 0.f; a.out.g_color[3 * pix + 2] = 0.f;
+                }
             }
         }
-    }
     }
 }
 

@@ -31,9 +31,6 @@ namespace {
 
 constexpr int NACC = 16;   // accumulators per Gaussian (3D uses 10)
 
-__device__ __forceinline__ int span_lo_(uint32_t s) { return (int)(s & 0xFFFFu); }
-__device__ __forceinline__ int span_hi_(uint32_t s) { return (int)(s >> 16); }
-
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -277,8 +274,8 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
             id = a.g_list[e];
             const float4 c = __ldg(reinterpret_cast<const float4*>(a.grec) + (size_t)id * (GK == 2 ? 6 : 4));
             const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
-            live = span_lo_(sxr) - ox <= px0 + 7 && span_hi_(sxr) - ox >= px0 && span_lo_(syr) - oy <= py0 + 3 &&
-                   span_hi_(syr) - oy >= py0 && (GK == 3 ? c.x < wdmax + c.y : !(c.x > wdmax));
+            live = span_lo(sxr) - ox <= px0 + 7 && span_hi(sxr) - ox >= px0 && span_lo(syr) - oy <= py0 + 3 &&
+                   span_hi(syr) - oy >= py0 && (GK == 3 ? c.x < wdmax + c.y : !(c.x > wdmax));
         }
         uint32_t vote = __ballot_sync(0xffffffffu, live);
         while (vote) {
