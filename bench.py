@@ -108,6 +108,16 @@ def base_config(cfg, per_rank, world, ss):
 
 
 # ----------------------------------------------------------------------------- CPU
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_sample(cfg, scene, cam, n_tiles, threads, ss=1):
     """Time the reference algorithm (oracle/ges_oracle.py, float32 like the
     reference default) on a bounded sample: the full per-frame preprocessing
@@ -158,6 +168,7 @@ def run_reference(args, rank, world):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": base_config(cfg, per_rank, world, args.ss),
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
+                             "cpu_model": cpu_model(),
                              "sample": sample, "measured_wall_s": wall},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -405,7 +416,7 @@ def run_gpu(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         fs, wall, nt, tot = cpu_sample(cfg, scene, cams[0], args.cpu_tiles, threads, args.ss)
-        cpu = {"value": 1.0 / fs, "unit": "frames/s", "cores": threads, "kind": "port",
+        cpu = {"value": 1.0 / fs, "unit": "frames/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"oracle/ges_oracle.py (reference algorithm, float32), full per-frame "
                          f"preprocessing + {nt} of {tot} tiles of one view, extrapolated; "
                          f"{threads} tile threads; {wall:.1f} s of CPU work",
