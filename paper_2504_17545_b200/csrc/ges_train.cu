@@ -640,25 +640,29 @@ __global__ void k_frozen_scatter(const int32_t* __restrict__ winner, const float
             for (int c = 0; c < 3; ++c) g[c] = (double)g_cs[3 * b + c] * share;
         }
         const bool uni = w[0] >= 0 && (grid == 1 || (w[1] == w[0] && w[2] == w[0] && w[3] == w[0]));
-        // lanes whose sub-samples all share one winner: aggregate over the warp
-        const unsigned peers = __match_any_sync(0xffffffffu, uni ? w[0] : -2 - (int)lane);
-        const int leader = __ffs(peers) - 1;
-        double tot[3] = {0.0, 0.0, 0.0};
-        const double m = (double)(grid * grid);
-        for (int src = 0; src < 32; ++src) {
-            const bool mine = (peers >> src) & 1u;
-            for (int c = 0; c < 3; ++c) {
-                const double x = __shfl_sync(0xffffffffu, g[c], src);
-                if (mine) tot[c] += x * m;
-            }
-        }
-        if (uni) {
-            if ((int)lane == leader)
-                for (int c = 0; c < 3; ++c) atomicAdd(col + 3 * (int64_t)w[0] + c, tot[c]);
-        } else {
+        if (!uni) {
             for (int k = 0; k < grid * grid; ++k)
                 if (w[k] >= 0)
                     for (int c = 0; c < 3; ++c) atomicAdd(col + 3 * (int64_t)w[k] + c, g[c]);
+        }
+        // lanes whose sub-samples all share one winner: one group per distinct
+        // winner of the warp (usually 1-3), summed with shuffles, one atomic each
+        const double m = (double)(grid * grid);
+        unsigned todo = __ballot_sync(0xffffffffu, uni);
+        while (todo) {
+            const int lead = __ffs(todo) - 1;
+            const int32_t key = __shfl_sync(0xffffffffu, w[0], lead);
+            const bool mine = uni && w[0] == key;
+            todo &= ~__ballot_sync(0xffffffffu, mine);
+            double t[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                t[c] = mine ? g[c] * m : 0.0;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) t[c] += __shfl_xor_sync(0xffffffffu, t[c], o);
+            }
+            if ((int)lane == lead)
+                for (int c = 0; c < 3; ++c) atomicAdd(col + 3 * (int64_t)key + c, t[c]);
         }
     }
 }

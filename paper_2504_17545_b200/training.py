@@ -126,6 +126,8 @@ def _frozen_entry(ds, scene, rc, settings, cache_key, dev):
                                           want=("s_depth", "s_normal", "s_winner"))
         entry = {"winner": fr.s_winner.reshape(-1), "depth": fr.s_depth.reshape(-1),
                  "normal": fr.s_normal.reshape(-1, 3), "_gpu": True}
+    if "covered_any" not in entry:   # once per cached z-buffer, not per step
+        entry["covered_any"] = bool((entry["winner"] >= 0).any())
         if cache_key is not None:
             cache[cache_key] = entry
     return entry
@@ -219,6 +221,7 @@ def render_training(scene, cam, settings: TrainSettings | None = None, cache_key
     frame.tape = {"scene": scene, "cam": cam, "settings": settings, "grid": grid, "late": late,
                   "device_scene": ds, "device": dev, "image": image, "gauss_weight": gw,
                   "surfel_depth": surfel_depth, "winner": winner, "use_surfels": use_surfels,
+                  "covered_any": bool(entry["covered_any"]) if fast else False,
                   "frozen": fast, "gaussians": gaussians, "gaussian_only": gaussian_only}
     return frame
 
@@ -295,7 +298,7 @@ def backward(frame: TrainFrame, g_image, *, g_blend_depth=None, g_blend_normal=N
             cap = max(cap, int(int(st[1]) * 1.25) + 1024)
         else:
             raise RuntimeError("tile pair lists overflowed repeatedly")
-    if tape["frozen"] and bool((tape["winner"] >= 0).any()):
+    if tape["frozen"] and tape["covered_any"]:
         col = torch.empty((ns, 3), **f64)
         _lib.check(L.ges_backward_surfels_frozen(C.byref(ds.src), C.byref(cam_c), int(tape["grid"]),
                                                  C.c_void_p(tape["winner"].data_ptr()),
