@@ -322,102 +322,100 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
             return warp_max(m);
         };
         float wmx = INFINITY;          // max over this warp's samples of the best depth
-        if (lane == 0) sm.wmax[warp] = INFINITY;
         if (threadIdx.x < NSLAB) sm.slab_end[threadIdx.x] = a.sbin.cnt[tile * NSLAB + threadIdx.x];
         __syncthreads();
         const int ox = tx * TP * SS, oy = ty * TP * SS;
         const uint32_t beg = a.sbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
-        uint32_t nid = beg + threadIdx.x < end ? a.s_list[beg + threadIdx.x] : 0u;
+        uint32_t nid = beg + lane < end ? a.s_list[beg + lane] : 0u;
         if constexpr ((MODE & 2) != 0) {
             if (gbeg + threadIdx.x < gend) {
                 const char* gp = static_cast<const char*>(a.grec) + (size_t)gid * (GK == 2 ? sizeof(Gauss2Rec) : sizeof(GaussRec));
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(gp));
             }
         }
-        for (uint32_t base = beg; base < end; base += NB) {
+        // Warp-independent, like pass 2: each warp walks the tile's near-to-far
+        // surfel list 32 entries at a time, culls every entry against ITS patch
+        // from the 16-byte cull record (pixel range; nearest disc depth vs the
+        // warp's current max hit depth), transforms the survivors into its own
+        // shared slots and tests them, and stops at the first slab behind all
+        // of its hits.  No CTA barriers: a warp never waits for the others.
+        constexpr int PW = 8 * G, PH = 4 * G;   // patch size in surfel-pass pixels
+        const int wx0 = ox + (warp & 1) * PW, wy0 = oy + (warp >> 1) * PH;
+        for (uint32_t base = beg; base < end; base += 32) {
             // slabs are near-to-far: stop once the next slab lies behind every hit so far
-            if (slab_floor(sm.slab_end, a.slabs, base - beg, lane) > tile_max(sm)) break;
-            const int nb = min((uint32_t)NB, end - base);
-            const uint32_t id = nid;   // ids of this batch were loaded one batch ahead
-            if (base + NB + threadIdx.x < end) nid = a.s_list[base + NB + threadIdx.x];
-            if ((int)threadIdx.x < nb) {
+            if (slab_floor(sm.slab_end, a.slabs, base - beg, lane) > wmx) break;
+            const uint32_t e = base + lane;
+            const uint32_t id = nid;   // this chunk's ids were loaded one chunk ahead
+            if (e + 32 < end) nid = a.s_list[e + 32];
+            bool live = false;
+            if (e < end) {
                 const SurfRec* r = a.srec + id;
-                const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2), r3 = __ldg(&r->r3);
-                const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
-                float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
-                const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
-                const float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
+                const float4 r3 = __ldg(&r->r3);
                 const uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
-                uint32_t mask = patch_mask<G>(span_lo(sxr) - ox, span_hi(sxr) - ox, span_lo(syr) - oy,
-                                              span_hi(syr) - oy);
-                // hit depth t = nq / den: orient den so that t > 0 <=> den > 0
-                float nq = r0.w, dx_ = r0.y, dy_ = r0.z;
-                if (nq < 0.f) { nq = -nq; d0 = -d0; dx_ = -dx_; dy_ = -dy_; }
-                if (!(nq > 0.f)) mask = 0;
-#pragma unroll
-                for (int w = 0; w < NWARP; ++w)   // already hidden behind warp w's surface
-                    if (r3.x > sm.wmax[w]) mask &= ~(1u << w);
-                // U, V pre-divided by R: coverage becomes U'^2 + V'^2 <= den^2
-                constexpr float IR = 1.0f / 3.3290429691304455f;
-                sm.st[0][threadIdx.x] = make_float4(d0, dx_, dy_, nq);
-                sm.st[1][threadIdx.x] = make_float4(u0 * IR, r1.y * IR, r1.z * IR, v0 * IR);
-                sm.st[2][threadIdx.x] = make_float4(r2.y * IR, r2.z * IR, r3.w, r3.x);   // r3.w: source id
-                sm.zp[threadIdx.x] = zkey_mask(r3.x, mask);
+                live = span_lo(sxr) < wx0 + PW && span_hi(sxr) >= wx0 && span_lo(syr) < wy0 + PH &&
+                       span_hi(syr) >= wy0 && !(r3.x > wmx);
+                if (live) {
+                    const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2);
+                    const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
+                    float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
+                    const float u0 = fmaf(r1.z, fy, fmaf(r1.y, fx, r1.x));
+                    const float v0 = fmaf(r2.z, fy, fmaf(r2.y, fx, r2.x));
+                    // hit depth t = nq / den: orient den so that t > 0 <=> den > 0
+                    float nq = r0.w, dx_ = r0.y, dy_ = r0.z;
+                    if (nq < 0.f) { nq = -nq; d0 = -d0; dx_ = -dx_; dy_ = -dy_; }
+                    live = nq > 0.f;
+                    // U, V pre-divided by R: coverage becomes U'^2 + V'^2 <= den^2
+                    constexpr float IR = 1.0f / 3.3290429691304455f;
+                    const int slot = warp * 32 + lane;
+                    sm.st[0][slot] = make_float4(d0, dx_, dy_, nq);
+                    sm.st[1][slot] = make_float4(u0 * IR, r1.y * IR, r1.z * IR, v0 * IR);
+                    sm.st[2][slot] = make_float4(r2.y * IR, r2.z * IR, r3.w, r3.x);   // r3.w: source id
+                }
             }
+            uint32_t vote = __ballot_sync(0xffffffffu, live);
 #ifdef GES_STATS
-            {
-                const unsigned live = __ballot_sync(0xffffffffu, (int)threadIdx.x < nb && (sm.zp[threadIdx.x] & 0xFFu));
-                if (lane == 0) GES_STAT(2, __popc(live));
-                if (threadIdx.x == 0) { GES_STAT(0, 1); GES_STAT(1, nb); }
-            }
+            if (lane == 0) { GES_STAT(0, 1); GES_STAT(1, min(32u, end - base)); GES_STAT(2, __popc(vote)); }
 #endif
-            __syncthreads();
-            for (int c = 0; c < nb; c += 32) {
-                const int e = c + lane;
-                const uint32_t zp = e < nb ? sm.zp[e] : 0u;
-                const bool want = ((zp >> warp) & 1u) && !(__uint_as_float(zp & ~0xFFu) > wmx);
-                uint32_t vote = __ballot_sync(0xffffffffu, want);
-                if (!vote) continue;     // nothing tested: the patch depth is unchanged
-                while (vote) {
-                    const int j = c + __ffs(vote) - 1;
-                    vote &= vote - 1;
-                    const float4 C = sm.st[2][j];
-                    if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
-                    if (lane == 0) GES_STAT(3, 1);
-                    const float4 A = sm.st[0][j], B = sm.st[1][j];
-                    // den, U, V at the thread's first sample, then stepped by the
-                    // per-sample increments across its G x G block
-                    const float den0 = fmaf(A.z, ly0, fmaf(A.y, lx0, A.x));
-                    const float U0 = fmaf(B.z, ly0, fmaf(B.y, lx0, B.x));
-                    const float V0 = fmaf(C.y, ly0, fmaf(C.x, lx0, B.w));
+            if (!vote) continue;     // nothing tested: the patch depth is unchanged
+            __syncwarp();
+            while (vote) {
+                const int j = warp * 32 + __ffs(vote) - 1;
+                vote &= vote - 1;
+                const float4 C = sm.st[2][j];
+                if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
+                if (lane == 0) GES_STAT(3, 1);
+                const float4 A = sm.st[0][j], B = sm.st[1][j];
+                // den, U, V at the thread's first sample, then stepped by the
+                // per-sample increments across its G x G block
+                const float den0 = fmaf(A.z, ly0, fmaf(A.y, lx0, A.x));
+                const float U0 = fmaf(B.z, ly0, fmaf(B.y, lx0, B.x));
+                const float V0 = fmaf(C.y, ly0, fmaf(C.x, lx0, B.w));
 #pragma unroll
-                    for (int gy = 0; gy < G; ++gy)
+                for (int gy = 0; gy < G; ++gy)
 #pragma unroll
-                        for (int gx = 0; gx < G; ++gx) {
-                            const int s = gy * G + gx;
-                            float den = den0, U = U0, V = V0;
-                            if (gx) { den = fmaf(A.y, (float)gx, den); U = fmaf(B.y, (float)gx, U); V = fmaf(C.x, (float)gx, V); }
-                            if (gy) { den = fmaf(A.z, (float)gy, den); U = fmaf(B.z, (float)gy, U); V = fmaf(C.y, (float)gy, V); }
-                            const float r2 = fmaf(U, U, V * V);
-                            // coverage u^2+v^2 <= R^2, |n.d| > eps|d| and t no later than the
-                            // current best (all multiplied out, den > 0 <=> t > 0); the exact
-                            // t > 0.01 and packed-key comparison run only for candidates
-                            if (den > pe && r2 <= den * den && A.w <= tb[s] * den) {
-                                const float t = A.w * rcp_ftz(den);   // den > 1e-8|d|; 2 ulp: ties are flagged
-                                const unsigned long long key =
-                                    ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
-                                GES_STAT(4, 1);
-                                if (t > NEAR_F && key < best[s]) {
-                                    best[s] = key;
-                                    tb[s] = t * 1.00001f;   // margin-inflated best depth
-                                }
+                    for (int gx = 0; gx < G; ++gx) {
+                        const int s = gy * G + gx;
+                        float den = den0, U = U0, V = V0;
+                        if (gx) { den = fmaf(A.y, (float)gx, den); U = fmaf(B.y, (float)gx, U); V = fmaf(C.x, (float)gx, V); }
+                        if (gy) { den = fmaf(A.z, (float)gy, den); U = fmaf(B.z, (float)gy, U); V = fmaf(C.y, (float)gy, V); }
+                        const float r2 = fmaf(U, U, V * V);
+                        // coverage u^2+v^2 <= R^2, |n.d| > eps|d| and t no later than the
+                        // current best (all multiplied out, den > 0 <=> t > 0); the exact
+                        // t > 0.01 and packed-key comparison run only for candidates
+                        if (den > pe && r2 <= den * den && A.w <= tb[s] * den) {
+                            const float t = A.w * rcp_ftz(den);   // den > 1e-8|d|; 2 ulp: ties are flagged
+                            const unsigned long long key =
+                                ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
+                            GES_STAT(4, 1);
+                            if (t > NEAR_F && key < best[s]) {
+                                best[s] = key;
+                                tb[s] = t * 1.00001f;   // margin-inflated best depth
                             }
                         }
-                }
-                wmx = patch_depth();
+                    }
             }
-            if (lane == 0) sm.wmax[warp] = wmx;
-            __syncthreads();
+            wmx = patch_depth();
+            __syncwarp();   // the slots are rewritten by the next chunk
         }
         // the winners' SH blocks are read at the end (deferred colour): find
         // their packed indices and start pulling them into L2 now, overlapping
