@@ -1,4 +1,5 @@
-// K3 + K6 fused: one CTA per 16x16 base-resolution tile, one thread per pixel.
+// K3 + K6 fused: one CTA (8 warps) per tile -- 16x16 base pixels with one
+// pixel per thread, or 32x32 with a 2x2 pixel block per thread (PX = 2).
 //
 // Pass 1 (forward.py:127-209): every thread keeps, per (sub)sample, the packed
 // key (float_bits(t) << 32 | surfel_id) of the nearest covering surfel in
@@ -11,14 +12,15 @@
 // never leaves the register file, fused with the composite write
 // (forward.py:384-417).
 //
-// Both passes stream the tile's (tile, depth-slab)-binned primitive list
-// through shared memory in batches of 256: one primitive per thread, turned
-// into tile-relative coefficients once, with an 8-bit mask of the warp
-// patches (8x4 pixels) its pixel range overlaps.  Each warp then scans the
-// batch 32 entries at a time, votes which entries can still matter to it
-// (patch overlap, and for surfels: disc not entirely behind every hit of the
-// patch so far; for Gaussians: depth can pass some gate in the patch) and
-// runs the per-pixel test only on those.  Culling never changes results: the
+// Both passes are warp-independent: each warp owns an 8x4-thread patch of
+// the tile and walks the tile's (tile, depth-slab)-binned list itself, 32
+// entries at a time, near to far.  Every lane culls one entry against the
+// warp's patch from its 16-byte cull record (pixel range; surfels: nearest
+// disc depth vs the patch's farthest current hit; Gaussians: depth - eps vs
+// the patch's farthest surfel depth); survivors are transformed into the
+// warp's shared slots and every lane then runs the exact per-pixel test for
+// each; a warp stops at the first slab behind everything it has drawn.  There
+// are no CTA barriers after the prologue.  Culling never changes results: the
 // per-pixel tests are exact and order-independent.
 #include <math.h>
 
@@ -27,7 +29,7 @@
 
 namespace ges {
 
-constexpr int NB = TILE_PX;     // batch = one primitive per thread
+constexpr int NB = TILE_PX;     // threads per CTA (32 shared slots per warp)
 
 // Work counters for tuning (compiled in only with -DGES_STATS; read with
 // ges_debug_stats).  0 surfel batches, 1 surfel entries staged, 2 staged with
@@ -42,53 +44,18 @@ __device__ unsigned long long g_stats[16];
 #endif
 
 struct __align__(16) TileSmem {
-    float4 st[4][NB];           // pass 1: staged surfel coefficients; pass 2: per-warp survivor records
-    uint32_t zp[NB];            // surfels: nearest disc depth with the low byte = warp-patch mask
-    float wmax[NWARP];          // per-warp max depth (surfels: current hits; Gaussians: final)
+    float4 st[4][NB];           // per-warp slots (32 each): pass-1 surfel coefficients, pass-2
+                                // Gaussian records, then the colour tasks
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
     uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
 };
 
 // Lower depth bound of the slab holding relative list position `rel` (slab
 // ends are non-decreasing, so the slab index is the number of ends <= rel:
-// one vote per warp) and the CTA-wide max of the per-warp depths in sm.wmax.
-// Both read shared memory only, so every warp gets the same answer.
+// one vote per 32 slabs); every lane of the warp gets the same answer.
 __device__ __forceinline__ float slab_floor(const uint32_t* ends, const SlabMap& m, uint32_t rel, int lane) {
     return m.lower(slab_of_pos(ends, rel, lane));
 }
-__device__ __forceinline__ float tile_max(const TileSmem& sm) {
-    float m = sm.wmax[0];
-#pragma unroll
-    for (int w = 1; w < NWARP; ++w) m = fmaxf(m, sm.wmax[w]);
-    return m;
-}
-
-// Bitmask of warp patches (8x4 base px each, 2 columns x 4 rows) that the
-// local inclusive range [x0,x1]x[y0,y1] (in units of `ss` subpixels) overlaps.
-template <int SS>
-__device__ __forceinline__ uint32_t patch_mask(int x0, int x1, int y0, int y1) {
-    uint32_t mx = 0, my = 0;
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-        if (x0 <= SS * (c * 8 + 8) - 1 && x1 >= SS * c * 8) mx |= 1u << c;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-        if (y0 <= SS * (r * 4 + 4) - 1 && y1 >= SS * r * 4) my |= 1u << r;
-    uint32_t m = 0;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-        if ((my >> r) & 1u) m |= mx << (2 * r);
-    return m;
-}
-
-// Nearest disc depth and 8-bit patch mask in one word: the depth rounded DOWN
-// to 15 mantissa bits (conservative for culling), the mask in the low byte.
-__device__ __forceinline__ uint32_t zkey_mask(float z, uint32_t mask) {
-    uint32_t b = __float_as_uint(z);
-    if (!(z >= 0.f)) b = __float_as_uint(-3.0e38f);   // negative / NaN: never culled
-    return (b & ~0xFFu) | mask;
-}
-
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
