@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    p.add_argument("--cpu-tiles", type=int, default=512, help="tiles in the CPU sample (about 10 s of CPU work)")
+    p.add_argument("--cpu-tiles", type=int, default=4096, help="tiles in the CPU sample (half the frame, about 10-15 s of CPU work)")
     p.add_argument("--profile-only", action="store_true", help="render a few frames, no JSON (for ncu)")
     return p.parse_args()
 
