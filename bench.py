@@ -259,8 +259,28 @@ def run_gpu(args, rank, world, local_rank):
     # --gather peer the tile kernel writes them straight into rank 0's batch over NVLink
     same_res = len({(int(c.height), int(c.width)) for c in cams}) == 1
     sink = None
+    gather_used = "none (N=1)" if world == 1 else "nccl"
     if world > 1 and args.gather == "peer" and same_res:
-        sink = PeerFrameGather(per_rank, int(cams[0].height), int(cams[0].width), dst=0, device=dev)
+        # every rank agrees on the form: if any rank cannot map rank 0's buffer
+        # (no peer access), all of them fall back to the NCCL gather
+        err = None
+        try:
+            sink = PeerFrameGather(per_rank, int(cams[0].height), int(cams[0].width), dst=0, device=dev)
+            if os.environ.get("GES_BENCH_PEER_FAIL") == str(rank):   # test-only: exercise the fallback
+                raise RuntimeError("peer mapping disabled by GES_BENCH_PEER_FAIL")
+        except RuntimeError as e:
+            err = str(e)
+        ok = torch.tensor([0 if err else 1], device=dev, dtype=torch.int32)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            if sink is not None:
+                sink.close()
+                sink = None
+            if rank == 0:
+                print(f"peer frame gather unavailable ({err or 'on another rank'}); using the NCCL gather",
+                      file=sys.stderr)
+        else:
+            gather_used = "peer"
     want = ("image", "s_depth", "s_winner") + (("image_rgba8",) if world > 1 and sink is None else ())
     vb = ViewBatchRenderer(rend, ds, cams, settings, want=want, streams=args.streams,
                            rgba_out=sink.slots if sink is not None else None)
@@ -452,7 +472,9 @@ def run_gpu(args, rank, world, local_rank):
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": base_config(cfg, per_rank, world, args.ss),
+        "config": {**base_config(cfg, per_rank, world, args.ss),
+                   **({} if gather_used != "nccl" or args.gather == "nccl" else
+                      {"frame_gather": "NCCL gather of RGBA8 frames (peer buffer unavailable)"})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "unit_of_work": "one frame (ges_render: 5 kernels + 2 memsets)",

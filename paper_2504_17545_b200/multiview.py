@@ -39,6 +39,9 @@ def gather_frames(local: torch.Tensor, dst: int = 0, group=None):
         return local
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if local.is_cuda and dist.get_backend(group) != "nccl":   # gloo gathers host tensors only
+        out = gather_frames(local.cpu(), dst, group)
+        return out.to(local.device) if out is not None else None
     if rank == dst:
         out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
         dist.gather(local.contiguous(), gather_list=list(out.unbind(0)), dst=dst, group=group)
@@ -90,13 +93,16 @@ class PeerFrameGather:
         if self.rank == dst:
             ptr = C.c_void_p()
             hbuf = (C.c_char * 64)()
-            _lib.check(self.L.ges_peer_alloc(total, C.byref(ptr), hbuf), "peer buffer")
-            self._owned = ptr.value
-            handle = bytes(hbuf)
-        if self.world > 1:
+            if self.L.ges_peer_alloc(total, C.byref(ptr), hbuf) == 0:
+                self._owned = ptr.value
+                handle = bytes(hbuf)
+        if self.world > 1:   # always reached by every rank, so a failure cannot strand the others
             obj = [handle]
             dist.broadcast_object_list(obj, src=dst, group=group)
             handle = obj[0]
+        if handle is None:
+            raise RuntimeError(f"peer buffer allocation failed on rank {dst}: {self.L.ges_last_error().decode(errors='replace')}"
+                               if self.rank == dst else f"peer buffer allocation failed on rank {dst}")
         if self.rank == dst:
             base = self._owned
         else:
