@@ -16,8 +16,9 @@
 // the tile and walks the tile's (tile, depth-slab)-binned list itself, 32
 // entries at a time, near to far.  Every lane culls one entry against the
 // warp's patch from its 16-byte cull record (pixel range; surfels: nearest
-// disc depth vs the patch's farthest current hit; Gaussians: depth - eps vs
-// the patch's farthest surfel depth); survivors are transformed into the
+// disc depth vs the farthest current hit of the 2 x 2-lane regions of the
+// patch its pixel range overlaps; Gaussians: depth - eps vs the patch's
+// farthest surfel depth); survivors are transformed into the
 // warp's shared slots and every lane then runs the exact per-pixel test for
 // each; a warp stops at the first slab behind everything it has drawn.  There
 // are no CTA barriers after the prologue.  Culling never changes results: the
@@ -46,6 +47,8 @@ __device__ unsigned long long g_stats[16];
 struct __align__(16) TileSmem {
     float4 st[4][NB];           // per-warp slots (32 each): pass-1 surfel coefficients, pass-2
                                 // Gaussian records, then the colour tasks
+    float4 rmax[NWARP][2];      // per warp: max best depth of each of its 4 x 2 regions of
+                                // 2 x 2 lanes (pass-1 culling)
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
     uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
 };
@@ -55,6 +58,35 @@ struct __align__(16) TileSmem {
 // one vote per 32 slabs); every lane of the warp gets the same answer.
 __device__ __forceinline__ float slab_floor(const uint32_t* ends, const SlabMap& m, uint32_t rel, int lane) {
     return m.lower(slab_of_pos(ends, rel, lane));
+}
+// Max of the per-region depth bounds of a warp (4 x 2 regions of 2 x 2 lanes,
+// RW pixels square) over the regions that the pixel range [x0, x1] x [y0, y1]
+// (relative to the patch origin, overlapping the patch) touches.
+template <int RW>
+__device__ __forceinline__ float region_max(const float4* rmax, int x0, int x1, int y0, int y1) {
+    const int c0 = max(x0, 0) / RW, c1 = min(x1, 4 * RW - 1) / RW;
+    const int q0 = max(y0, 0) / RW, q1 = min(y1, 2 * RW - 1) / RW;
+    auto rowmax = [&](const float4& m) {
+        float v = -INFINITY;
+        v = (c0 <= 0) ? fmaxf(v, m.x) : v;
+        v = (c0 <= 1 && c1 >= 1) ? fmaxf(v, m.y) : v;
+        v = (c0 <= 2 && c1 >= 2) ? fmaxf(v, m.z) : v;
+        v = (c1 >= 3) ? fmaxf(v, m.w) : v;
+        return v;
+    };
+    float r = q0 == 0 ? rowmax(rmax[0]) : -INFINITY;
+    if (q1 == 1) r = fmaxf(r, rowmax(rmax[1]));
+    return r;
+}
+// Per-region maxima of v over 2 x 2 lanes (lane = x + 8 y in the warp's 8 x 4
+// lane grid) into rm[4 x 2]; returns the max over the warp.
+__device__ __forceinline__ float region_reduce(float m, float* rm, int lane) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+    if ((lane & 9) == 0) rm[((lane & 7) >> 1) + 4 * (lane >> 4)] = m;
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+    return fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
 }
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -282,12 +314,19 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 tb[gy * G + gx] = in ? INFINITY : 0.f;
             }
         pe = PARALLEL_EPS_F * sqrtf(pe + 1.0f);   // max over the samples of 1e-8 |d|
+        // Depth culling bounds, refreshed after every chunk: the max over each
+        // region of 2 x 2 lanes (one entry of sm.rmax) and over the whole
+        // patch (wmx).  A single uncovered sample keeps its bound at +inf, so
+        // per-region bounds let covered parts of the patch cull entries long
+        // before the whole patch is covered.
+        float* const rm = reinterpret_cast<float*>(sm.rmax[warp]);
         auto patch_depth = [&]() {
             float m = tb[0];
 #pragma unroll
             for (int s = 1; s < NS; ++s) m = fmaxf(m, tb[s]);
-            return warp_max(m);
+            return region_reduce(m, rm, lane);
         };
+        if (lane < 8) rm[lane] = INFINITY;
         float wmx = INFINITY;          // max over this warp's samples of the best depth
         if (threadIdx.x < NSLAB) sm.slab_end[threadIdx.x] = a.sbin.cnt[tile * NSLAB + threadIdx.x];
         __syncthreads();
@@ -321,6 +360,9 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 const uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
                 live = span_lo(sxr) < wx0 + PW && span_hi(sxr) >= wx0 && span_lo(syr) < wy0 + PH &&
                        span_hi(syr) >= wy0 && !(r3.x > wmx);
+                // nearest disc depth vs the regions its pixel range overlaps
+                if (live) live = !(r3.x > region_max<2 * G>(sm.rmax[warp], span_lo(sxr) - wx0, span_hi(sxr) - wx0,
+                                                            span_lo(syr) - wy0, span_hi(syr) - wy0));
                 if (live) {
                     const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2);
                     const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
@@ -351,6 +393,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 const float4 C = sm.st[2][j];
                 if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
                 if (lane == 0) GES_STAT(3, 1);
+                if (lane == 0) GES_STAT(12, wmx == INFINITY);
                 const float4 A = sm.st[0][j], B = sm.st[1][j];
                 // den, U, V at the thread's first sample, then stepped by the
                 // per-sample increments across its G x G block
@@ -366,6 +409,14 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                         if (gx) { den = fmaf(A.y, (float)gx, den); U = fmaf(B.y, (float)gx, U); V = fmaf(C.x, (float)gx, V); }
                         if (gy) { den = fmaf(A.z, (float)gy, den); U = fmaf(B.z, (float)gy, U); V = fmaf(C.y, (float)gy, V); }
                         const float r2 = fmaf(U, U, V * V);
+#ifdef GES_STATS
+                        {
+                            const bool inside = bx + gx / SS < a.W && by + gy / SS < a.H;
+                            const bool cov = den > pe && r2 <= den * den;
+                            if (inside) GES_STAT(cov ? 14 : 13, 1);
+                            if (inside && cov && tb[s] == INFINITY) GES_STAT(15, 1);
+                        }
+#endif
                         // coverage u^2+v^2 <= R^2, |n.d| > eps|d| and t no later than the
                         // current best (all multiplied out, den > 0 <=> t > 0); the exact
                         // t > 0.01 and packed-key comparison run only for candidates

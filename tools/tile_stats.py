@@ -17,7 +17,9 @@ from paper_2504_17545_b200 import _lib, scenes as S  # noqa: E402
 
 NAMES = ["surfel batches", "surfel entries staged", "  with live mask", "surfel warp tests",
          "candidate lanes", "gauss batches", "gauss entries walked (x warps)", "  surviving the warp cull",
-         "gauss warp tests", "contributing lanes", "tiles", "tiles with uncovered px"]
+         "gauss warp tests", "contributing lanes", "tiles", "tiles with uncovered px",
+         "surfel warp tests at wmx=inf", "sample tests: not covered", "sample tests: covered",
+         "  covered, sample still empty"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
