@@ -37,7 +37,7 @@ constexpr int NB = TILE_PX;     // threads per CTA (32 shared slots per warp)
 // a live warp mask, 3 surfel warp tests, 4 candidate lanes, 5 Gaussian
 // batches, 6 Gaussian entries staged, 7 staged with a live mask, 8 Gaussian
 // warp tests, 9 contributing lanes, 10 tiles, 11 tiles with uncovered pixels.
-__device__ unsigned long long g_stats[16];
+__device__ unsigned long long g_stats[20];
 #ifdef GES_STATS
 #define GES_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 #else
@@ -804,7 +804,7 @@ __global__ void k_smooth(const float* __restrict__ sd, const float* __restrict__
 
 int read_stats(unsigned long long* out) {
     if (cudaMemcpyFromSymbol(out, g_stats, sizeof(g_stats)) != cudaSuccess) return 1;
-    unsigned long long z[16] = {};
+    unsigned long long z[20] = {};
     return cudaMemcpyToSymbol(g_stats, z, sizeof(z)) == cudaSuccess ? 0 : 1;
 }
 

@@ -19,7 +19,7 @@ NAMES = ["surfel batches", "surfel entries staged", "  with live mask", "surfel 
          "candidate lanes", "gauss batches", "gauss entries walked (x warps)", "  surviving the warp cull",
          "gauss warp tests", "contributing lanes", "tiles", "tiles with uncovered px",
          "surfel warp tests at wmx=inf", "sample tests: not covered", "sample tests: covered",
-         "  covered, sample still empty"]
+         "  covered, sample still empty", "-", "-", "-", "-"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
@@ -31,7 +31,7 @@ ds = G.DeviceScene(sc)
 r = G.Renderer()
 st = G.RenderSettings(supersample=a.ss)
 fr = r.render(ds, cam, st, check=True)
-buf = (C.c_uint64 * 16)()
+buf = (C.c_uint64 * 20)()
 _lib.lib().ges_debug_stats(buf)            # reset after the sizing render
 fr = r.render(ds, cam, st, check=True)
 torch.cuda.synchronize()
