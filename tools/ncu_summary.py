@@ -114,7 +114,26 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--lines", help="kernel regex: per-source-line breakdown")
     ap.add_argument("--top", type=int, default=30)
+    ap.add_argument("--traffic-json", help="write per-frame DRAM bytes and warp instructions (bench roofline input)")
+    ap.add_argument("--b-alg", type=float, default=340272000.0)
     a = ap.parse_args()
+    if a.traffic_json:
+        import json
+        dram, inst = {}, {}
+        for d, u in raw(a.rep):
+            name = d.get("Kernel Name", "?").split("(")[0].replace("ges::", "")
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            b = sum(float(d[k].replace(",", "")) * scale.get(u.get(k, "byte"), 1)
+                    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            dram[name] = dram.get(name, 0.0) + b
+            inst[name] = inst.get(name, 0.0) + float(d["smsp__inst_executed.sum"].replace(",", ""))
+        out = {"config": 2, "source": f"{a.rep} (ncu --set full, one frame, cold-cache replay)",
+               "dram_bytes_per_frame": sum(dram.values()), "per_kernel": dram,
+               "b_alg_bytes_per_frame": a.b_alg, "warp_instructions_per_frame": sum(inst.values()),
+               "warp_instructions_per_kernel": inst}
+        with open(a.traffic_json, "w") as f:
+            json.dump(out, f, indent=1)
+        print(json.dumps(out, indent=1))
     if a.launches:
         launches(a.launches)
     if a.lines:
