@@ -30,7 +30,6 @@
 
 namespace ges {
 
-constexpr int NB = TILE_PX;     // threads per CTA (32 shared slots per warp)
 
 // Work counters for tuning (compiled in only with -DGES_STATS; read with
 // ges_debug_stats).  0 surfel batches, 1 surfel entries staged, 2 staged with
@@ -44,10 +43,22 @@ __device__ unsigned long long g_stats[20];
 #define GES_STAT(i, v) ((void)0)
 #endif
 
+// Warps per CTA.  The 8 warps of a tile never synchronise after the
+// prologue, so a tile can be split over 8 / WPC CTAs: a CTA's registers are
+// held until its slowest warp finishes, and small CTAs hand them back warp by
+// warp (the warps of one tile have very different amounts of work).
+#ifndef GES_TILE_WPC
+#define GES_TILE_WPC 1   // 32x32-pixel tiles and ss=4
+#endif
+#ifndef GES_TILE_WPC1
+#define GES_TILE_WPC1 2  // 16x16-pixel tiles (40 registers: 24 two-warp CTAs per SM)
+#endif
+
+template <int WPC>
 struct __align__(16) TileSmem {
-    float4 st[4][NB];           // per-warp slots (32 each): pass-1 surfel coefficients, pass-2
+    float4 st[4][32 * WPC];     // per-warp slots (32 each): pass-1 surfel coefficients, pass-2
                                 // Gaussian records, then the colour tasks
-    float4 rmax[NWARP][2];      // per warp: max best depth of each of its 4 x 2 regions of
+    float4 rmax[WPC][2];        // per warp: max best depth of each of its 4 x 2 regions of
                                 // 2 x 2 lanes (pass-1 culling)
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
     uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
@@ -182,8 +193,8 @@ static __device__ __noinline__ float3 surfel_color_eval(const float* __restrict_
 // lanes is evaluated once), the list is evaluated 32 tasks per SIMT pass, and
 // every sample reads its colour back.  Must be called by all 32 lanes, with
 // the warp's slice of sm.st free.
-template <int NS>
-__device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, TileSmem& sm, uint32_t covm,
+template <int NS, class Smem>
+__device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, Smem& sm, uint32_t covm,
                                                       const uint32_t* bp, int lane, int warp, float3* col) {
     const float3 bg = make_float3(a.bg[0], a.bg[1], a.bg[2]);
     if constexpr (NS == 1) {
@@ -257,13 +268,24 @@ __device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, TileSme
 // tiles, each thread a 2x2 pixel block, so every staged surfel and every
 // list step is shared by 4 pixels).  A thread owns G x G = (SS*PX)^2 samples
 // in pass 1 and PX x PX pixels in pass 2.
+template <int SS, int PX>
+__host__ __device__ constexpr int tile_wpc() { return (PX == 2 || SS == 2) ? GES_TILE_WPC : GES_TILE_WPC1; }
+template <int SS, int PX>
+__host__ __device__ constexpr int tile_min_blocks() {   // resident CTAs per SM: 4 (64 registers) or 6 (40) tiles' worth of warps
+    return ((PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6) * NWARP / tile_wpc<SS, PX>() > 32
+               ? 32 : ((PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6) * NWARP / tile_wpc<SS, PX>();
+}
+
 template <int SS, int PX, int MODE, int GK, bool GEOM>
-__global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6) k_tile(TileArgs a) {
+__global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, PX>()) k_tile(TileArgs a) {
     constexpr int G = SS * PX, NS = G * G, NP = PX * PX, TP = TILE * PX;
-    __shared__ TileSmem sm;
+    constexpr int WPC = tile_wpc<SS, PX>(), TPB = 32 * WPC;
+    __shared__ TileSmem<WPC> sm;
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tx = blockIdx.x, ty = blockIdx.y;
+    // warp: the warp's patch within the tile (0..7); wl: its index within the CTA
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int warp = (int)(blockIdx.x % (NWARP / WPC)) * WPC + wl;
+    const int tx = blockIdx.x / (NWARP / WPC), ty = blockIdx.y;
     const int tile = ty * a.ntx + tx;
     const int plx = (warp & 1) * 8 + (lane & 7), ply = (warp >> 1) * 4 + (lane >> 3);
     const int bx = tx * TP + PX * plx, by = ty * TP + PX * ply;   // first base pixel of the thread
@@ -280,10 +302,10 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
     // prefetch) overlaps the surfel pass.
     uint32_t gbeg = 0, gend = 0, gid = 0;
     if constexpr ((MODE & 2) != 0) {
-        if (threadIdx.x < NSLAB) sm.gslab_end[threadIdx.x] = a.gbin.cnt[tile * NSLAB + threadIdx.x];
+        for (int k = threadIdx.x; k < NSLAB; k += TPB) sm.gslab_end[k] = a.gbin.cnt[tile * NSLAB + k];
         gbeg = a.gbin.tile_off(tile);
         gend = gbeg + a.gbin.cnt[tile * NSLAB + NSLAB - 1];
-        if (gbeg + threadIdx.x < gend) gid = a.g_list[gbeg + threadIdx.x];
+        if (gbeg + warp * 32 + lane < gend) gid = a.g_list[gbeg + warp * 32 + lane];
     }
 
     // best[s]: packed (t_bits << 32 | source id) of the nearest surfel hit so
@@ -319,7 +341,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
         // patch (wmx).  A single uncovered sample keeps its bound at +inf, so
         // per-region bounds let covered parts of the patch cull entries long
         // before the whole patch is covered.
-        float* const rm = reinterpret_cast<float*>(sm.rmax[warp]);
+        float* const rm = reinterpret_cast<float*>(sm.rmax[wl]);
         auto patch_depth = [&]() {
             float m = tb[0];
 #pragma unroll
@@ -328,13 +350,13 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
         };
         if (lane < 8) rm[lane] = INFINITY;
         float wmx = INFINITY;          // max over this warp's samples of the best depth
-        if (threadIdx.x < NSLAB) sm.slab_end[threadIdx.x] = a.sbin.cnt[tile * NSLAB + threadIdx.x];
+        for (int k = threadIdx.x; k < NSLAB; k += TPB) sm.slab_end[k] = a.sbin.cnt[tile * NSLAB + k];
         __syncthreads();
         const int ox = tx * TP * SS, oy = ty * TP * SS;
         const uint32_t beg = a.sbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
         uint32_t nid = beg + lane < end ? a.s_list[beg + lane] : 0u;
         if constexpr ((MODE & 2) != 0) {
-            if (gbeg + threadIdx.x < gend) {
+            if (gbeg + warp * 32 + lane < gend) {
                 const char* gp = static_cast<const char*>(a.grec) + (size_t)gid * (GK == 2 ? sizeof(Gauss2Rec) : sizeof(GaussRec));
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(gp));
             }
@@ -361,7 +383,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 live = span_lo(sxr) < wx0 + PW && span_hi(sxr) >= wx0 && span_lo(syr) < wy0 + PH &&
                        span_hi(syr) >= wy0 && !(r3.x > wmx);
                 // nearest disc depth vs the regions its pixel range overlaps
-                if (live) live = !(r3.x > region_max<2 * G>(sm.rmax[warp], span_lo(sxr) - wx0, span_hi(sxr) - wx0,
+                if (live) live = !(r3.x > region_max<2 * G>(sm.rmax[wl], span_lo(sxr) - wx0, span_hi(sxr) - wx0,
                                                             span_lo(syr) - wy0, span_hi(syr) - wy0));
                 if (live) {
                     const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2);
@@ -375,7 +397,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                     live = nq > 0.f;
                     // U, V pre-divided by R: coverage becomes U'^2 + V'^2 <= den^2
                     constexpr float IR = 1.0f / 3.3290429691304455f;
-                    const int slot = warp * 32 + lane;
+                    const int slot = wl * 32 + lane;
                     sm.st[0][slot] = make_float4(d0, dx_, dy_, nq);
                     sm.st[1][slot] = make_float4(u0 * IR, r1.y * IR, r1.z * IR, v0 * IR);
                     sm.st[2][slot] = make_float4(r2.y * IR, r2.z * IR, r3.w, r3.x);   // r3.w: source id
@@ -388,7 +410,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
             if (!vote) continue;     // nothing tested: the patch depth is unchanged
             __syncwarp();
             while (vote) {
-                const int j = warp * 32 + __ffs(vote) - 1;
+                const int j = wl * 32 + __ffs(vote) - 1;
                 vote &= vote - 1;
                 const float4 C = sm.st[2][j];
                 if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
@@ -508,7 +530,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
 #pragma unroll
         for (int p = 0; p < NP; ++p) dm = fmaxf(dm, inside_px(p) ? ds[p] : -INFINITY);
         const float wdmax = warp_max(dm);
-        if (threadIdx.x == 0) GES_STAT(10, 1);
+        if (warp == 0 && lane == 0) GES_STAT(10, 1);
         if (lane == 0) GES_STAT(11, wdmax == INFINITY);
         float pe[NP];
 #pragma unroll
@@ -575,7 +597,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
             }
             // survivors park their record in this warp's slice of shared memory;
             // every lane then reads each survivor with broadcast loads
-            const int slot = warp * 32 + lane;
+            const int slot = wl * 32 + lane;
             if (live) {
                 sm.st[0][slot] = make_float4(v[0], v[1], v[2], v[3]);
                 sm.st[1][slot] = make_float4(v[4], v[5], v[6], v[7]);
@@ -591,13 +613,13 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
                 if (lane == 0) GES_STAT(8, 1);
                 float w[16];
                 {
-                    const float4 q0 = sm.st[0][warp * 32 + j], q1 = sm.st[1][warp * 32 + j],
-                                 q2 = sm.st[2][warp * 32 + j];
+                    const float4 q0 = sm.st[0][wl * 32 + j], q1 = sm.st[1][wl * 32 + j],
+                                 q2 = sm.st[2][wl * 32 + j];
                     w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
                     w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
                     w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
                     if constexpr (GK == 2 || GEOM) {
-                        const float4 q3 = sm.st[3][warp * 32 + j];
+                        const float4 q3 = sm.st[3][wl * 32 + j];
                         w[12] = q3.x; w[13] = q3.y; w[14] = q3.z; w[15] = q3.w;
                     }
                 }
@@ -660,7 +682,7 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
     for (int p = 0; p < NP; ++p) cs[p] = make_float3(a.bg[0], a.bg[1], a.bg[2]);
     if constexpr ((MODE & 1) != 0) {
         float3 col[NS];
-        resolve_surfel_colors<NS>(a, sm, covm, bp, lane, warp, col);
+        resolve_surfel_colors<NS>(a, sm, covm, bp, lane, wl, col);
         if constexpr (PX == 1) {   // box mean over the sub-samples (forward.py:201-203)
             float3 acc = make_float3(0.f, 0.f, 0.f);
 #pragma unroll
@@ -749,13 +771,14 @@ __global__ void __launch_bounds__(NB, (PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6)
 
 template <int SS, int PX, int MODE>
 static void launch_kind(const TileArgs& a, int g_kind, bool geom, cudaStream_t s) {
-    const dim3 nt((unsigned)a.ntx, (unsigned)a.nty);
+    constexpr int WPC = tile_wpc<SS, PX>();
+    const dim3 nt((unsigned)(a.ntx * (NWARP / WPC)), (unsigned)a.nty);
     if (g_kind == 2) {
-        if (geom) k_tile<SS, PX, MODE, 2, true><<<nt, NB, 0, s>>>(a);
-        else k_tile<SS, PX, MODE, 2, false><<<nt, NB, 0, s>>>(a);
+        if (geom) k_tile<SS, PX, MODE, 2, true><<<nt, 32 * WPC, 0, s>>>(a);
+        else k_tile<SS, PX, MODE, 2, false><<<nt, 32 * WPC, 0, s>>>(a);
     } else {
-        if (geom) k_tile<SS, PX, MODE, 3, true><<<nt, NB, 0, s>>>(a);
-        else k_tile<SS, PX, MODE, 3, false><<<nt, NB, 0, s>>>(a);
+        if (geom) k_tile<SS, PX, MODE, 3, true><<<nt, 32 * WPC, 0, s>>>(a);
+        else k_tile<SS, PX, MODE, 3, false><<<nt, 32 * WPC, 0, s>>>(a);
     }
 }
 
