@@ -68,7 +68,9 @@ int check_cam(const ges_camera_t* c) {
 // Frame workspace layout; base == nullptr only measures.
 struct Frame {
     SurfRec* srec;
+    float4* scull;
     void* grec;
+    float4* gcull;
     float4* g_nrm;
     uint32_t *cnt_s, *off_s, *cnt_g, *off_g, *chunk_s, *chunk_g, *tickets;
     size_t zero_bytes;   // counters + tickets, cleared by one memset per frame
@@ -108,7 +110,9 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, const g
     f.chunk_s = c.take<uint32_t>(nchunk);
     f.chunk_g = c.take<uint32_t>(nchunk);
     f.srec = c.take<SurfRec>(ns);
+    f.scull = c.take<float4>(ns);
     f.grec = c.take<char>(ng * (sc->gaussian_dim == 2 ? sizeof(Gauss2Rec) : sizeof(GaussRec)));
+    f.gcull = c.take<float4>(ng);
     f.g_nrm = c.take<float4>(ng);
     f.list_s = c.take<uint32_t>((size_t)cap_s);
     f.list_g = c.take<uint32_t>((size_t)cap_g);
@@ -178,15 +182,15 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, tp * grid,
                      log2i(tp * grid)};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, tp, log2i(tp)};
-    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, nullptr, f.cnt_s}, s)))
+    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, nullptr, f.cnt_s, nullptr, f.scull}, s)))
         return cuda_fail(e, "surfel preprocess");
-    if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g}, s)))
+    if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g, nullptr, f.gcull}, s)))
         return cuda_fail(e, "gaussian preprocess");
     mark(2);
     if ((e = launch_scan(bs, bg, status, s)))
         return cuda_fail(e, "tile scan");
     mark(3);
-    if ((e = launch_fill(f.srec, scs.n_surfels, bs, f.grec, scs.n_gaussians, sc->gaussian_dim, bg, slabs, s)))
+    if ((e = launch_fill(f.scull, scs.n_surfels, bs, f.gcull, scs.n_gaussians, sc->gaussian_dim, bg, slabs, s)))
         return cuda_fail(e, "tile fill");
     mark(4);
     TileArgs a{};
@@ -194,7 +198,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     a.layers = st->layers;
     for (int i = 0; i < 3; ++i) a.bg[i] = st->background[i];
     a.rcx = (float)cs.cx; a.rcy = (float)cs.cy; a.rifx = (float)(1.0 / cs.fx); a.rify = (float)(1.0 / cs.fy);
-    a.srec = f.srec; a.s_list = f.list_s; a.sbin = bs;
+    a.srec = f.srec; a.scull = f.scull; a.s_list = f.list_s; a.sbin = bs;
     a.s_sh = sc->s_sh; a.sh_deg = sc->sh_degree; a.sh_bytes = (sc->sh_degree + 1) * (sc->sh_degree + 1) * 12;
     for (int i = 0; i < 3; ++i) a.cpos[i] = cs.pos[i];
     a.s_quat = reinterpret_cast<const float4*>(sc->s_quat);
@@ -204,7 +208,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     for (int i = 0; i < 3; ++i) a.t[i] = cs.t[i];
     a.slabs = slabs;
     a.gcx = (float)cg.cx; a.gcy = (float)cg.cy; a.gifx = (float)(1.0 / cg.fx); a.gify = (float)(1.0 / cg.fy);
-    a.grec = f.grec; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg;
+    a.grec = f.grec; a.gcull = f.gcull; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg;
     a.ds_in = ds_in;
     a.out = *out;
     a.status = status;
@@ -386,13 +390,13 @@ int ges_backward_gaussians(const ges_scene_t* sc, const ges_scene_src_t* src, in
     scs.n_surfels = 0;
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, 0, f.ntiles, f.ntx, TILE, 4};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE, 4};
-    PrepOut po{f.grec, nullptr, f.g_nrm, f.cnt_g, sc->gaussian_dim == 2 ? aux : nullptr};
+    PrepOut po{f.grec, nullptr, f.g_nrm, f.cnt_g, sc->gaussian_dim == 2 ? aux : nullptr, f.gcull};
     if ((e = launch_gauss_prep(scs, cg, gg, s2, po, s))) return cuda_fail(e, "gaussian preprocess");
     if ((e = launch_scan(bs, bg, status, s))) return cuda_fail(e, "tile scan");
-    if ((e = launch_fill(f.srec, 0, bs, f.grec, ng, sc->gaussian_dim, bg, slabs, s))) return cuda_fail(e, "tile fill");
+    if ((e = launch_fill(f.scull, 0, bs, f.gcull, ng, sc->gaussian_dim, bg, slabs, s))) return cuda_fail(e, "tile fill");
     BwdArgs a{};
     a.W = cam->width; a.H = cam->height; a.ntx = f.ntx; a.nty = f.nty;
-    a.grec = f.grec; a.aux = aux; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg; a.slabs = slabs;
+    a.grec = f.grec; a.gcull = f.gcull; a.aux = aux; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg; a.slabs = slabs;
     a.ds = surfel_depth; a.g_cg = g_color; a.g_wg = g_weight; a.g_gd = g_depth; a.g_gn = geom ? g_normal : nullptr;
     a.gcx = (float)cg.cx; a.gcy = (float)cg.cy; a.gifx = (float)(1.0 / cg.fx); a.gify = (float)(1.0 / cg.fy);
     a.acc = acc;
@@ -442,13 +446,13 @@ int ges_gaussian_contributions(const ges_scene_t* sc, const ges_scene_src_t* src
     scs.n_surfels = 0;
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, 0, f.ntiles, f.ntx, TILE, 4};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE, 4};
-    PrepOut po{f.grec, nullptr, f.g_nrm, f.cnt_g, nullptr};
+    PrepOut po{f.grec, nullptr, f.g_nrm, f.cnt_g, nullptr, f.gcull};
     if ((e = launch_gauss_prep(scs, cg, gg, s2, po, s))) return cuda_fail(e, "gaussian preprocess");
     if ((e = launch_scan(bs, bg, status, s))) return cuda_fail(e, "tile scan");
-    if ((e = launch_fill(f.srec, 0, bs, f.grec, ng, sc->gaussian_dim, bg, slabs, s))) return cuda_fail(e, "tile fill");
+    if ((e = launch_fill(f.scull, 0, bs, f.gcull, ng, sc->gaussian_dim, bg, slabs, s))) return cuda_fail(e, "tile fill");
     BwdArgs a{};
     a.W = cam->width; a.H = cam->height; a.ntx = f.ntx; a.nty = f.nty;
-    a.grec = f.grec; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg; a.slabs = slabs;
+    a.grec = f.grec; a.gcull = f.gcull; a.g_nrm = f.g_nrm; a.g_list = f.list_g; a.gbin = bg; a.slabs = slabs;
     a.ds = surfel_depth; a.g_wg = g_weight;
     a.gcx = (float)cg.cx; a.gcy = (float)cg.cy; a.gifx = (float)(1.0 / cg.fx); a.gify = (float)(1.0 / cg.fy);
     a.scores = scores;

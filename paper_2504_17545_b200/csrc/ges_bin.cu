@@ -168,14 +168,14 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
 }
 
 // Surfel blocks first, then Gaussian blocks, so every warp is one class.
-__global__ void __launch_bounds__(256) k_fill(const SurfRec* __restrict__ srec, int64_t ns, BinPass ps,
-                                              const float4* __restrict__ grec, int64_t ng, int g_kind, BinPass pg,
+__global__ void __launch_bounds__(256) k_fill(const float4* __restrict__ scull, int64_t ns, BinPass ps,
+                                              const float4* __restrict__ gcull, int64_t ng, int g_kind, BinPass pg,
                                               SlabMap sm) {
     const unsigned sblocks = (unsigned)((ns + 255) >> 8);   // blockDim.x == 256
     if (blockIdx.x < sblocks) {
         const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
         const bool live = i < ns;
-        const float4 r3 = live ? __ldg(&srec[i].r3) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 r3 = live ? __ldg(scull + i) : make_float4(0.f, 0.f, 0.f, 0.f);
         fill_one(live, (uint32_t)i, __float_as_uint(r3.y), __float_as_uint(r3.z), sm.slab(r3.x), ps);
     } else {
         const int64_t j = (int64_t)(blockIdx.x - sblocks) * 256 + threadIdx.x;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) k_fill(const SurfRec* __restrict__ srec, 
         uint32_t sx = 0, sy = 0;
         float key = 0.f;
         if (live) {   // cull fields: c = (depth or key, eps, rect_x, rect_y)
-            const float4 c = __ldg(grec + j * (g_kind == 2 ? 6 : 4));
+            const float4 c = __ldg(gcull + j);
             sx = __float_as_uint(c.z); sy = __float_as_uint(c.w);
             key = g_kind == 2 ? c.x : gauss_key(c.x, c.y);
         }
@@ -191,11 +191,11 @@ __global__ void __launch_bounds__(256) k_fill(const SurfRec* __restrict__ srec, 
     }
 }
 
-cudaError_t launch_fill(const void* srec, int64_t ns, const BinPass& ps, const void* grec, int64_t ng, int g_kind,
+cudaError_t launch_fill(const float4* scull, int64_t ns, const BinPass& ps, const float4* gcull, int64_t ng, int g_kind,
                         const BinPass& pg, const SlabMap& sm, cudaStream_t s) {
     const int64_t nb = (ns + 255) / 256 + (ng + 255) / 256;
     if (nb == 0) return cudaSuccess;
-    k_fill<<<(unsigned)nb, 256, 0, s>>>((const SurfRec*)srec, ns, ps, (const float4*)grec, ng, g_kind, pg, sm);
+    k_fill<<<(unsigned)nb, 256, 0, s>>>(scull, ns, ps, gcull, ng, g_kind, pg, sm);
     return cudaGetLastError();
 }
 

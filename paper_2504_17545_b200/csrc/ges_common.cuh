@@ -47,34 +47,35 @@ struct CamK {
     int W, H;           // resolution of THIS pass (hi-res for ss=4 surfels)
 };
 
-// Per-surfel screen record written by the surfel preprocess (64 B).
+// Per-surfel screen record written by the surfel preprocess (48 B).
 //   r0 = (D0, Dx, Dy, nq)   den(x,y) = n.d = D0 + Dx*(x-xr) + Dy*(y-yr)
 //   r1 = (U0, Ux, Uy, xr)   U = ((n.q) a1 - (a1.q) n).d / s1, u = U/den
 //   r2 = (V0, Vx, Vy, yr)   V likewise with a2, s2
-//   r3 = (zmin, rect_x, rect_y, 0)  rect packed lo | hi << 16 (pixel ranges)
+// and, in a separate dense array (16 B per surfel, so binning and the tile
+// kernel's cull read 16 B instead of a 64-byte DRAM burst per surfel):
+//   cull = (zmin, rect_x, rect_y, source id)  rect packed lo | hi << 16 (pixel ranges)
 struct __align__(16) SurfRec {
-    float4 r0, r1, r2, r3;
+    float4 r0, r1, r2;
 };
 
-// Per-Gaussian screen records.  The first float4 `c` holds everything the
-// cull needs (depth test inputs and pixel range), so binning and the tile
-// kernel's staging read 16 B per entry and fetch the rest only for the few
-// entries that survive.
-// 3D EWA, 64 B:
-//   c  = (depth, eps, rect_x, rect_y)
+// Per-Gaussian screen records.  Everything the cull needs (depth test inputs
+// and pixel range) is a separate dense array of 16-byte records `c`, so
+// binning and the tile kernel's staging read 16 B per entry and fetch the
+// rest only for the few entries that survive.
+// 3D EWA: c = (depth, eps, rect_x, rect_y), and 48 B
 //   r0 = (mx_int, mx_frac, my_int, my_frac)       mean2d split for precision
 //   r1 = (pa, pb, pc, sigma)  log2(e) * power = pa dx^2 + pb dx dy + pc dy^2,
 //                             alpha = sigma * 2^(pa dx^2 + ...)
 //   r2 = (pmin, r, g, b)      pmin: log2(e) * power below which alpha < 1/255
 struct __align__(16) GaussRec {
-    float4 c, r0, r1, r2;
+    float4 r0, r1, r2;
 };
 
-// Planar 2D Gaussian, 96 B: c = (slab/cull key, eps, rect_x, rect_y), then the
+// Planar 2D Gaussian: c = (slab/cull key, eps, rect_x, rect_y), and 80 B: the
 // ray-plane homography r0..r2 like SurfRec, r3 = (sigma, r2max, 0, 0),
 // r4 = (r, g, b, 0).
 struct __align__(16) Gauss2Rec {
-    float4 c, r0, r1, r2, r3, r4;
+    float4 r0, r1, r2, r3, r4;
 };
 
 // Depth slabs of the (tile, slab) bins: NSLAB equal slabs over the view's

@@ -14,6 +14,7 @@ struct PrepOut {
     uint32_t* bin_count;    // per-(tile, slab) pair counters (zeroed by the caller)
     float4* aux;            // 2D Gaussians, training backward only: (a1/s1).d and (a2/s2).d
                             // as affine functions of the pixel (2 per Gaussian), or NULL
+    float4* cull;           // dense cull records (see SurfRec, GaussRec)
 };
 
 // Tile grid for the pass: ntx x nty tiles of `tile_px` pixels at resolution W x H.
@@ -30,7 +31,7 @@ cudaError_t launch_surfel_prep(const ges_scene_t& sc, const CamK& cam, const Gri
 cudaError_t launch_gauss_prep(const ges_scene_t& sc, const CamK& cam, const Grid& g,
                               const ges_settings_t& st, const PrepOut& o, cudaStream_t s);
 cudaError_t launch_scan(const BinPass& s, const BinPass& g, ges_frame_status_t* status, cudaStream_t st);
-cudaError_t launch_fill(const void* srec, int64_t ns, const BinPass& ps, const void* grec, int64_t ng, int g_kind,
+cudaError_t launch_fill(const float4* scull, int64_t ns, const BinPass& ps, const float4* gcull, int64_t ng, int g_kind,
                         const BinPass& pg, const SlabMap& sm, cudaStream_t s);
 
 struct TileArgs {
@@ -40,6 +41,7 @@ struct TileArgs {
     // surfel pass (resolution = ss * base)
     float rcx, rcy, rifx, rify;   // principal point and 1/f of the surfel pass
     const SurfRec* srec;
+    const float4* scull;          // dense surfel cull records
     const float* s_sh;            // packed SH (deferred colour of winners)
     int sh_deg, sh_bytes;
     double cpos[3];               // camera centre (world)
@@ -51,6 +53,7 @@ struct TileArgs {
     // Gaussian pass (base resolution)
     float gcx, gcy, gifx, gify;
     const void* grec;
+    const float4* gcull;          // dense Gaussian cull records
     const float4* g_rgb;          // 2D Gaussians: colours
     const float4* g_nrm;          // with_geometry normals
     const uint32_t* g_list;
@@ -76,6 +79,7 @@ cudaError_t launch_smooth(const float* sd, const float* sn, const float* gd, con
 struct BwdArgs {
     int W, H, ntx, nty;           // base resolution, 16x16 tiles
     const void* grec;
+    const float4* gcull;
     const float4* aux;            // 2D: (k1, k2) affine coefficients per Gaussian
     const float4* g_nrm;          // normal cotangent given: camera-facing normals
     const uint32_t* g_list;

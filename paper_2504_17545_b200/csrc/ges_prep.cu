@@ -241,16 +241,15 @@ __global__ void __launch_bounds__(256, GES_PREP_MINB) k_surfel_prep(ges_scene_t 
     const int32_t sid = __ldg(sc.s_id + i);
     if (alive) {
         planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
-        rec.r3 = make_float4(zkey, __uint_as_float(pack_span(x0, x1)),
-                             __uint_as_float(pack_span(y0, y1)), __int_as_float(sid));
+        o.cull[i] = make_float4(zkey, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)),
+                                __int_as_float(sid));
+        reinterpret_cast<SurfRec*>(o.rec)[i] = rec;
         // view colour (forward.py:99-103) and n_vis (:152) are evaluated for
         // winners only, in the tile kernel
-    } else {
-        rec.r0 = rec.r1 = rec.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
-        rec.r3 = make_float4(0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)),
-                             __int_as_float(sid));
+    } else {   // empty pixel range: never binned, the coefficients are never read
+        o.cull[i] = make_float4(0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)),
+                                __int_as_float(sid));
     }
-    reinterpret_cast<SurfRec*>(o.rec)[i] = rec;
 }
 
 cudaError_t launch_surfel_prep(const ges_scene_t& sc, const CamK& cam, const Grid& g, const PrepOut& o,
@@ -349,7 +348,7 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_
     if (!valid_thread) return;
     if (valid) {
         double mxi = floor(mx), myi = floor(my);
-        rec.c = make_float4(depf, epsf, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)));
+        o.cull[i] = make_float4(depf, epsf, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)));
         rec.r0 = make_float4((float)mxi, (float)(mx - mxi), (float)myi, (float)(my - myi));
         // conic pre-scaled by log2(e): the tile kernel evaluates exp as one ex2
         const double L2E = 1.4426950408889634;
@@ -365,11 +364,10 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_
             double sgn = dot(nv, t) < 0.0 ? 1.0 : -1.0;
             o.nrm[i] = make_float4((float)(nv.x * sgn), (float)(nv.y * sgn), (float)(nv.z * sgn), 0.f);
         }
-    } else {
-        rec.r0 = rec.r1 = rec.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
-        rec.c = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
+        reinterpret_cast<GaussRec*>(o.rec)[i] = rec;
+    } else {   // empty pixel range: never binned, the record is never read
+        o.cull[i] = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
     }
-    reinterpret_cast<GaussRec*>(o.rec)[i] = rec;
 }
 
 // Planar 2D Gaussians: forward.py:324-351 (+ filters.py:84-109 when mip).
@@ -423,7 +421,7 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss2_prep(ges_
     Gauss2Rec rec;
     if (valid) {
         planar_coeffs(q, a1, a2, n, s1, s2, cam, x0, x1, y0, y1, rec.r0, rec.r1, rec.r2);
-        rec.c = make_float4(gkey, epsf, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)));
+        o.cull[i] = make_float4(gkey, epsf, __uint_as_float(pack_span(x0, x1)), __uint_as_float(pack_span(y0, y1)));
         rec.r3 = make_float4((float)sig, (float)m2max * 1.0001f + 1e-4f, 0.f, 0.f);
         rec.r4 = make_float4(col.x, col.y, col.z, 0.f);
         if (o.aux) {   // k1 = a1.d/s1, k2 = a2.d/s2 of ray_splat_backward (geometry.py:229-252)
@@ -435,11 +433,10 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss2_prep(ges_
             double sgn = dot(n, q) < 0.0 ? 1.0 : -1.0;   // forward.py:337
             o.nrm[i] = make_float4((float)(n.x * sgn), (float)(n.y * sgn), (float)(n.z * sgn), 0.f);
         }
-    } else {
-        rec.r0 = rec.r1 = rec.r2 = rec.r3 = rec.r4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        rec.c = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
+        reinterpret_cast<Gauss2Rec*>(o.rec)[i] = rec;
+    } else {   // empty pixel range: never binned, the record is never read
+        o.cull[i] = make_float4(0.f, 0.f, __uint_as_float(pack_span(1, 0)), __uint_as_float(pack_span(1, 0)));
     }
-    reinterpret_cast<Gauss2Rec*>(o.rec)[i] = rec;
 }
 
 cudaError_t launch_gauss_prep(const ges_scene_t& sc, const CamK& cam, const Grid& g,

@@ -377,8 +377,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             if (e + 32 < end) nid = a.s_list[e + 32];
             bool live = false;
             if (e < end) {
-                const SurfRec* r = a.srec + id;
-                const float4 r3 = __ldg(&r->r3);
+                const float4 r3 = __ldg(a.scull + id);
                 const uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
                 live = span_lo(sxr) < wx0 + PW && span_hi(sxr) >= wx0 && span_lo(syr) < wy0 + PH &&
                        span_hi(syr) >= wy0 && !(r3.x > wmx);
@@ -386,6 +385,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 if (live) live = !(r3.x > region_max<2 * G>(sm.rmax[wl], span_lo(sxr) - wx0, span_hi(sxr) - wx0,
                                                             span_lo(syr) - wy0, span_hi(syr) - wy0));
                 if (live) {
+                    const SurfRec* r = a.srec + id;
                     const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2);
                     const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
                     float d0 = fmaf(r0.z, fy, fmaf(r0.y, fx, r0.x));
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 const uint32_t id = a.g_list[e];
                 if constexpr (GK == 3) {
                     const GaussRec* r = reinterpret_cast<const GaussRec*>(a.grec) + id;
-                    const float4 c = __ldg(&r->c);
+                    const float4 c = __ldg(a.gcull + id);
                     const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
                     // exact conservative cull: d < fl(max_ds + eps) is necessary for the gate
                     live = span_lo(sxr) - ox <= px0 + 8 * PX - 1 && span_hi(sxr) - ox >= px0 &&
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                     }
                 } else {
                     const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + id;
-                    const float4 c = __ldg(&r->c);
+                    const float4 c = __ldg(a.gcull + id);
                     const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
                     live = span_lo(sxr) - ox <= px0 + 8 * PX - 1 && span_hi(sxr) - ox >= px0 &&
                            span_lo(syr) - oy <= py0 + 4 * PX - 1 && span_hi(syr) - oy >= py0 && !(c.x > wdmax);

@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
         uint32_t id = 0;
         if (e < gend) {
             id = a.g_list[e];
-            const float4 c = __ldg(reinterpret_cast<const float4*>(a.grec) + (size_t)id * (GK == 2 ? 6 : 4));
+            const float4 c = __ldg(a.gcull + id);
             const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
             live = span_lo(sxr) - ox <= px0 + 7 && span_hi(sxr) - ox >= px0 && span_lo(syr) - oy <= py0 + 3 &&
                    span_hi(syr) - oy >= py0 && (GK == 3 ? c.x < wdmax + c.y : !(c.x > wdmax));
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
             bool contrib = false;
             if constexpr (GK == 3) {
                 const GaussRec* r = reinterpret_cast<const GaussRec*>(a.grec) + gid;
-                const float4 c = r->c, r0 = r->r0, r1 = r->r1, r2 = r->r2;
+                const float4 c = a.gcull[gid], r0 = r->r0, r1 = r->r1, r2 = r->r2;
                 const float mx = (r0.x - (float)ox) + (r0.y - 0.5f), my = (r0.z - (float)oy) + (r0.w - 0.5f);
                 // identical to the forward tile kernel (forward.py:301-311)
                 const float dx = lx - mx, dy = ly - my;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256) k_gauss_bwd(BwdArgs a) {
                 }
             } else {
                 const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + gid;
-                const float4 c = r->c, r0 = r->r0, r1 = r->r1, r2 = r->r2, r3 = r->r3, r4 = r->r4;
+                const float4 c = a.gcull[gid], r0 = r->r0, r1 = r->r1, r2 = r->r2, r3 = r->r3, r4 = r->r4;
                 const float4 k1c = CONTRIB ? float4{} : a.aux[2 * (size_t)gid];
                 const float4 k2c = CONTRIB ? float4{} : a.aux[2 * (size_t)gid + 1];
                 const float fx = (float)(ox - (int)r1.w), fy = (float)(oy - (int)r2.w);
