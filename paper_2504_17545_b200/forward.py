@@ -92,8 +92,28 @@ def _check_settings(settings):
     return settings
 
 
+def _host(t):
+    """Start the device -> host copy of ``t`` into pinned memory (torch's
+    caching host allocator: blocks come back to the pool when the caller drops
+    the array, so steady-state calls allocate nothing and copy at PCIe speed
+    instead of through pageable staging).  Call ``_numpy`` after a sync."""
+    if t is None:
+        return None
+    h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    return h
+
+
+def _numpy(*hs):
+    """Wait for the copies started by ``_host`` and view them as NumPy arrays
+    (each array keeps its pinned block alive)."""
+    if hs and any(h is not None for h in hs):
+        torch.cuda.current_stream().synchronize()
+    return tuple(None if h is None else h.numpy() for h in hs)
+
+
 def _np(t):
-    return None if t is None else t.cpu().numpy()
+    return _numpy(_host(t))[0]
 
 
 def _device():
@@ -102,18 +122,22 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_SURF = ("color", "depth", "normal", "coverage", "winner")
+_GAUSS = ("color", "weight", "depth", "normal")
+
+
 def _surfel_buffers(fr, to_numpy):
     cov = torch.isfinite(fr.s_depth)
     sb = SurfelBuffers(fr.s_color, fr.s_depth, fr.s_normal, cov, fr.s_winner)
     if to_numpy:
-        sb = SurfelBuffers(*(_np(getattr(sb, k)) for k in ("color", "depth", "normal", "coverage", "winner")))
+        sb = SurfelBuffers(*_numpy(*(_host(getattr(sb, k)) for k in _SURF)))
     return sb
 
 
 def _gauss_buffers(fr, to_numpy):
     gb = GaussianBuffers(fr.g_color, fr.g_weight, fr.g_depth, fr.g_normal)
     if to_numpy:
-        gb = GaussianBuffers(_np(gb.color), _np(gb.weight), _np(gb.depth), _np(gb.normal))
+        gb = GaussianBuffers(*_numpy(*(_host(getattr(gb, k)) for k in _GAUSS)))
     return gb
 
 
@@ -124,9 +148,14 @@ def render(scene, cam, settings: RenderSettings | None = None, *, to_numpy: bool
     dev = _device()
     ds = SCENE_CACHE.get(scene, dev)
     fr = default_renderer(dev).render(ds, cam, settings, mode=3)
-    sb = _surfel_buffers(fr, to_numpy)
-    gb = _gauss_buffers(fr, to_numpy)
-    return RenderResult(_np(fr.image) if to_numpy else fr.image, sb, gb)
+    if not to_numpy:
+        return RenderResult(fr.image, _surfel_buffers(fr, False), _gauss_buffers(fr, False))
+    # every buffer's copy is queued before the one synchronisation
+    cov = torch.isfinite(fr.s_depth)
+    hs = [_host(t) for t in (fr.image, fr.s_color, fr.s_depth, fr.s_normal, cov, fr.s_winner,
+                             fr.g_color, fr.g_weight, fr.g_depth, fr.g_normal)]
+    a = _numpy(*hs)
+    return RenderResult(a[0], SurfelBuffers(*a[1:6]), GaussianBuffers(*a[6:10]))
 
 
 def rasterize_surfels(scene, cam, settings: RenderSettings | None = None, *, to_numpy: bool = True) -> SurfelBuffers:
@@ -172,7 +201,7 @@ def composite(surfel_color, gaussian: GaussianBuffers, surfel_weight: float = 1.
     _lib.check(_lib.lib().ges_composite(sc.data_ptr(), gc.data_ptr(), gw.data_ptr(), float(surfel_weight),
                                         img.data_ptr(), n, torch.cuda.current_stream(dev).cuda_stream),
                "ges_composite")
-    return img.cpu().numpy() if as_np else img
+    return _np(img) if as_np else img
 
 
 def smooth_geometry(surfel_buffers: SurfelBuffers, gaussian: GaussianBuffers):
@@ -193,5 +222,5 @@ def smooth_geometry(surfel_buffers: SurfelBuffers, gaussian: GaussianBuffers):
                                               torch.cuda.current_stream(dev).cuda_stream),
                "ges_smooth_geometry")
     if as_np:
-        return d.cpu().numpy(), nrm.cpu().numpy()
+        return _numpy(_host(d), _host(nrm))
     return d, nrm
