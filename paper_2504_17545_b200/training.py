@@ -39,6 +39,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .forward import _host, _numpy
 from .renderer import DeviceScene, camera_struct, default_renderer, settings_struct
 from .types import GaussianKind, GradientSet
 
@@ -102,7 +103,7 @@ def _pass_settings(st: TrainSettings, **kw):
 def _out(t, to_numpy, dtype):
     if t is None or not to_numpy:
         return t
-    return t.detach().cpu().numpy().astype(dtype, copy=False)
+    return _numpy(_host(t.detach()))[0].astype(dtype, copy=False)
 
 
 def _as_dev(a, dev, dtype=torch.float32):
@@ -309,7 +310,8 @@ def backward(frame: TrainFrame, g_image, *, g_blend_depth=None, g_blend_normal=N
                    "frozen surfel backward")
     if not to_numpy:
         return GradientSet(**out)
-    return GradientSet(**{k: v.cpu().numpy() for k, v in out.items()})
+    keys = list(out)   # pinned copies, all queued before one synchronisation (forward._host)
+    return GradientSet(**dict(zip(keys, _numpy(*(_host(out[k]) for k in keys)))))
 
 
 def contribution_scores(scene, cams, settings: TrainSettings | None = None, cache_keys=None, *,

@@ -67,8 +67,22 @@ def main():
     wall = (time.perf_counter() - t0) / a.steps
     fwd = float(np.median([e[0].elapsed_time(e[1]) for e in evs]))
     bwd = float(np.median([e[1].elapsed_time(e[2]) for e in evs]))
+    # the reference-facing form: NumPy frame out, NumPy cotangent in, NumPy gradients out
+    tgt = target.cpu().numpy()
+
+    def step_np():
+        fr = TR.render_training(sc, cam, st, cache_key=0, device_scene=ds)
+        return TR.backward(fr, 2.0 * (fr.image - tgt))
+
+    for _ in range(2):
+        step_np()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        step_np()
+    np_wall = (time.perf_counter() - t0) / 3
     print(json.dumps({"metric": "train_step_ms", "value": fwd + bwd, "unit": "ms", "forward_ms": fwd,
-                      "backward_ms": bwd, "wall_ms": wall * 1e3, "steps": a.steps, "warmup": a.warmup,
+                      "backward_ms": bwd, "wall_ms": wall * 1e3, "numpy_wall_ms": np_wall * 1e3,
+                      "steps": a.steps, "warmup": a.warmup,
                       "config": {"workload": f"config{a.config} joint-stage step, {a.kind} Gaussians, ss={a.ss}",
                                  "surfels": ds.n_surfels, "gaussians": ds.n_gaussians,
                                  "resolution": [cam.width, cam.height]}}))
