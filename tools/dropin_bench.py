@@ -28,3 +28,13 @@ for to_np in (False, True):
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / n
     print(f"render(to_numpy={to_np}): {dt * 1e3:.2f} ms/frame ({1 / dt:.0f} frames/s)")
+
+# scene (re)pack: what a caller pays when it hands over new parameter arrays
+from paper_2504_17545_b200.renderer import DeviceScene  # noqa: E402
+for k in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ds = DeviceScene(sc)
+    torch.cuda.synchronize()
+    print(f"DeviceScene pack #{k}: {(time.perf_counter() - t0) * 1e3:.1f} ms")
+    del ds
