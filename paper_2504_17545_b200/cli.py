@@ -1,10 +1,12 @@
 """Command line front end for the GPU render path,
-mirroring the reference's ``ges render`` / ``ges path`` (``cli.py:126-174``):
+mirroring the reference's ``ges render`` / ``ges path`` / ``ges eval`` (``cli.py:126-174``):
 
   python -m paper_2504_17545_b200 render --model m.ges --camera cams.json --out o.png
          [--view K] [--ss {1,4}] [--layer {full,surfels,gaussians}] [--mip] [--background R G B]
   python -m paper_2504_17545_b200 path --model m.ges --camera cams.json --out DIR
          [--frames N] [--radius-scale S] [--ss {1,4}]
+  python -m paper_2504_17545_b200 eval --model m.ges --scene DATASET_DIR --out report.json
+         [--test-every N] [--ss {1,4}]
 
 Camera files use the reference's dataset entries ({fx, fy, cx, cy, width,
 height, w2c[16]}, ``datasets.py:125-137``).  Exit codes: 0 ok, 1 error,
@@ -111,6 +113,20 @@ def cmd_path(args) -> int:
     return 0
 
 
+def cmd_eval(args) -> int:
+    """``ges eval`` (cli.py:138-144): render the dataset's test views on the
+    GPU and write the PSNR/SSIM report (metrics.evaluate)."""
+    from .datasets import load_dataset
+    from .forward import RenderSettings
+    from .metrics import evaluate
+    scene, _ = load_ges(args.model)
+    dataset = load_dataset(Path(args.scene), test_every=args.test_every)
+    rep = evaluate(scene, dataset, settings=RenderSettings(supersample=args.ss))
+    Path(args.out).write_text(rep.to_json())
+    print(f"mean PSNR {rep.mean_psnr:.2f} dB  SSIM {rep.mean_ssim:.4f} -> {args.out}")
+    return 0
+
+
 def build_parser():
     p = argparse.ArgumentParser(prog="paper_2504_17545_b200")
     sub = p.add_subparsers(dest="cmd", required=True)
@@ -133,6 +149,13 @@ def build_parser():
     pa.add_argument("--frames", type=int, default=16)
     pa.add_argument("--radius-scale", type=float, default=1.0)
     pa.set_defaults(fn=cmd_path)
+    ev = sub.add_parser("eval", help="PSNR/SSIM of a model on a dataset's test views")
+    ev.add_argument("--model", required=True)
+    ev.add_argument("--scene", required=True, help="dataset directory (cameras.json + images)")
+    ev.add_argument("--out", required=True)
+    ev.add_argument("--test-every", type=int, default=8)
+    ev.add_argument("--ss", type=int, default=4, choices=[1, 4])
+    ev.set_defaults(fn=cmd_eval)
     return p
 
 
