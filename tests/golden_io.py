@@ -17,9 +17,9 @@ GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def names():
-    """Render golden cases (the .ges fixtures have their own *_load.npz)."""
+    """Render golden cases (the .ges, training and metrics fixtures are separate)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
-                  if not os.path.basename(p).startswith(("ges_", "train_")))
+                  if not os.path.basename(p).startswith(("ges_", "train_", "metrics")))
 
 
 def train_names():
