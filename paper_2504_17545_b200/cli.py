@@ -4,7 +4,7 @@ mirroring the reference's ``ges render`` / ``ges path`` / ``ges eval`` (``cli.py
   python -m paper_2504_17545_b200 render --model m.ges --camera cams.json --out o.png
          [--view K] [--ss {1,4}] [--layer {full,surfels,gaussians}] [--mip] [--background R G B]
   python -m paper_2504_17545_b200 path --model m.ges --camera cams.json --out DIR
-         [--frames N] [--radius-scale S] [--ss {1,4}]
+         [--target X Y Z] [--frames N] [--angle RAD] [--ss {1,4}]
   python -m paper_2504_17545_b200 eval --model m.ges --scene DATASET_DIR --out report.json
          [--test-every N] [--ss {1,4}]
 
@@ -17,14 +17,13 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import sys
 from pathlib import Path
 
 import numpy as np
 
 from .gesfile import load_ges
-from .types import Camera, look_at
+from .types import Camera
 
 
 def camera_from_entry(e: dict) -> Camera:
@@ -66,50 +65,41 @@ def cmd_render(args) -> int:
     return 0
 
 
-def orbit_path(base: Camera, frames: int, radius_scale: float = 1.0):
-    """Frames on a circle through the base camera's eye around its look-at
-    point at the same distance (a multi-view batch like cli.py:154-174)."""
-    R = np.asarray(base.world_to_camera)[:3, :3]
-    eye = np.asarray(base.position)
-    fwd = R[2]
-    target = eye + fwd * np.linalg.norm(eye) * 1.0
-    rad = np.linalg.norm(eye - target) * radius_scale
-    off = eye - target
-    ang0 = math.atan2(off[1], off[0])
-    cams = []
-    for k in range(frames):
-        a = ang0 + 2 * math.pi * k / frames
-        e = target + np.array([rad * math.cos(a), rad * math.sin(a), off[2]])
-        cams.append(Camera(base.fx, base.fy, base.cx, base.cy, base.width, base.height, look_at(e, target)))
-    return cams
-
-
 def cmd_path(args) -> int:
+    """``ges path`` (cli.py:154-174): the small orbit of metrics.camera_path
+    rendered as one batch on the GPU (views pipelined over CUDA streams),
+    frames written as PNG, plus path.json and the consistency probe
+    (probe.json, computed on the device)."""
     import torch
 
     from .forward import _device
+    from .metrics import camera_path, consistency_probe
     from .multiview import ViewBatchRenderer
     from .renderer import SCENE_CACHE, default_renderer
     scene, _ = load_ges(args.model)
     base = camera_from_entry(_load_cams(args.camera)[0])
-    cams = orbit_path(base, args.frames, args.radius_scale)
+    cams = camera_path(base, args.target, frames=args.frames, angle=args.angle)
     out_dir = Path(args.out)
     out_dir.mkdir(parents=True, exist_ok=True)
     dev = _device()
     ds = SCENE_CACHE.get(scene, dev)
-    vb = ViewBatchRenderer(default_renderer(dev), ds, cams, _settings(args), want=("image_rgba8",))
-    for c, fr in zip(vb.cams, vb.frames):          # size the pair lists, then render the batch
-        vb.r.render(ds, c, vb.settings, frame=fr, check=True)
-    rgba = vb.render(check=False)
+    vb = ViewBatchRenderer(default_renderer(dev), ds, cams, _settings(args), want=("image", "image_rgba8"),
+                           streams=4)
+    for r in vb.pool:                             # size every workspace's pair lists, then render the batch
+        for c, fr in zip(vb.cams, vb.frames):
+            r.render(ds, c, vb.settings, frame=fr, check=True)
+    vb.render(check=False)
     torch.cuda.synchronize(dev)
     if vb.overflowed():
-        rgba = vb.render(check=True)
+        vb.render(check=True)
     from PIL import Image
-    frames = rgba if isinstance(rgba, list) else list(rgba.unbind(0))
-    for k, f in enumerate(frames):
+    rgba = vb.rgba if isinstance(vb.rgba, list) else list(vb.rgba.unbind(0))
+    for k, f in enumerate(rgba):
         Image.fromarray(f[..., :3].cpu().numpy()).save(out_dir / f"frame_{k:04d}.png")
+    probe = consistency_probe(None, cams, images=torch.stack([fr.image for fr in vb.frames]))
     (out_dir / "path.json").write_text(json.dumps([camera_to_entry(c) for c in cams], indent=1))
-    print(f"wrote {len(frames)} frames to {out_dir}")
+    (out_dir / "probe.json").write_text(json.dumps(probe, indent=1))
+    print(f"wrote {len(rgba)} frames to {out_dir}")
     return 0
 
 
@@ -131,11 +121,11 @@ def build_parser():
     p = argparse.ArgumentParser(prog="paper_2504_17545_b200")
     sub = p.add_subparsers(dest="cmd", required=True)
 
-    def common(sp):
+    def common(sp, ss_default=4):
         sp.add_argument("--model", required=True)
         sp.add_argument("--camera", required=True)
         sp.add_argument("--out", required=True)
-        sp.add_argument("--ss", type=int, default=4, choices=[1, 4])
+        sp.add_argument("--ss", type=int, default=ss_default, choices=[1, 4])
         sp.add_argument("--layer", default="full", choices=["full", "surfels", "gaussians"])
         sp.add_argument("--mip", action="store_true")
         sp.add_argument("--background", type=float, nargs=3, default=[0.0, 0.0, 0.0])
@@ -144,10 +134,11 @@ def build_parser():
     common(r)
     r.add_argument("--view", type=int, default=0)
     r.set_defaults(fn=cmd_render)
-    pa = sub.add_parser("path", help="render an orbit of views as a batch")
-    common(pa)
-    pa.add_argument("--frames", type=int, default=16)
-    pa.add_argument("--radius-scale", type=float, default=1.0)
+    pa = sub.add_parser("path", help="render an orbit path as a batch and probe consistency")
+    common(pa, ss_default=1)
+    pa.add_argument("--target", type=float, nargs=3, default=[0.0, 0.0, 0.0])
+    pa.add_argument("--frames", type=int, default=24)
+    pa.add_argument("--angle", type=float, default=0.02, help="radians per frame")
     pa.set_defaults(fn=cmd_path)
     ev = sub.add_parser("eval", help="PSNR/SSIM of a model on a dataset's test views")
     ev.add_argument("--model", required=True)

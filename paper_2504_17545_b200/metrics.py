@@ -133,3 +133,61 @@ def evaluate(scene, dataset, views=None, settings=None) -> EvalReport:
     rep.mean_ssim = float(np.mean(rep.per_view_ssim)) if rep.per_view_ssim else 0.0
     rep.ms_per_frame = float(np.mean(times) * 1000.0) if times else 0.0
     return rep
+
+
+# --------------------------------------------------------------------------- view consistency
+def camera_path(base, target, *, frames: int, angle: float = 0.02, radius_scale: float = 1.0) -> list:
+    """Small orbit around ``target`` through the base camera's eye, ``angle``
+    radians per frame (metrics.py:79-95)."""
+    from .types import Camera, look_at
+    target = np.asarray(target, dtype=np.float64)
+    rel = np.asarray(base.position, dtype=np.float64) - target
+    r = float(np.linalg.norm(rel[:2]))
+    a0 = math.atan2(rel[1], rel[0])
+    cams = []
+    for k in range(frames):
+        a = a0 + angle * k
+        eye = target + np.array([r * radius_scale * math.cos(a), r * radius_scale * math.sin(a), rel[2]])
+        cams.append(Camera(base.fx, base.fy, base.cx, base.cy, base.width, base.height, look_at(eye, target)))
+    return cams
+
+
+def motion_bound(prev_img, flow_px: float, quantum: float = 1.0 / 255.0) -> float:
+    """Max finite-difference image gradient x max pixel displacement + the
+    clamp quantum (metrics.py:98-107)."""
+    gy, gx = np.gradient(np.asarray(prev_img, dtype=np.float64), axis=(0, 1))
+    return float(np.maximum(np.abs(gx), np.abs(gy)).max()) * flow_px + quantum
+
+
+def max_flow_px(cam_a, cam_b, points) -> float:
+    """Largest screen displacement of the anchor points between two views (metrics.py:110-114)."""
+    pa = cam_a.project(cam_a.to_camera(points))
+    pb = cam_b.project(cam_b.to_camera(points))
+    return float(np.linalg.norm(pa - pb, axis=1).max())
+
+
+def consistency_probe(render_fn, cams: list, anchor_points=None, images=None) -> dict:
+    """Per-pair max / mean absolute pixel change along a path, plus the
+    camera-motion bounds when anchor points are given (metrics.py:116-140).
+    ``images`` may be a (V, H, W, 3) device tensor: the changes are then
+    computed on the device in float64."""
+    if not cams:
+        raise ValueError("empty camera path")
+    if images is None:
+        images = [render_fn(c) for c in cams]
+    if torch.is_tensor(images):
+        d = (images[1:].double() - images[:-1].double()).abs().flatten(1)
+        max_change = [float(v) for v in d.max(dim=1).values.cpu()] if len(images) > 1 else []
+        mean_change = [float(v) for v in d.mean(dim=1).cpu()] if len(images) > 1 else []
+        imgs = None
+    else:
+        imgs = [np.asarray(im, dtype=np.float64) for im in images]
+        max_change = [float(np.abs(a - b).max()) for a, b in zip(imgs, imgs[1:])]
+        mean_change = [float(np.abs(a - b).mean()) for a, b in zip(imgs, imgs[1:])]
+    bounds = []
+    if anchor_points is not None and len(cams) > 1:
+        if imgs is None:
+            imgs = [im.double().cpu().numpy() for im in images]
+        for (ca, cb), img in zip(zip(cams, cams[1:]), imgs):
+            bounds.append(motion_bound(img, max_flow_px(ca, cb, anchor_points)))
+    return {"max_change": max_change, "mean_change": mean_change, "bounds": bounds}

@@ -12,8 +12,9 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from ges.losses import ssim  # noqa: E402  (reference, read-only)
-from ges.metrics import psnr  # noqa: E402
+import ges  # noqa: E402  (reference, read-only)
+from ges.losses import ssim  # noqa: E402
+from ges.metrics import camera_path, consistency_probe, psnr  # noqa: E402
 
 
 def main():
@@ -28,6 +29,18 @@ def main():
         out[f"{name}_ssim"] = np.float64(ssim(a, b))
     out["same_psnr"] = np.float64(psnr(out["rgb_a"], out["rgb_a"]))   # +inf
     out["same_ssim"] = np.float64(ssim(out["rgb_a"], out["rgb_a"]))
+    # camera_path / consistency_probe (metrics.py:79-140)
+    w2c = ges.look_at(np.array([3.0, 1.0, 1.5]), np.zeros(3))
+    base = ges.Camera(60.0, 58.0, 31.5, 24.0, 64, 48, w2c)
+    cams = camera_path(base, [0.1, -0.2, 0.0], frames=5, angle=0.05)
+    out["path_base_w2c"] = w2c
+    out["path_w2c"] = np.stack([c.world_to_camera for c in cams])
+    imgs = rng.random((5, 48, 64, 3))
+    pts = rng.normal(size=(20, 3))
+    probe = consistency_probe(None, cams, anchor_points=pts, images=list(imgs))
+    out["probe_images"], out["probe_points"] = imgs, pts
+    for k in ("max_change", "mean_change", "bounds"):
+        out[f"probe_{k}"] = np.array(probe[k])
     np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
     print({k: float(v) for k, v in out.items() if v.ndim == 0})
 

@@ -67,6 +67,20 @@ def test_cli_path_and_errors(tmp_path):
                    str(tmp_path / "cams.json"), "--out", str(tmp_path / "p"), "--frames", "5"])
     assert rc == 0
     assert len(list((tmp_path / "p").glob("frame_*.png"))) == 5
+    # cli.py:154-174: the small orbit (metrics.camera_path) and the consistency probe
+    from paper_2504_17545_b200 import metrics as M
+    from paper_2504_17545_b200.forward import RenderSettings, render
+    from paper_2504_17545_b200.gesfile import load_ges
+    cams = M.camera_path(_cam(z), [0.0, 0.0, 0.0], frames=5, angle=0.02)
+    path = json.loads((tmp_path / "p" / "path.json").read_text())
+    assert np.allclose([e["w2c"] for e in path], [c.world_to_camera.reshape(-1) for c in cams])
+    probe = json.loads((tmp_path / "p" / "probe.json").read_text())
+    scene, _ = load_ges(os.path.join(GOLD, "ges_2d_rgb.ges"))
+    imgs = [render(scene, c, RenderSettings(supersample=1)).image for c in cams]
+    want = M.consistency_probe(None, cams, images=imgs)
+    assert len(probe["max_change"]) == 4 and probe["bounds"] == []
+    assert np.allclose(probe["max_change"], want["max_change"], atol=1e-5)
+    assert np.allclose(probe["mean_change"], want["mean_change"], atol=1e-6)
     assert cli.main(["render", "--model", str(tmp_path / "missing.ges"), "--camera",
                      str(tmp_path / "cams.json"), "--out", str(tmp_path / "x.png")]) == 1
 

@@ -100,3 +100,23 @@ def test_evaluate_and_eval_command_on_gpu(tmp_path):
                      "--test-every", "3"]) == 0
     r = json.loads(out.read_text())
     assert len(r["per_view_psnr"]) == 2 and r["mean_psnr"] > 40.0 and r["mean_ssim"] > 0.99
+
+
+def test_camera_path_and_probe_match_reference():
+    import torch
+
+    from paper_2504_17545_b200.types import Camera
+    g = np.load(GOLD)
+    base = Camera(60.0, 58.0, 31.5, 24.0, 64, 48, g["path_base_w2c"])
+    cams = M.camera_path(base, [0.1, -0.2, 0.0], frames=5, angle=0.05)
+    assert np.allclose(np.stack([c.world_to_camera for c in cams]), g["path_w2c"], rtol=0, atol=1e-12)
+    imgs = g["probe_images"]
+    p = M.consistency_probe(None, cams, anchor_points=g["probe_points"], images=list(imgs))
+    for k in ("max_change", "mean_change", "bounds"):
+        assert np.allclose(p[k], g[f"probe_{k}"], rtol=1e-12, atol=0)
+    # the tensor form (device batches in the path command) gives the same changes
+    pt = M.consistency_probe(None, cams, images=torch.as_tensor(imgs))
+    assert np.allclose(pt["max_change"], g["probe_max_change"], rtol=1e-12)
+    assert np.allclose(pt["mean_change"], g["probe_mean_change"], rtol=1e-12) and pt["bounds"] == []
+    with pytest.raises(ValueError):
+        M.consistency_probe(None, [])
