@@ -7,6 +7,7 @@ mirroring the reference's ``ges render`` / ``ges path`` / ``ges eval`` (``cli.py
          [--target X Y Z] [--frames N] [--angle RAD] [--ss {1,4}]
   python -m paper_2504_17545_b200 eval --model m.ges --scene DATASET_DIR --out report.json
          [--test-every N] [--ss {1,4}]
+  python -m paper_2504_17545_b200 export --model m.ges --out n.ges
 
 Camera files use the reference's dataset entries ({fx, fy, cx, cy, width,
 height, w2c[16]}, ``datasets.py:125-137``).  Exit codes: 0 ok, 1 error,
@@ -117,6 +118,15 @@ def cmd_eval(args) -> int:
     return 0
 
 
+def cmd_export(args) -> int:
+    """``ges export`` (cli.py:147-151): re-write a model in the normal layout."""
+    from .gesfile import save_ges
+    scene, info = load_ges(args.model)
+    save_ges(scene, args.out, rgb_surfels=bool(info["rgb_surfels"]))
+    print(f"wrote {args.out}")
+    return 0
+
+
 def build_parser():
     p = argparse.ArgumentParser(prog="paper_2504_17545_b200")
     sub = p.add_subparsers(dest="cmd", required=True)
@@ -147,6 +157,10 @@ def build_parser():
     ev.add_argument("--test-every", type=int, default=8)
     ev.add_argument("--ss", type=int, default=4, choices=[1, 4])
     ev.set_defaults(fn=cmd_eval)
+    x = sub.add_parser("export", help="re-export a model file (normalizes layout)")
+    x.add_argument("--model", required=True)
+    x.add_argument("--out", required=True)
+    x.set_defaults(fn=cmd_export)
     return p
 
 

@@ -60,3 +60,16 @@ def test_error_cases(tmp_path):
     bad.write_bytes(HEADER.pack(magic, 2, deg, flags, ns, ng) + good[HEADER.size:])
     with pytest.raises(GesFileError, match="version"):
         load_ges(bad)
+
+
+def test_cli_export_roundtrip(tmp_path):
+    """``export`` (cli.py:147-151) re-writes a model that loads to the same arrays."""
+    from paper_2504_17545_b200 import cli
+    src = os.path.join(GOLD, "ges_2d_rgb.ges")
+    out = tmp_path / "re.ges"
+    assert cli.main(["export", "--model", src, "--out", str(out)]) == 0
+    a, ia = load_ges(src)
+    b, ib = load_ges(out)
+    assert ia["rgb_surfels"] == ib["rgb_surfels"]
+    assert np.array_equal(a.surfels.pos, b.surfels.pos) and np.array_equal(a.gaussians.sh, b.gaussians.sh)
+    assert cli.main(["export", "--model", str(tmp_path / "missing.ges"), "--out", str(out)]) == 1
