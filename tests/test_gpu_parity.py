@@ -97,6 +97,42 @@ def test_config2_tile_sample():
     assert rep["pixels"] >= 12 * 256
 
 
+def test_config2_full_frame_properties():
+    """Every pixel of the full config-2 frame through size-independent
+    properties: the fused render equals its split entry points (surfel pass
+    alone: identical winner/depth maps -- min over packed keys is order-free;
+    Gaussian pass against that depth: the same accumulations to fp32 order
+    noise; composite of the two: the image), coverage == finite depth, the
+    winner's surfel is in view, and layer modes are consistent."""
+    import torch
+    sc = S.config_scene(2)
+    cam = S.config_cameras(2)[0]
+    full = G.render(sc, cam, to_numpy=False)
+    sb = G.rasterize_surfels(sc, cam, to_numpy=False)
+    assert torch.equal(full.surfels.winner, sb.winner)
+    assert torch.equal(full.surfels.depth, sb.depth)
+    assert torch.equal(full.surfels.coverage, torch.isfinite(full.surfels.depth))
+    assert torch.equal(full.surfels.coverage, full.surfels.winner >= 0)
+    assert float(full.surfels.coverage.float().mean()) > 0.5
+    gb = G.accumulate_gaussians(sc, cam, sb.depth, to_numpy=False)
+    assert torch.allclose(gb.weight, full.gaussians.weight, rtol=1e-5, atol=1e-6)
+    assert torch.allclose(gb.color, full.gaussians.color, rtol=1e-5, atol=1e-6)
+    img = G.composite(full.surfels.color, full.gaussians)
+    assert float((img - full.image).abs().max()) <= 1e-6
+    so = G.render(sc, cam, G.RenderSettings(layers="surfels_only"), to_numpy=False)
+    assert torch.equal(so.image, full.surfels.color) and float(so.gaussians.weight.abs().max()) == 0.0
+    # winners are surfels whose centre projects near the pixel (within the largest disc radius)
+    ys, xs = torch.nonzero(full.surfels.coverage, as_tuple=True)
+    pick = torch.randperm(len(ys), generator=torch.Generator().manual_seed(0))[:2000].to(ys.device)
+    w = full.surfels.winner[ys[pick], xs[pick]].cpu().numpy()
+    pc = sc.surfels.pos[w] @ np.asarray(cam.world_to_camera)[:3, :3].T + np.asarray(cam.world_to_camera)[:3, 3]
+    px = cam.fx * pc[:, 0] / pc[:, 2] + cam.cx
+    py = cam.fy * pc[:, 1] / pc[:, 2] + cam.cy
+    rmax = 3.33 * float(np.exp(sc.surfels.log_scale.max())) * cam.fx / pc[:, 2].min()
+    d = np.hypot(px - xs[pick].cpu().numpy() - 0.5, py - ys[pick].cpu().numpy() - 0.5)
+    assert float(d.max()) <= rmax + 1.0
+
+
 # ---- known-answer tests (test_forward.py:79-145) --------------------------------
 def frontal(color=0.2, depth=3.0, scale=1.0):
     sh = np.zeros((1, 1, 3))
