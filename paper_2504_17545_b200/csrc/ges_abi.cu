@@ -182,9 +182,9 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, tp * grid,
                      log2i(tp * grid)};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, tp, log2i(tp)};
-    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, nullptr, f.cnt_s, nullptr, f.scull}, s)))
+    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, f.cnt_s, nullptr, f.scull}, s)))
         return cuda_fail(e, "surfel preprocess");
-    if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, nullptr, f.g_nrm, f.cnt_g, nullptr, f.gcull}, s)))
+    if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, f.g_nrm, f.cnt_g, nullptr, f.gcull}, s)))
         return cuda_fail(e, "gaussian preprocess");
     mark(2);
     if ((e = launch_scan(bs, bg, status, s)))
@@ -390,7 +390,7 @@ int ges_backward_gaussians(const ges_scene_t* sc, const ges_scene_src_t* src, in
     scs.n_surfels = 0;
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, 0, f.ntiles, f.ntx, TILE, 4};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE, 4};
-    PrepOut po{f.grec, nullptr, f.g_nrm, f.cnt_g, sc->gaussian_dim == 2 ? aux : nullptr, f.gcull};
+    PrepOut po{f.grec, f.g_nrm, f.cnt_g, sc->gaussian_dim == 2 ? aux : nullptr, f.gcull};
     if ((e = launch_gauss_prep(scs, cg, gg, s2, po, s))) return cuda_fail(e, "gaussian preprocess");
     if ((e = launch_scan(bs, bg, status, s))) return cuda_fail(e, "tile scan");
     if ((e = launch_fill(f.scull, 0, bs, f.gcull, ng, sc->gaussian_dim, bg, slabs, s))) return cuda_fail(e, "tile fill");
@@ -446,7 +446,7 @@ int ges_gaussian_contributions(const ges_scene_t* sc, const ges_scene_src_t* src
     scs.n_surfels = 0;
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, 0, f.ntiles, f.ntx, TILE, 4};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, TILE, 4};
-    PrepOut po{f.grec, nullptr, f.g_nrm, f.cnt_g, nullptr, f.gcull};
+    PrepOut po{f.grec, f.g_nrm, f.cnt_g, nullptr, f.gcull};
     if ((e = launch_gauss_prep(scs, cg, gg, s2, po, s))) return cuda_fail(e, "gaussian preprocess");
     if ((e = launch_scan(bs, bg, status, s))) return cuda_fail(e, "tile scan");
     if ((e = launch_fill(f.scull, 0, bs, f.gcull, ng, sc->gaussian_dim, bg, slabs, s))) return cuda_fail(e, "tile fill");

@@ -9,7 +9,6 @@ namespace ges {
 
 struct PrepOut {
     void* rec;              // SurfRec / GaussRec / Gauss2Rec per primitive
-    float4* rgb;            // per-primitive view colour (surfels; Gaussians 3D keep it in rec)
     float4* nrm;            // per-primitive camera-facing normal (surfels; Gaussians if geometry)
     uint32_t* bin_count;    // per-(tile, slab) pair counters (zeroed by the caller)
     float4* aux;            // 2D Gaussians, training backward only: (a1/s1).d and (a2/s2).d
@@ -54,7 +53,6 @@ struct TileArgs {
     float gcx, gcy, gifx, gify;
     const void* grec;
     const float4* gcull;          // dense Gaussian cull records
-    const float4* g_rgb;          // 2D Gaussians: colours
     const float4* g_nrm;          // with_geometry normals
     const uint32_t* g_list;
     BinPass gbin;
