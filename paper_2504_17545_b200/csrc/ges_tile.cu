@@ -1,10 +1,10 @@
 // K3 + K6 fused: one CTA (8 warps) per tile -- 16x16 base pixels with one
 // pixel per thread, or 32x32 with a 2x2 pixel block per thread (PX = 2).
 //
-// Pass 1 (forward.py:127-209): every thread keeps, per (sub)sample, the packed
-// key (float_bits(t) << 32 | surfel_id) of the nearest covering surfel in
-// registers; min over keys == argmin over hit depth with ties to the lowest
-// index, exactly np.argmin over the ascending candidate list (forward.py:187).
+// Pass 1 (forward.py:127-209): every thread keeps, per (sub)sample, the hit
+// depth and source id of the nearest covering surfel in registers, compared
+// lexicographically: argmin over hit depth with ties to the lowest index,
+// exactly np.argmin over the ascending candidate list (forward.py:187).
 // No atomics: the z-buffer is private per pixel.
 //
 // Pass 2 (forward.py:248-381): order-independent, depth-gated accumulation of
@@ -58,6 +58,8 @@ template <int WPC>
 struct __align__(16) TileSmem {
     float4 st[4][32 * WPC];     // per-warp slots (32 each): pass-1 surfel coefficients, pass-2
                                 // Gaussian records, then the colour tasks
+    uint32_t wpk[4][32 * WPC];  // per lane: packed indices of its samples' winners, parked
+                                // in shared memory through the Gaussian pass
     float4 rmax[WPC][2];        // per warp: max best depth of each of its 4 x 2 regions of
                                 // 2 x 2 lanes (pass-1 culling)
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
@@ -270,10 +272,13 @@ __device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, Smem& s
 // in pass 1 and PX x PX pixels in pass 2.
 template <int SS, int PX>
 __host__ __device__ constexpr int tile_wpc() { return (PX == 2 || SS == 2) ? GES_TILE_WPC : GES_TILE_WPC1; }
+#ifndef GES_TILE_MINW2
+#define GES_TILE_MINW2 (GES_TILE_MINB2 * 8)   // resident warps per SM, 4-sample variants (64 registers)
+#endif
 template <int SS, int PX>
-__host__ __device__ constexpr int tile_min_blocks() {   // resident CTAs per SM: 4 (64 registers) or 6 (40) tiles' worth of warps
-    return ((PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6) * NWARP / tile_wpc<SS, PX>() > 32
-               ? 32 : ((PX == 2 || SS == 2) ? GES_TILE_MINB2 : 6) * NWARP / tile_wpc<SS, PX>();
+__host__ __device__ constexpr int tile_min_blocks() {   // resident CTAs per SM (at most 32)
+    return ((PX == 2 || SS == 2) ? GES_TILE_MINW2 : 48) / tile_wpc<SS, PX>() > 32
+               ? 32 : ((PX == 2 || SS == 2) ? GES_TILE_MINW2 : 48) / tile_wpc<SS, PX>();
 }
 
 template <int SS, int PX, int MODE, int GK, bool GEOM>
@@ -308,21 +313,24 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
         if (gbeg + warp * 32 + lane < gend) gid = a.g_list[gbeg + warp * 32 + lane];
     }
 
-    // best[s]: packed (t_bits << 32 | source id) of the nearest surfel hit so
-    // far; bp[s]: its packed index (SH address of the deferred colour), looked
-    // up once after pass 1
-    unsigned long long best[NS];
+    // bid[s]: source id of the nearest surfel hit so far (~0u: none); with
+    // bt[s] (its hit depth) the pair (bt, bid) is compared lexicographically,
+    // == np.argmin with lowest-index ties (forward.py:187); bp[s]: the
+    // winner's packed index (SH address of the deferred colour), looked up
+    // once after pass 1
+    uint32_t bid[NS];
     uint32_t bp[NS];
-    uint32_t covm = 0;   // bit s: sample s covered (best[] is dead after pass 1)
+    uint32_t covm = 0;   // bit s: sample s covered (bt[], bid[] are dead after pass 1)
 
     // ------------------------------------------------------------ pass 1
     if constexpr (MODE & 1) {
-        // tb[s]: the best t inflated by 1e-5 (candidate filter and culling bound;
-        // samples outside the image start at 0 so they never take work or block culling)
+        // bt[s]: the best hit depth (candidate filter with a 1e-5 margin and
+        // culling bound; samples outside the image start at 0 so they never
+        // take work or block culling)
         // pe: the near-parallel threshold 1e-8|d|, one per thread (the max over
         // its samples: the 2x2 block's |d| differ by < 1e-3 relative, inside the
         // flagged grazing band of the parity rule)
-        float tb[NS], pe = 0.f;
+        float bt[NS], pe = 0.f;
         const float lx0 = (float)(G * plx), ly0 = (float)(G * ply);
 #pragma unroll
         for (int gy = 0; gy < G; ++gy)
@@ -331,9 +339,9 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 const int X = bx * SS + gx, Y = by * SS + gy;
                 const float dxn = ((float)X + 0.5f - a.rcx) * a.rifx, dyn = ((float)Y + 0.5f - a.rcy) * a.rify;
                 pe = fmaxf(pe, fmaf(dxn, dxn, dyn * dyn));
-                best[gy * G + gx] = ~0ull;
+                bid[gy * G + gx] = ~0u;
                 const bool in = bx + gx / SS < a.W && by + gy / SS < a.H;
-                tb[gy * G + gx] = in ? INFINITY : 0.f;
+                bt[gy * G + gx] = in ? INFINITY : 0.f;
             }
         pe = PARALLEL_EPS_F * sqrtf(pe + 1.0f);   // max over the samples of 1e-8 |d|
         // Depth culling bounds, refreshed after every chunk: the max over each
@@ -343,9 +351,10 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
         // before the whole patch is covered.
         float* const rm = reinterpret_cast<float*>(sm.rmax[wl]);
         auto patch_depth = [&]() {
-            float m = tb[0];
+            float m = bt[0];
 #pragma unroll
-            for (int s = 1; s < NS; ++s) m = fmaxf(m, tb[s]);
+            for (int s = 1; s < NS; ++s) m = fmaxf(m, bt[s]);
+            m *= 1.00001f;   // margin-inflated: culling stays conservative
             return region_reduce(m, rm, lane);
         };
         if (lane < 8) rm[lane] = INFINITY;
@@ -417,6 +426,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 if (lane == 0) GES_STAT(3, 1);
                 if (lane == 0) GES_STAT(12, wmx == INFINITY);
                 const float4 A = sm.st[0][j], B = sm.st[1][j];
+                const float Awf = A.w * 0.99999f;   // candidate filter t <= 1.00001 bt (margin vs rounding)
                 // den, U, V at the thread's first sample, then stepped by the
                 // per-sample increments across its G x G block
                 const float den0 = fmaf(A.z, ly0, fmaf(A.y, lx0, A.x));
@@ -436,20 +446,19 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                             const bool inside = bx + gx / SS < a.W && by + gy / SS < a.H;
                             const bool cov = den > pe && r2 <= den * den;
                             if (inside) GES_STAT(cov ? 14 : 13, 1);
-                            if (inside && cov && tb[s] == INFINITY) GES_STAT(15, 1);
+                            if (inside && cov && bid[s] == ~0u) GES_STAT(15, 1);
                         }
 #endif
                         // coverage u^2+v^2 <= R^2, |n.d| > eps|d| and t no later than the
                         // current best (all multiplied out, den > 0 <=> t > 0); the exact
                         // t > 0.01 and packed-key comparison run only for candidates
-                        if (den > pe && r2 <= den * den && A.w <= tb[s] * den) {
+                        if (den > pe && r2 <= den * den && Awf <= bt[s] * den) {
                             const float t = A.w * rcp_ftz(den);   // den > 1e-8|d|; 2 ulp: ties are flagged
-                            const unsigned long long key =
-                                ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(C.z);
+                            const uint32_t sid = __float_as_uint(C.z);
                             GES_STAT(4, 1);
-                            if (t > NEAR_F && key < best[s]) {
-                                best[s] = key;
-                                tb[s] = t * 1.00001f;   // margin-inflated best depth
+                            if (t > NEAR_F && (t < bt[s] || (t == bt[s] && sid < bid[s]))) {
+                                bt[s] = t;
+                                bid[s] = sid;
                             }
                         }
                     }
@@ -462,43 +471,44 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
         // the Gaussian pass
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-            bp[s] = best[s] != ~0ull ? __ldg(a.s_pack + (uint32_t)best[s]) : 0u;
-            covm |= (best[s] != ~0ull ? 1u : 0u) << s;
+            bp[s] = bid[s] != ~0u ? __ldg(a.s_pack + bid[s]) : 0u;
+            covm |= (bid[s] != ~0u ? 1u : 0u) << s;
         }
-        asm volatile("" : "+r"(covm));   // materialise now so best[] dies before pass 2
+        asm volatile("" : "+r"(covm));   // materialise now so bid[] dies before pass 2
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-            if (best[s] != ~0ull) {
+            if (bid[s] != ~0u) {
                 const char* p = reinterpret_cast<const char*>(a.s_sh) + (size_t)bp[s] * a.sh_bytes;
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
                 if (a.sh_bytes > 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + a.sh_bytes - 4));
             }
+            sm.wpk[s][threadIdx.x] = bp[s];   // (reloaded for the deferred colour: no registers in pass 2)
         }
         // depth/normal/winner of each pixel from its sub-sample 0 (forward.py:205-207)
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const int s0 = (p / PX) * SS * G + (p % PX) * SS;
-            const bool cov = best[s0] != ~0ull;
-            ds[p] = cov ? __uint_as_float((uint32_t)(best[s0] >> 32)) : INFINITY;
-            asm volatile("" : "+f"(ds[p]));   // (not rematerialised from best[] in pass 2)
+            const bool cov = bid[s0] != ~0u;
+            ds[p] = cov ? bt[s0] : INFINITY;
+            asm volatile("" : "+f"(ds[p]));   // (not rematerialised from bt[] in pass 2)
             if (inside_px(p)) {
                 const int64_t pix = pix_of(p);
                 if constexpr (PX == 2) {   // depth and winner of the row pair in one store each
                     if (p % 2 == 0) {
                         const int s1 = s0 + SS;
-                        const bool in1 = inside_px(p + 1), cov1 = best[s1] != ~0ull;
-                        const float d1 = cov1 ? __uint_as_float((uint32_t)(best[s1] >> 32)) : INFINITY;
+                        const bool in1 = inside_px(p + 1), cov1 = bid[s1] != ~0u;
+                        const float d1 = cov1 ? bt[s1] : INFINITY;
                         if (a.out.s_depth) put1_pair(a.out.s_depth, pix, ds[p], d1, in1);
                         if (a.out.s_winner)
-                            put1_pair(a.out.s_winner, pix, cov ? (int32_t)(uint32_t)best[s0] : -1,
-                                      cov1 ? (int32_t)(uint32_t)best[s1] : -1, in1);
+                            put1_pair(a.out.s_winner, pix, cov ? (int32_t)bid[s0] : -1,
+                                      cov1 ? (int32_t)bid[s1] : -1, in1);
                     }
                 } else {
                     if (a.out.s_depth) a.out.s_depth[pix] = ds[p];
-                    if (a.out.s_winner) a.out.s_winner[pix] = cov ? (int32_t)(uint32_t)best[s0] : -1;
+                    if (a.out.s_winner) a.out.s_winner[pix] = cov ? (int32_t)bid[s0] : -1;
                 }
                 if (a.out.s_normal) {
-                    const float3 n = cov ? surfel_nvis(a, (uint32_t)best[s0]) : make_float3(0.f, 0.f, 0.f);
+                    const float3 n = cov ? surfel_nvis(a, bid[s0]) : make_float3(0.f, 0.f, 0.f);
                     a.out.s_normal[3 * pix] = n.x; a.out.s_normal[3 * pix + 1] = n.y;
                     a.out.s_normal[3 * pix + 2] = n.z;
                 }
@@ -682,6 +692,8 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
     for (int p = 0; p < NP; ++p) cs[p] = make_float3(a.bg[0], a.bg[1], a.bg[2]);
     if constexpr ((MODE & 1) != 0) {
         float3 col[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) bp[s] = reinterpret_cast<volatile uint32_t*>(sm.wpk[s])[threadIdx.x];
         resolve_surfel_colors<NS>(a, sm, covm, bp, lane, wl, col);
         if constexpr (PX == 1) {   // box mean over the sub-samples (forward.py:201-203)
             float3 acc = make_float3(0.f, 0.f, 0.f);
