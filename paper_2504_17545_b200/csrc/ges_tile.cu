@@ -357,8 +357,11 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             m *= 1.00001f;   // margin-inflated: culling stays conservative
             return region_reduce(m, rm, lane);
         };
-        if (lane < 8) rm[lane] = INFINITY;
-        float wmx = INFINITY;          // max over this warp's samples of the best depth
+        // max over this warp's samples of the best depth, and per region: +inf
+        // for samples in the image, 0 outside, so a patch that lies entirely
+        // below the image's last row (the partial bottom tile row) stops at
+        // its first slab instead of walking the whole list
+        float wmx = patch_depth();
         for (int k = threadIdx.x; k < NSLAB; k += TPB) sm.slab_end[k] = a.sbin.cnt[tile * NSLAB + k];
         __syncthreads();
         const int ox = tx * TP * SS, oy = ty * TP * SS;
