@@ -287,6 +287,13 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
     constexpr int WPC = tile_wpc<SS, PX>(), TPB = 32 * WPC;
     __shared__ TileSmem<WPC> sm;
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders
+#ifdef GES_TIMING   // warp lifetimes (tuning builds only, see read_stats / tools/tile_stats.py --timing)
+    const long long t_start = clock64();
+    unsigned tm_len = 0, tm_b1 = 0, tm_t1 = 0;
+#define GES_TM(x) (x)
+#else
+#define GES_TM(x) ((void)0)
+#endif
     // warp: the warp's patch within the tile (0..7); wl: its index within the CTA
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int warp = (int)(blockIdx.x % (NWARP / WPC)) * WPC + wl;
@@ -366,6 +373,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
         __syncthreads();
         const int ox = tx * TP * SS, oy = ty * TP * SS;
         const uint32_t beg = a.sbin.tile_off(tile), end = beg + sm.slab_end[NSLAB - 1];
+        GES_TM(tm_len = end - beg);
         uint32_t nid = beg + lane < end ? a.s_list[beg + lane] : 0u;
         if constexpr ((MODE & 2) != 0) {
             if (gbeg + warp * 32 + lane < gend) {
@@ -416,6 +424,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 }
             }
             uint32_t vote = __ballot_sync(0xffffffffu, live);
+            GES_TM(++tm_b1);
 #ifdef GES_STATS
             if (lane == 0) { GES_STAT(0, 1); GES_STAT(1, min(32u, end - base)); GES_STAT(2, __popc(vote)); }
 #endif
@@ -428,6 +437,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
                 if (lane == 0) GES_STAT(3, 1);
                 if (lane == 0) GES_STAT(12, wmx == INFINITY);
+                GES_TM(++tm_t1);
                 const float4 A = sm.st[0][j], B = sm.st[1][j];
                 const float Awf = A.w * 0.99999f;   // candidate filter t <= 1.00001 bt (margin vs rounding)
                 // den, U, V at the thread's first sample, then stepped by the
@@ -782,6 +792,21 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             }
         }
     }
+#ifdef GES_TIMING
+    if (lane == 0) {   // 16: sum of warp cycles, 17: max, 18: max (cycles << 24 | tile << 3 | warp),
+                       // 19: warps over 50 us; 12-14: their list lengths, chunks walked, warp tests
+        const unsigned long long dt = (unsigned long long)(clock64() - t_start);
+        atomicAdd(&g_stats[16], dt);
+        atomicMax(&g_stats[17], dt);
+        atomicMax(&g_stats[18], (dt << 24) | ((unsigned long long)tile << 3) | (unsigned long long)warp);
+        if (dt > 98000ull) {
+            atomicAdd(&g_stats[19], 1ull);
+            atomicAdd(&g_stats[12], (unsigned long long)tm_len);
+            atomicAdd(&g_stats[13], (unsigned long long)tm_b1);
+            atomicAdd(&g_stats[14], (unsigned long long)tm_t1);
+        }
+    }
+#endif
 }
 
 template <int SS, int PX, int MODE>

@@ -2,6 +2,7 @@
 
   python -m paper_2504_17545_b200._build stats
   GES_B200_LIB=paper_2504_17545_b200/libges_b200_stats.so python tools/tile_stats.py [--ss 4]
+  (or a -DGES_TIMING build with --timing: warp lifetimes and the slowest warps)
 """
 import argparse
 import ctypes as C
@@ -24,6 +25,7 @@ NAMES = ["surfel batches", "surfel entries staged", "  with live mask", "surfel 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--ss", type=int, default=1)
+ap.add_argument("--timing", action="store_true", help="library built with -DGES_TIMING (warp lifetimes)")
 a = ap.parse_args()
 sc = S.config_scene(a.config)
 cam = S.config_cameras(a.config)[0]
@@ -38,5 +40,15 @@ torch.cuda.synchronize()
 _lib.lib().ges_debug_stats(buf)
 sp, gp, _ = fr.pairs()
 print(f"pairs: surfel {sp}  gaussian {gp}   pixels {cam.width * cam.height}")
-for n, v in zip(NAMES, buf):
-    print(f"{n:28s} {v:14d}")
+if a.timing:
+    nw = ((cam.width + 31) // 32) * ((cam.height + 31) // 32) * 8
+    ntx = (cam.width + 31) // 32
+    k = buf[18]
+    print(f"warps {nw}: mean lifetime {buf[16] / nw:.0f} cycles, max {buf[17]} "
+          f"(tile ({(k >> 3) % (1 << 21) % ntx}, {(k >> 3) % (1 << 21) // ntx}), warp {k & 7})")
+    n = max(buf[19], 1)
+    print(f"warps over 50 us: {buf[19]}; their mean list length {buf[12] / n:.0f}, "
+          f"chunks walked {buf[13] / n:.1f}, warp tests {buf[14] / n:.1f}")
+else:
+    for n, v in zip(NAMES, buf):
+        print(f"{n:28s} {v:14d}")
