@@ -75,6 +75,7 @@ struct Frame {
     uint32_t *cnt_s, *off_s, *cnt_g, *off_g, *chunk_s, *chunk_g, *tickets;
     size_t zero_bytes;   // counters + tickets, cleared by one memset per frame
     uint32_t *list_s, *list_g;
+    uint32_t *order, *tot;
     ges_frame_status_t* status;
     size_t bytes;
     int ntx, nty, ntiles, px;
@@ -105,6 +106,8 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, const g
     f.tickets = f.cnt_s ? f.cnt_s + 2 * nbins : nullptr;
     f.zero_bytes = (2 * nbins + 64) * sizeof(uint32_t);
     const size_t nchunk = (size_t)(f.ntiles + 255) / 256 + 1;
+    f.order = c.take<uint32_t>(f.ntiles);
+    f.tot = c.take<uint32_t>(f.ntiles);
     f.off_s = c.take<uint32_t>(f.ntiles);
     f.off_g = c.take<uint32_t>(f.ntiles);
     f.chunk_s = c.take<uint32_t>(nchunk);
@@ -180,7 +183,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     if (!do_g) scs.n_gaussians = 0;
     auto log2i = [](int v) { int k = 0; while ((1 << k) < v) ++k; return k; };
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, tp * grid,
-                     log2i(tp * grid)};
+                     log2i(tp * grid), do_s ? f.order : nullptr, f.tot};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, tp, log2i(tp)};
     if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, f.cnt_s, nullptr, f.scull}, s)))
         return cuda_fail(e, "surfel preprocess");
@@ -199,6 +202,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     for (int i = 0; i < 3; ++i) a.bg[i] = st->background[i];
     a.rcx = (float)cs.cx; a.rcy = (float)cs.cy; a.rifx = (float)(1.0 / cs.fx); a.rify = (float)(1.0 / cs.fy);
     a.srec = f.srec; a.scull = f.scull; a.s_list = f.list_s; a.sbin = bs;
+    a.order = bs.order;
     a.s_sh = sc->s_sh; a.sh_deg = sc->sh_degree; a.sh_bytes = (sc->sh_degree + 1) * (sc->sh_degree + 1) * 12;
     for (int i = 0; i < 3; ++i) a.cpos[i] = cs.pos[i];
     a.s_quat = reinterpret_cast<const float4*>(sc->s_quat);

@@ -48,7 +48,10 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
     }
     uint32_t ex, blk;
     Scan(tmp).ExclusiveSum(tot, ex, blk);
-    if (t < n) p.off[t] = ex;
+    if (t < n) {
+        p.off[t] = ex;
+        if (p.order) p.tot[t] = tot;
+    }
     if (threadIdx.x == 0) {
         p.chunk[blockIdx.x] = blk;
         __threadfence();
@@ -83,6 +86,60 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
         p.chunk[nc] = total;
         if (blockIdx.y) st->gaussian_pairs = total; else st->surfel_pairs = total;
         if ((int64_t)total > p.cap) atomicOr(&st->overflow, 1);
+    }
+    if (!p.order) return;
+    // Tile launch order for the tile kernel: by descending pair count
+    // (counting sort over log2 buckets), so the longest tiles start first and
+    // do not end up as the last wave's tail.  Any order gives the same
+    // results (tiles are independent).
+    __shared__ uint32_t bucket[33];
+    if (threadIdx.x < 33) bucket[threadIdx.x] = 0;
+    constexpr int PER = 8;   // tiles per thread (n <= 2048 here; larger grids loop)
+    const unsigned lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    for (int c0 = 0; c0 < n; c0 += SCAN_T * PER) {
+        int bk[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {   // all loads first: one round trip, not PER
+            const int i = c0 + k * SCAN_T + threadIdx.x;
+            bk[k] = i < n ? (int)*((volatile uint32_t*)p.tot + i) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) bk[k] = bk[k] < 0 ? -1 : 32 - __clz((uint32_t)bk[k]);
+        __syncthreads();   // (bucket cleared / previous scatter done)
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {   // one shared atomic per (warp, bucket)
+            const unsigned peers = __match_any_sync(0xffffffffu, bk[k]);
+            if (bk[k] >= 0 && (peers & lt) == 0) atomicAdd(&bucket[bk[k]], (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 32; b >= 0; --b) {
+            const uint32_t c = bucket[b];
+            bucket[b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < n; c0 += SCAN_T * PER) {
+        int bk[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = c0 + k * SCAN_T + threadIdx.x;
+            bk[k] = i < n ? (int)*((volatile uint32_t*)p.tot + i) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = c0 + k * SCAN_T + threadIdx.x;
+            const int b = bk[k] < 0 ? -1 : 32 - __clz((uint32_t)bk[k]);
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            const int leader = __ffs(peers) - 1;
+            uint32_t pos = 0;
+            if (b >= 0 && (int)lane == leader) pos = atomicAdd(&bucket[b], (uint32_t)__popc(peers));
+            pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(peers & lt);
+            if (b >= 0) p.order[pos] = (uint32_t)i;
+        }
     }
 }
 

@@ -127,6 +127,8 @@ struct BinPass {
     uint32_t* list;     // cap primitive ids (packed indices)
     int64_t cap;
     int ntiles, ntx, tile_px, tile_shift;
+    uint32_t* order;    // or NULL; surfel pass: tiles by descending pair count (tile kernel launch order)
+    uint32_t* tot;      // with order: per-tile pair totals (scan scratch)
     __device__ __forceinline__ uint32_t tile_off(int t) const { return chunk[t >> 8] + off[t]; }
 };
 

@@ -41,6 +41,7 @@ struct TileArgs {
     float rcx, rcy, rifx, rify;   // principal point and 1/f of the surfel pass
     const SurfRec* srec;
     const float4* scull;          // dense surfel cull records
+    const uint32_t* order;        // tile launch order (by descending surfel pairs), or NULL
     const float* s_sh;            // packed SH (deferred colour of winners)
     int sh_deg, sh_bytes;
     double cpos[3];               // camera centre (world)

@@ -296,9 +296,11 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
 #endif
     // warp: the warp's patch within the tile (0..7); wl: its index within the CTA
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    const int warp = (int)(blockIdx.x % (NWARP / WPC)) * WPC + wl;
-    const int tx = blockIdx.x / (NWARP / WPC), ty = blockIdx.y;
-    const int tile = ty * a.ntx + tx;
+    // CTAs in launch order; with a.order the heaviest tiles come first
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+    const int warp = (cta % (NWARP / WPC)) * WPC + wl;
+    const int tile = a.order ? (int)__ldg(a.order + cta / (NWARP / WPC)) : cta / (NWARP / WPC);
+    const int tx = tile % a.ntx, ty = tile / a.ntx;
     const int plx = (warp & 1) * 8 + (lane & 7), ply = (warp >> 1) * 4 + (lane >> 3);
     const int bx = tx * TP + PX * plx, by = ty * TP + PX * ply;   // first base pixel of the thread
 
