@@ -204,9 +204,50 @@ def tile_list(height, width):
 
 
 def _select(idx, x0, x1, y0, y1, t):
+    """The reference's per-tile selection (forward.py:168-169, :294-295):
+    alive primitives whose pixel range overlaps the tile, ascending index."""
     ty0, ty1, tx0, tx1 = t
     return idx[(x0[idx] <= tx1 - 1) & (x1[idx] >= tx0)
                & (y0[idx] <= ty1 - 1) & (y1[idx] >= ty0)]
+
+
+# Above this many (primitive x tile) range tests per frame the selection is
+# done through per-tile index lists built once per frame (same lists, same
+# ascending order, so results are identical; the O(N x tiles) scan of the
+# reference is kept for the timed CPU baseline, see FAST_SELECT).
+FAST_SELECT = [True]
+_FAST_MIN = 1 << 24
+
+
+class _Selector:
+    """Per-tile candidate lists, identical to ``_select`` for every tile: the
+    (tile, primitive) pairs are generated in ascending primitive order and
+    grouped by a stable sort on the tile key."""
+
+    def __init__(self, idx, x0, x1, y0, y1, height, width):
+        self.args = (idx, x0, x1, y0, y1)
+        self.ntx = (width + TILE - 1) // TILE
+        nt = self.ntx * ((height + TILE - 1) // TILE)
+        self.lists = None
+        if not FAST_SELECT[0] or idx.size * nt < _FAST_MIN:
+            return
+        a0, a1 = x0[idx] // TILE, x1[idx] // TILE
+        b0, b1 = y0[idx] // TILE, y1[idx] // TILE
+        nx, ny = a1 - a0 + 1, b1 - b0 + 1
+        cnt = nx * ny
+        rep = np.repeat(np.arange(idx.size), cnt)
+        k = np.arange(rep.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+        tile = (b0[rep] + k // nx[rep]) * self.ntx + a0[rep] + k % nx[rep]
+        order = np.argsort(tile, kind="stable")
+        self.ids = idx[rep[order]]
+        self.start = np.searchsorted(tile[order], np.arange(nt + 1))
+        self.lists = True
+
+    def __call__(self, t):
+        if self.lists is None:
+            return _select(*self.args, t)
+        ti = (t[0] // TILE) * self.ntx + t[2] // TILE
+        return self.ids[self.start[ti]:self.start[ti + 1]]
 
 
 # Seconds spent inside per-tile loops since the last reset (lets the CPU
@@ -268,7 +309,8 @@ class GaussOut:
     weight: np.ndarray
     depth: np.ndarray = None
     normal: np.ndarray = None
-    tie: np.ndarray = None
+    tie: np.ndarray = None       # (H, W) bool: a depth-gate decision within TIE_GATE_REL
+    tie_cut: np.ndarray = None   # (H, W) int: fragments within TIE_ALPHA of the 1/255 cutoff
 
 
 @dataclass
@@ -279,10 +321,24 @@ class RenderOut:
 
     @property
     def tie(self):
+        """Pixels whose result a float32 evaluation may legitimately change
+        by more than one near-cutoff fragment: surfel winner/coverage ties and
+        finite depth-gate ties.  These are excluded from the parity checks
+        (and counted)."""
         t = self.surfels.tie
         if self.gaussians.tie is not None:
             t = t | self.gaussians.tie
         return t
+
+    @property
+    def tie_cut(self):
+        """Per pixel, the number of contributing Gaussian fragments whose
+        alpha lies within TIE_ALPHA of the 1/255 cutoff: a float32 evaluation
+        may drop or add each of them, which moves the pixel by at most
+        ~1/255 per fragment.  Checked against that bound, not excluded."""
+        if self.gaussians.tie_cut is None:
+            return np.zeros(self.surfels.tie.shape, np.int32)
+        return self.gaussians.tie_cut
 
 
 def _settings(settings):
@@ -331,10 +387,11 @@ def rasterize_surfels(scene, cam, settings=None, *, tiles=None, ties=False) -> S
         a1q_all = np.sum(a1d * qd, axis=1)
         a2q_all = np.sum(a2d * qd, axis=1)
         R2 = R_OPAQUE * R_OPAQUE
+        select = _Selector(idx, x0, x1, y0, y1, H, W)
 
         def do_tile(t):
             ty0, ty1, tx0, tx1 = t
-            sel = _select(idx, x0, x1, y0, y1, t)
+            sel = select(t)
             if sel.size == 0:
                 return
             d = rays[ty0:ty1, tx0:tx1].reshape(-1, 3)
@@ -381,6 +438,27 @@ def rasterize_surfels(scene, cam, settings=None, *, tiles=None, ties=False) -> S
         winner = winner[0::grid, 0::grid]
         tie = tie.reshape(h, grid, w, grid).any(axis=(1, 3))
     return SurfelOut(color, depth, normal, np.isfinite(depth), winner, tie)
+
+
+def surfel_tile_counts(scene, cam):
+    """Per 16x16 tile (ss = 1), the number of alive surfels whose pixel range
+    overlaps it -- the length of the reference's per-tile candidate list
+    (forward.py:168-169).  Used to pick the densest tiles for sampled parity."""
+    c = as_cam(cam)
+    s = scene.surfels
+    q, a1, a2, n = frames(s.pos, s.quat, c)
+    scale = np.exp(np.asarray(s.log_scale, dtype=np.float64))
+    bounds, whole = disc_bounds(q, a1, a2, scale[:, 0] * R_OPAQUE, scale[:, 1] * R_OPAQUE, c)
+    x0, x1, y0, y1 = pixel_ranges(bounds, whole, c.width, c.height)
+    idx = np.flatnonzero((q[:, 2] > NEAR) & (x1 >= x0) & (y1 >= y0))
+    sel = _Selector(idx, x0, x1, y0, y1, c.height, c.width) if idx.size else None
+    ntx = (c.width + TILE - 1) // TILE
+    nt = ntx * ((c.height + TILE - 1) // TILE)
+    if sel is None:
+        return np.zeros(nt, np.int64)
+    if sel.lists is None:
+        return np.array([sel(t).size for t in tile_list(c.height, c.width)], np.int64)
+    return np.diff(sel.start)
 
 
 # --- pass 2: order-independent Gaussian accumulation (forward.py:212-381) ---
@@ -453,6 +531,7 @@ def accumulate_gaussians(scene, cam, surfel_depth, settings=None, *, tiles=None,
         out.depth = np.zeros((H, W), dtype=dt)
         out.normal = np.zeros((H, W, 3), dtype=dt)
     out.tie = np.zeros((H, W), dtype=bool)
+    out.tie_cut = np.zeros((H, W), dtype=np.int32)
     g = scene.gaussians
     ng = int(np.asarray(g.pos).shape[0])
     if ng == 0:
@@ -468,6 +547,13 @@ def accumulate_gaussians(scene, cam, surfel_depth, settings=None, *, tiles=None,
     else:
         _acc_3d(g, c, ds, eps, cols, es, sigma, st, out, tiles, ties)
     return out
+
+
+def _near_gate(d, thr):
+    """Gate decision d < D_s + eps within TIE_GATE_REL of flipping.  An
+    uncovered pixel has thr = +inf: its gate always passes (forward.py:310,
+    SPEC.md:227) and is never a tie."""
+    return np.isfinite(thr) & (np.abs(d - thr) < TIE_GATE_REL * np.abs(thr))
 
 
 def _acc_3d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
@@ -510,9 +596,11 @@ def _acc_3d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
     xs = (np.arange(W) + 0.5).astype(dt)
     ys = (np.arange(H) + 0.5).astype(dt)
 
+    select = _Selector(idx, x0, x1, y0, y1, H, W)
+
     def do_tile(t):
         ty0, ty1, tx0, tx1 = t
-        sel = _select(idx, x0, x1, y0, y1, t)
+        sel = select(t)
         if sel.size == 0:
             return
         sel = sel[np.lexsort((sg[sel], my[sel], mx[sel], dep[sel]))]   # forward.py:298-300
@@ -537,9 +625,10 @@ def _acc_3d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
             with np.errstate(invalid="ignore"):
                 raw = sg[sel][:, None, None] * np.exp(pw)
                 near_cut = np.abs(255.0 * raw - 1.0) < TIE_ALPHA
-                near_gate = np.abs(dep[sel][:, None, None] - thr) <= TIE_GATE_REL * np.abs(thr)
-                fl = (near_cut & gate) | (near_gate & keep)
-            out.tie[ty0:ty1, tx0:tx1] |= fl.any(axis=0)
+                near_gate = _near_gate(dep[sel][:, None, None], thr)
+            hard = near_gate & keep
+            out.tie[ty0:ty1, tx0:tx1] |= hard.any(axis=0)
+            out.tie_cut[ty0:ty1, tx0:tx1] += (near_cut & (gate | near_gate) & ~hard).sum(axis=0)
 
     _run(do_tile, _tiles_for(H, W, tiles), st["threads"])
 
@@ -572,9 +661,11 @@ def _acc_2d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
     s1, s2 = scale[:, 0].astype(dt), scale[:, 1].astype(dt)
     sg = sig.astype(dt)
 
+    select = _Selector(idx, x0, x1, y0, y1, H, W)
+
     def do_tile(t):
         ty0, ty1, tx0, tx1 = t
-        sel = _select(idx, x0, x1, y0, y1, t)
+        sel = select(t)
         if sel.size == 0:
             return
         sel = sel[np.lexsort((sg[sel], qd[sel, 1], qd[sel, 0], depc[sel]))]
@@ -600,10 +691,11 @@ def _acc_2d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
         if ties:
             with np.errstate(invalid="ignore"):
                 near_cut = np.abs(255.0 * raw - 1.0) < TIE_ALPHA
-                near_gate = np.abs(th - thr) <= TIE_GATE_REL * np.abs(thr)
-                fl = (near_cut & gate) | (near_gate & keep)
+                near_gate = _near_gate(th, thr)
+                fl = near_gate & keep
                 fl |= ok & (np.abs(ndot) < TIE_PARALLEL * PARALLEL_EPS * dn) & keep
             out.tie[ty0:ty1, tx0:tx1] |= fl.any(axis=0).reshape(th_, tw_)
+            out.tie_cut[ty0:ty1, tx0:tx1] += (near_cut & (gate | near_gate) & ~fl).sum(axis=0).reshape(th_, tw_)
 
     _run(do_tile, _tiles_for(H, W, tiles), st["threads"])
 
@@ -629,7 +721,7 @@ def render(scene, cam, settings=None, *, tiles=None, ties=False) -> RenderOut:
     sb = rasterize_surfels(scene, cam, settings, tiles=tiles, ties=ties)
     if st["layers"] == "surfels_only":
         gb = GaussOut(np.zeros_like(sb.color), np.zeros_like(sb.depth),
-                      tie=np.zeros(sb.depth.shape, bool))
+                      tie=np.zeros(sb.depth.shape, bool), tie_cut=np.zeros(sb.depth.shape, np.int32))
         return RenderOut(sb.color.copy(), sb, gb)
     gb = accumulate_gaussians(scene, cam, sb.depth, settings, tiles=tiles, ties=ties)
     if st["layers"] == "gaussians_only":

@@ -52,6 +52,11 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
         p.off[t] = ex;
         if (p.order) p.tot[t] = tot;
     }
+    // every thread's off/tot stores must be ordered before the ticket: the
+    // last block reads p.tot (twice, for the order's bucket counts and its
+    // scatter) as soon as the ticket says all blocks are done
+    __threadfence();
+    __syncthreads();
     if (threadIdx.x == 0) {
         p.chunk[blockIdx.x] = blk;
         __threadfence();

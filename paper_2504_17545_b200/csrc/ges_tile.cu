@@ -127,10 +127,11 @@ __device__ __forceinline__ void store_rgba8(uint8_t* dst, int64_t pix, float3 c)
 }
 
 // Row-pair stores of a thread's two horizontally adjacent pixels (PX = 2):
-// one 8-byte store per pair of words when the first pixel index is even (and
-// both pixels are inside the image), plain stores otherwise.
+// one 8-byte store per pair of words when the destination address is 8-byte
+// aligned (and both pixels are inside the image), plain stores otherwise --
+// the C ABI only requires 4-byte alignment of the output buffers.
 __device__ __forceinline__ void put1_pair(float* dst, int64_t pix, float v0, float v1, bool in1) {
-    if (in1 && !(pix & 1)) {
+    if (in1 && !(reinterpret_cast<uintptr_t>(dst + pix) & 7)) {
         *reinterpret_cast<float2*>(dst + pix) = make_float2(v0, v1);
     } else {
         dst[pix] = v0;
@@ -138,7 +139,7 @@ __device__ __forceinline__ void put1_pair(float* dst, int64_t pix, float v0, flo
     }
 }
 __device__ __forceinline__ void put1_pair(int32_t* dst, int64_t pix, int32_t v0, int32_t v1, bool in1) {
-    if (in1 && !(pix & 1)) {
+    if (in1 && !(reinterpret_cast<uintptr_t>(dst + pix) & 7)) {
         *reinterpret_cast<int2*>(dst + pix) = make_int2(v0, v1);
     } else {
         dst[pix] = v0;
@@ -147,7 +148,7 @@ __device__ __forceinline__ void put1_pair(int32_t* dst, int64_t pix, int32_t v0,
 }
 __device__ __forceinline__ void put3_pair(float* dst, int64_t pix, float3 v0, float3 v1, bool in1) {
     float* d = dst + 3 * pix;
-    if (in1 && !(pix & 1)) {   // 3 * pix even: the 6 floats start 8-byte aligned
+    if (in1 && !(reinterpret_cast<uintptr_t>(d) & 7)) {   // the 6 floats start 8-byte aligned
         float2* d2 = reinterpret_cast<float2*>(d);
         d2[0] = make_float2(v0.x, v0.y); d2[1] = make_float2(v0.z, v1.x); d2[2] = make_float2(v1.y, v1.z);
     } else {

@@ -83,8 +83,14 @@ def load_ges(path) -> tuple[Scene, dict]:
 
 def save_ges(scene: Scene, path, *, rgb_surfels: bool = False):
     """Write a frozen scene in the same format (for fixtures and round trips;
-    epsilon baked from the effective scales like ``gesfile.py:42-76``)."""
+    epsilon baked from the effective scales like ``gesfile.py:42-76``), with
+    the reference's export checks: frozen stage and w = 255 on every surfel
+    (``gesfile.py:44-47``), finite records (``:66-69``)."""
+    if getattr(scene.stage, "value", scene.stage) != getattr(Stage.FROZEN, "value", Stage.FROZEN):
+        raise GesFileError("only frozen scenes can be exported")
     s, g = scene.surfels, scene.gaussians
+    if not np.all(np.asarray(s.w) == W_OPAQUE):
+        raise GesFileError("export requires w = 255 on every surfel")
     deg = int(scene.sh_degree)
     K = (deg + 1) ** 2
     two_d = getattr(g.kind, "value", g.kind) == "2d"
@@ -103,6 +109,10 @@ def save_ges(scene: Scene, path, *, rgb_surfels: bool = False):
     eps = (5.0 / gs.shape[1]) * gs.sum(axis=1)
     grec = np.concatenate([g.pos, sig[:, None], g.quat, gs, eps[:, None],
                            g.sh.reshape(g.count, 3 * K)], axis=1).astype("<f4")
+    if srec.size and not np.all(np.isfinite(srec)):
+        raise GesFileError("non-finite surfel values")
+    if grec.size and not np.all(np.isfinite(grec)):
+        raise GesFileError("non-finite gaussian values")
     with open(path, "wb") as f:
         f.write(HEADER.pack(MAGIC, VERSION, deg, flags, s.count, g.count))
         f.write(srec.tobytes())

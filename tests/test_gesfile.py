@@ -73,3 +73,30 @@ def test_cli_export_roundtrip(tmp_path):
     assert ia["rgb_surfels"] == ib["rgb_surfels"]
     assert np.array_equal(a.surfels.pos, b.surfels.pos) and np.array_equal(a.gaussians.sh, b.gaussians.sh)
     assert cli.main(["export", "--model", str(tmp_path / "missing.ges"), "--out", str(out)]) == 1
+
+
+def test_save_rejects_like_reference_export(tmp_path):
+    """save_ges applies export_ges's checks (gesfile.py:44-47, :66-69)."""
+    import copy
+    from paper_2504_17545_b200.types import Scene, Stage
+    scene, _ = load_ges(os.path.join(GOLD, "ges_3d_deg3.ges"))
+    p = tmp_path / "x.ges"
+    joint = Scene(scene.surfels, scene.gaussians, scene.sh_degree, Stage.JOINT)
+    with pytest.raises(GesFileError, match="frozen"):
+        save_ges(joint, p)
+    s2 = copy.deepcopy(scene)
+    s2.surfels.w = s2.surfels.w.copy()
+    s2.surfels.w[0] = 128.0
+    with pytest.raises(GesFileError, match="w = 255"):
+        save_ges(s2, p)
+    s3 = copy.deepcopy(scene)
+    s3.surfels.pos = s3.surfels.pos.copy()
+    s3.surfels.pos[0, 0] = np.nan
+    with pytest.raises(GesFileError, match="non-finite surfel"):
+        save_ges(s3, p)
+    s4 = copy.deepcopy(scene)
+    s4.gaussians.sh = s4.gaussians.sh.copy()
+    s4.gaussians.sh[0, 0, 0] = np.inf
+    with pytest.raises(GesFileError, match="non-finite gaussian"):
+        save_ges(s4, p)
+    assert not p.exists()

@@ -41,7 +41,7 @@ def test_ges_file_renders_like_reference(name):
     out = G.render(scene, cam)
     ora = O.render(scene, cam, settings_ns({}), ties=True)
     rep = compare(dict(image=out.image, s_winner=out.surfels.winner, s_depth=out.surfels.depth),
-                  dict(image=z["image"], s_winner=z["s_winner"], s_depth=z["s_depth"]), ora.tie)
+                  dict(image=z["image"], s_winner=z["s_winner"], s_depth=z["s_depth"]), ora.tie, tie_cut=ora.tie_cut)
     assert_parity(rep)
 
 
@@ -90,15 +90,30 @@ def test_covering_counts_match_oracle_winners():
     cams = S.orbit_views(3, 48, 40)
     got = covering_counts(scene, cams)
     best = np.zeros(60, np.int64)
-    slack = np.zeros(60, np.int64)
+    ties = 0
     for c in cams:
         o = O.rasterize_surfels(scene, c, settings_ns({}), ties=True)
         w = o.winner.reshape(-1)
         best = np.maximum(best, np.bincount(w[w >= 0], minlength=60))
-        tw = o.winner[o.tie]
-        slack += np.bincount(tw[tw >= 0], minlength=60) + int(o.tie.sum())
-    assert np.all(np.abs(got - best) <= slack)
+        ties += int(o.tie.sum())
+    # each flagged pixel can move at most one count from one surfel to another
+    assert ties <= 2
+    assert int(np.abs(got - best).sum()) <= 2 * ties
     assert got.sum() > 0
+
+
+def test_covering_counts_exact_like_reference():
+    """test_optim.py:141-178: 10 stacked random surfels at 32x32 (rng 1234),
+    per-surfel frontmost counts equal the brute-force scan exactly (the
+    oracle flags no tie pixel on this scene)."""
+    from paper_2504_17545_b200.types import GaussianSet, Scene, Stage
+    rng = np.random.default_rng(1234)
+    cam = S.make_camera()
+    scene = Scene(S.random_surfels(rng, 10), GaussianSet.empty(1), 1, Stage.FROZEN)
+    o = O.rasterize_surfels(scene, cam, settings_ns({}), ties=True)
+    assert not o.tie.any()
+    ref = np.bincount(o.winner[o.winner >= 0], minlength=10)
+    assert np.array_equal(covering_counts(scene, [cam]), ref)
 
 
 def test_scene_cache_replaced_and_invalidated_arrays():

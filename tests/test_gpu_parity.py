@@ -58,7 +58,7 @@ def test_golden_parity(name):
                g_weight=gold["g_weight"])
     if "g_depth" in gold:
         ref.update(g_depth=gold["g_depth"], g_normal=gold["g_normal"])
-    rep = compare(gpu_dict(out), ref, ora.tie)
+    rep = compare(gpu_dict(out), ref, ora.tie, tie_cut=ora.tie_cut)
     assert_parity(rep, weight_tol=5e-4)
     if "g_depth_maxabs" in rep:
         assert rep["g_depth_maxabs"] < 5e-4 and rep["g_normal_maxabs"] < 5e-4, rep
@@ -73,7 +73,7 @@ def test_random_scene_480x270(seed):
     cam = S.make_camera(480, 270)
     out = G.render(sc, cam)
     ora = O.render(sc, cam, settings_ns({}), ties=True)
-    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie)
+    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut)
     assert_parity(rep)
 
 
@@ -92,7 +92,7 @@ def test_config2_tile_sample():
     for ti in tiles:
         ty0, ty1, tx0, tx1 = O.tile_list(cam.height, cam.width)[ti]
         region[ty0:ty1, tx0:tx1] = True
-    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie, region=region)
+    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut, region=region)
     assert_parity(rep)
     assert rep["pixels"] >= 12 * 256
 
@@ -260,7 +260,7 @@ def test_near_plane_crossing_surfel():
     cam = S.make_camera(64, 64)
     out = G.render(sc, cam)
     ora = O.render(sc, cam, settings_ns({}), ties=True)
-    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut))
 
 
 def test_settings_validation():
@@ -298,7 +298,7 @@ def test_supersample4_480x270_stress():
     st = {"supersample": 4, "background": [0.1, 0.2, 0.3]}
     out = G.render(sc, cam, settings32(st))
     ora = O.render(sc, cam, settings_ns(st), ties=True)
-    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut))
 
 
 def test_mip_filtered_scene_multiscale():
@@ -311,7 +311,7 @@ def test_mip_filtered_scene_multiscale():
         cam = S.make_camera(w, h)
         out = G.render(sc, cam, settings32({"mip": True}))
         ora = O.render(sc, cam, settings_ns({"mip": True}), ties=True)
-        assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+        assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut))
 
 
 def test_pair_list_overflow_grows_and_rerenders():
@@ -379,7 +379,7 @@ def test_camera_inside_scene_near_plane():
     cam = S.make_camera(160, 120, dist=0.3)
     out = G.render(sc, cam)
     ora = O.render(sc, cam, settings_ns({}), ties=True)
-    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+    assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut))
 
 
 def test_4k_supersampled_config2_scene_tile_sample():
@@ -392,7 +392,7 @@ def test_4k_supersampled_config2_scene_tile_sample():
     nt = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
     tiles = sorted(np.random.default_rng(9).choice(nt, 6, replace=False).tolist() + [nt // 2 + 120])
     ora = O.render(sc, cam, settings_ns(st), tiles=tiles, ties=True)
-    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie, region=_tile_region(cam, tiles))
+    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut, region=_tile_region(cam, tiles))
     assert_parity(rep)
 
 
@@ -405,7 +405,7 @@ def test_planar_gaussians_dense_with_geometry():
     st = {"with_geometry": True, "mip": True}
     out = G.render(sc, cam, settings32(st))
     ora = O.render(sc, cam, settings_ns(st), ties=True)
-    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie)
+    rep = compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut)
     assert_parity(rep)
     assert rep["g_depth_maxabs"] < 1e-3 and rep["g_normal_maxabs"] < 1e-3, rep
 
@@ -416,7 +416,7 @@ def test_odd_sizes_and_aspect():
         cam = S.make_camera(w, h)
         out = G.render(sc, cam)
         ora = O.render(sc, cam, settings_ns({}), ties=True)
-        assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie))
+        assert_parity(compare(gpu_dict(out), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut))
 
 
 @pytest.mark.parametrize("name", ["g3d_500", "g2d_901", "bg_gonly", "bg_sonly", "eps_const", "mip3d",
@@ -432,7 +432,7 @@ def test_golden_parity_2x2_pixel_tiles(name):
     ref = dict(image=gold["image"], s_winner=gold["s_winner"], s_depth=gold["s_depth"],
                s_color=gold["s_color"], s_normal=gold["s_normal"], g_color=gold["g_color"],
                g_weight=gold["g_weight"])
-    assert_parity(compare(gpu_dict(out), ref, ora.tie), weight_tol=5e-4)
+    assert_parity(compare(gpu_dict(out), ref, ora.tie, tie_cut=ora.tie_cut), weight_tol=5e-4)
 
 
 def test_tile_modes_agree_480x270():
@@ -448,4 +448,4 @@ def test_tile_modes_agree_480x270():
     assert np.array_equal(outs[0].surfels.winner, outs[1].surfels.winner)
     assert np.max(np.abs(outs[0].image - outs[1].image)) <= 1e-5
     ora = O.render(sc, cam, settings_ns({}), ties=True)
-    assert_parity(compare(gpu_dict(outs[1]), ora_dict(ora), ora.tie))
+    assert_parity(compare(gpu_dict(outs[1]), ora_dict(ora), ora.tie, tie_cut=ora.tie_cut))

@@ -57,7 +57,35 @@ def test_tie_flags_are_rare():
     scene, cam, st, gold, _ = load("config1")
     out = O.render(scene, cam, settings_ns(st), ties=True)
     frac = out.tie.mean()
-    assert frac < 0.01, frac
+    assert frac < 0.005, frac
+
+
+def test_uncovered_pixels_are_never_gate_ties():
+    """A pixel with no surfel has D_s = +inf: every Gaussian passes its gate
+    (forward.py:310), so the gate can never be a tie there."""
+    scene, cam, st, gold, _ = load("bg_gonly")
+    out = O.render(scene, cam, settings_ns(st), ties=True)
+    unc = ~np.isfinite(out.surfels.depth)
+    assert unc.any() and (out.gaussians.weight[unc] > 0).any()
+    assert not out.tie[unc].any()
+
+
+@pytest.mark.parametrize("name", names())
+def test_parity_rule_accepts_reference_fp32(name):
+    """The parity rule itself, checked on the reference's own float32 path
+    (this oracle in float32, pinned above) against the float64 goldens: the
+    hard ties stay within the excluded-pixel bound and every other pixel is
+    within 1e-4 (or the one-fragment bound at the alpha cutoff)."""
+    from parity import assert_parity, compare
+    scene, cam, st, gold, _ = load(name)
+    o32 = O.render(scene, cam, settings_ns(st, np.float32))
+    o64 = O.render(scene, cam, settings_ns(st), ties=True)
+    d32 = dict(image=o32.image, s_winner=o32.surfels.winner, s_depth=o32.surfels.depth,
+               s_color=o32.surfels.color, g_color=o32.gaussians.color, g_weight=o32.gaussians.weight)
+    ref = dict(image=gold["image"], s_winner=gold["s_winner"], s_depth=gold["s_depth"],
+               s_color=gold["s_color"], g_color=gold["g_color"], g_weight=gold["g_weight"])
+    rep = compare(d32, ref, o64.tie, tie_cut=o64.tie_cut)
+    assert_parity(rep, weight_tol=5e-4)
 
 
 def test_oracle_fp32_close_to_fp64():
