@@ -119,58 +119,129 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def _oracle_settings(cfg, threads, ss):
+    from types import SimpleNamespace
+    return SimpleNamespace(supersample=ss, background=(0.0, 0.0, 0.0), layers="full", mip=cfg == 4,
+                           epsilon_mode="adaptive", epsilon_value=0.0, dtype=np.float32,
+                           threads=threads, with_geometry=False)
+
+
 def cpu_sample(cfg, scene, cam, n_tiles, threads, ss=1):
     """Time the reference algorithm (oracle/ges_oracle.py, float32 like the
     reference default) on a bounded sample: the full per-frame preprocessing
     plus ``n_tiles`` random tiles of the frame; the tile time is extrapolated
-    to all tiles.  Returns (frame seconds, wall seconds, tiles, total tiles)."""
+    to all tiles (no extrapolation when n_tiles covers the frame).  Returns
+    (frame seconds, wall seconds, tiles, total tiles)."""
     from oracle import ges_oracle as O
-    from types import SimpleNamespace
-    st = SimpleNamespace(supersample=ss, background=(0.0, 0.0, 0.0), layers="full", mip=cfg == 4,
-                         epsilon_mode="adaptive", epsilon_value=0.0, dtype=np.float32,
-                         threads=threads, with_geometry=False)
+    st = _oracle_settings(cfg, threads, ss)
     nt = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
     rng = np.random.default_rng(7)
-    tiles = sorted(rng.choice(nt, min(n_tiles, nt), replace=False).tolist())
+    tiles = None if n_tiles >= nt else sorted(rng.choice(nt, n_tiles, replace=False).tolist())
     O.TILE_SECONDS[0] = 0.0
     t0 = time.perf_counter()
     O.render(scene, cam, st, tiles=tiles)
     wall = time.perf_counter() - t0
     tile_s = O.TILE_SECONDS[0]
-    frame_s = (wall - tile_s) + tile_s * nt / len(tiles)
-    return frame_s, wall, len(tiles), nt
+    frame_s = wall if tiles is None else (wall - tile_s) + tile_s * nt / len(tiles)
+    return frame_s, wall, min(n_tiles, nt), nt
+
+
+# strips per frame of the reference arm: one step = one strip of tile rows, so
+# a step is a bounded ~1-3 s of host work at every config
+STRIPS_TARGET = {1: 1, 2: 8, 3: 4, 4: 16, 5: 32}
+
+
+def strips_for(cfg, steps):
+    """Strips per frame: the smallest divisor of ``steps`` >= the config's
+    target (so the timed steps are exactly steps / strips whole frames), or
+    ``steps`` itself when it is smaller than the target."""
+    tgt = STRIPS_TARGET[cfg]
+    for d in range(tgt, steps + 1):
+        if steps % d == 0:
+            return d
+    return max(steps, 1)
+
+
+def single_thread_sample(cfg, scene, cam, ss):
+    """BASELINE.md section 2 variant (b): threads=1 with default (multi-
+    threaded) OpenBLAS.  Bounded: the per-frame preprocessing + every 16th
+    tile row, extrapolated to the frame (rows x 16)."""
+    from oracle import ges_oracle as O
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:   # pragma: no cover
+        threadpool_limits = None
+    st = _oracle_settings(cfg, 1, ss)
+    ntx = (cam.width + 15) // 16
+    nty = (cam.height + 15) // 16
+    tiles = [r * ntx + c for r in range(0, nty, 16) for c in range(ntx)]
+    ctx = threadpool_limits(limits=os.cpu_count() or 1, user_api="blas") if threadpool_limits else None
+    try:
+        if ctx is not None:
+            ctx.__enter__()
+        O.TILE_SECONDS[0] = 0.0
+        t0 = time.perf_counter()
+        O.render(scene, cam, st, tiles=tiles)
+        wall = time.perf_counter() - t0
+    finally:
+        if ctx is not None:
+            ctx.__exit__(None, None, None)
+    tile_s = O.TILE_SECONDS[0]
+    frame_s = (wall - tile_s) + tile_s * (ntx * nty) / len(tiles)
+    return {"value": 1.0 / frame_s, "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": f"threads=1, default OpenBLAS threading (BASELINE.md 2(b)): per-frame preprocessing "
+                      f"+ {len(tiles)} of {ntx * nty} tiles (every 16th tile row), extrapolated to the frame",
+            "frame_s": frame_s, "measured_wall_s": wall}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm on this box's host cores."""
+    """--impl reference: the reference algorithm (oracle/ges_oracle.py, the
+    NumPy restatement pinned to the reference's goldens; float32 like the
+    reference default) on this box's host cores, all threads, timed in whole
+    frames.  One step = one strip of tile rows of the frame (the first strip
+    of a frame also does the frame's preprocessing), so K steps are exactly
+    K / strips frames and ms_per_step is the measured wall time per step."""
     if rank != 0:
         return
+    from oracle import ges_oracle as O
     cfg = args.config
     scene = S.config_scene(cfg)
     cam = views_for(cfg, 0, 1, 1)[0]
     threads = os.cpu_count() or 1
-    per_rank = args.views or DEFAULT_VIEWS[cfg]
-    n_tiles = 64
-    times = []
-    wall = 0.0
-    for i in range(args.warmup + args.steps):
-        fs, w, nt, tot = cpu_sample(cfg, scene, cam, n_tiles, threads, args.ss)
-        if i >= args.warmup:
-            times.append(fs)
-            wall += w
-    frame_s = statistics.median(times)
-    fps = 1.0 / frame_s
-    sample = (f"per step: full per-frame preprocessing + {nt} of {tot} tiles of one "
-              f"{cam.width}x{cam.height} view, extrapolated to the frame; float32; "
-              f"{threads} tile threads, OPENBLAS_NUM_THREADS=1")
+    st = _oracle_settings(cfg, threads, args.ss)
+    nstrips = strips_for(cfg, args.steps)
+    groups = O.strip_groups(cam.height, cam.width, nstrips)
+    nstrips = len(groups)
+
+    def strips():
+        while True:   # an endless sequence of frames, one strip per step
+            yield from O.render_steps(scene, cam, st, groups)
+
+    seq = strips()
+    for _ in range(args.warmup):
+        next(seq)
+    seq = strips()   # the timed steps start at a frame boundary
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        next(seq)
+    wall = time.perf_counter() - t0
+    frames = args.steps / nstrips
+    fps = frames / wall
+    single = None if args.no_cpu else single_thread_sample(cfg, scene, cam, args.ss)
+    sample = (f"{args.steps} steps = {frames:g} whole {cam.width}x{cam.height} frames, each rendered as "
+              f"{nstrips} strips of tile rows (one strip per step, the frame's preprocessing in its first "
+              f"strip); oracle/ges_oracle.py float32 with per-tile candidate lists (faster than the "
+              f"reference's O(N x tiles) selection scan, forward.py:168-169); {threads} tile threads, "
+              f"OPENBLAS_NUM_THREADS=1 (BASELINE.md 2(a))")
     line = {"metric": METRIC, "value": fps, "unit": "frames/s", "impl": "reference",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": frame_s * per_rank * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": wall * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": base_config(cfg, per_rank, world, args.ss),
+            "config": {**base_config(cfg, 1, world, args.ss), "strips_per_frame": nstrips,
+                       "views_per_rank_per_step": f"1/{nstrips} of a view"},
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
-                             "cpu_model": cpu_model(),
-                             "sample": sample, "measured_wall_s": wall},
+                             "cpu_model": cpu_model(), "sample": sample, "measured_wall_s": wall,
+                             "frame_s": wall / frames, "single_thread": single},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -61,6 +61,18 @@ TIE_PARALLEL = 10.0         # |n.d| within 10x the parallel threshold
 TIE_NEAR_ABS = 1e-6         # |t - 0.01| below this
 TIE_ALPHA = 1e-3            # |255 alpha - 1| below this
 TIE_GATE_REL = 1e-5         # |d - (D_s + eps)| < TIE_GATE_REL * |D_s + eps|
+# Conditioning-aware float32 error model for ray-plane hits.  At grazing
+# incidence the hit depth t = n.q / n.d and the disc coordinates (u, v) are
+# ill-conditioned in the ray direction d (condition ~ |d| / |n.d|), so a float32
+# evaluation (whose ray and plane coefficients carry ~EPS32 relative rounding)
+# can move r^2 = u^2 + v^2 and t far more than the fixed relative thresholds
+# above.  A decision is also a tie when its float64 margin lies within
+# TIE_F32_K first-order float32 error bounds:
+#   err(t)   = K * EPS32 * t * (|d| / |n.d| + 2)
+#   err(r^2) = K * EPS32 * |d| * (2 (|u| |c_u| + |v| |c_v|) + 2 r^2) / |n.d|
+# with c_u = (a1 (n.q) - n (a1.q)) / s1 (so that u = c_u.d / n.d), c_v alike.
+EPS32 = 2.0 ** -24
+TIE_F32_K = 4.0
 
 
 def _is_2d(kind) -> bool:
@@ -301,6 +313,10 @@ class SurfelOut:
     coverage: np.ndarray
     winner: np.ndarray
     tie: np.ndarray = None      # (H, W) bool, oracle extension
+    depth_err: np.ndarray = None  # (H, W) float32 error bound of the winner's depth (TIE_F32_K model)
+    tie_sub: np.ndarray = None    # (H, W) bool, supersample=4: a tie at sub-samples (0,1), (1,0) or
+                                  # (1,1) only -- winner/depth come from sub-sample (0,0), so only
+                                  # the box-mean colour may legitimately differ
 
 
 @dataclass
@@ -331,6 +347,16 @@ class RenderOut:
         return t
 
     @property
+    def tie_color(self):
+        """supersample=4: pixels whose box-mean colour (only) may differ
+        because a sub-sample other than (0, 0) is a surfel tie.  Their winner,
+        depth and Gaussian sums are still checked; image and surfel colour
+        are excluded (and counted)."""
+        if self.surfels.tie_sub is None:
+            return np.zeros(self.surfels.tie.shape, bool)
+        return self.surfels.tie_sub & ~self.tie
+
+    @property
     def tie_cut(self):
         """Per pixel, the number of contributing Gaussian fragments whose
         alpha lies within TIE_ALPHA of the 1/255 cutoff: a float32 evaluation
@@ -352,6 +378,17 @@ def _settings(settings):
 
 # --- pass 1: surfel z-buffer (forward.py:127-209) --------------------------
 def rasterize_surfels(scene, cam, settings=None, *, tiles=None, ties=False) -> SurfelOut:
+    run, finish, _ = _surfel_job(scene, cam, settings, ties)
+    run(tiles)
+    return finish()
+
+
+def _surfel_job(scene, cam, settings, ties):
+    """The surfel pass split at its tile loop: the per-frame preprocessing
+    (forward.py:148-158) runs here; returns ``run(tiles)`` (the per-tile
+    z-buffer of the given base-resolution tiles, forward.py:166-207),
+    ``finish()`` (the supersample reduction, forward.py:201-207 -> SurfelOut)
+    and the base-resolution depth map view the Gaussian pass gates against."""
     st = _settings(settings)
     dt = st["dtype"]
     grid = 2 if st["supersample"] == 4 else 1
@@ -365,6 +402,7 @@ def rasterize_surfels(scene, cam, settings=None, *, tiles=None, ties=False) -> S
     normal = np.zeros((H, W, 3), dtype=dt)
     winner = np.full((H, W), -1, dtype=np.int32)
     tie = np.zeros((H, W), dtype=bool)
+    derr = np.zeros((H, W), dtype=np.float64)
 
     s = scene.surfels
     ns = int(np.asarray(s.pos).shape[0])
@@ -387,6 +425,10 @@ def rasterize_surfels(scene, cam, settings=None, *, tiles=None, ties=False) -> S
         a1q_all = np.sum(a1d * qd, axis=1)
         a2q_all = np.sum(a2d * qd, axis=1)
         R2 = R_OPAQUE * R_OPAQUE
+        cu_n = np.linalg.norm(a1 * np.sum(n * q, axis=1, keepdims=True)
+                              - n * np.sum(a1 * q, axis=1, keepdims=True), axis=1) / scale[:, 0]
+        cv_n = np.linalg.norm(a2 * np.sum(n * q, axis=1, keepdims=True)
+                              - n * np.sum(a2 * q, axis=1, keepdims=True), axis=1) / scale[:, 1]
         select = _Selector(idx, x0, x1, y0, y1, H, W)
 
         def do_tile(t):
@@ -414,30 +456,44 @@ def rasterize_surfels(scene, cam, settings=None, *, tiles=None, ties=False) -> S
             color[ty0:ty1, tx0:tx1] = np.where(cov[:, None], cols[sel[k]], bg).reshape(shp + (3,))
             normal[ty0:ty1, tx0:tx1] = np.where(cov[:, None], n_vis[sel[k]], 0.0).reshape(shp + (3,))
             if ties:
-                with np.errstate(invalid="ignore", over="ignore"):
-                    lim = np.where(cov, best * (1.0 + TIE_DEPTH_REL), np.inf)
-                    dm2 = dm.copy()
-                    dm2[k, cols_px] = np.inf
-                    second = dm2.min(axis=0)
-                    close = cov & (second <= lim)
-                    fragile = ((np.abs(r2 - R2) < TIE_RADIUS_REL * R2)
-                               | (np.abs(ndot) < TIE_PARALLEL * PARALLEL_EPS * dn)
-                               | (np.abs(th - NEAR) < TIE_NEAR_ABS))
-                    front = (th > NEAR - TIE_NEAR_ABS) & (th <= lim[None, :])
-                    near_par = np.abs(ndot) < TIE_PARALLEL * PARALLEL_EPS * dn
+                with np.errstate(invalid="ignore", over="ignore", divide="ignore"):
+                    andot = np.abs(ndot)
+                    f32 = TIE_F32_K * EPS32
+                    terr = f32 * np.abs(th) * (dn / andot + 2.0)          # err(t)
+                    rerr = f32 * dn * (2.0 * (np.abs(u) * cu_n[sel][:, None] + np.abs(v) * cv_n[sel][:, None])
+                                       + 2.0 * r2) / andot             # err(r^2)
+                    berr = np.where(cov, terr[k, cols_px], 0.0)
+                    lim = np.where(cov, best * (1.0 + TIE_DEPTH_REL) + berr, np.inf)
+                    lo = th - terr
+                    lo[k, cols_px] = np.inf
+                    close = cov & (np.where(ok, lo, np.inf).min(axis=0) <= lim)
+                    fragile = ((np.abs(r2 - R2) < np.maximum(TIE_RADIUS_REL * R2, rerr))
+                               | (andot < TIE_PARALLEL * PARALLEL_EPS * dn)
+                               | (np.abs(th - NEAR) < np.maximum(TIE_NEAR_ABS, terr)))
+                    front = (th + terr > NEAR - TIE_NEAR_ABS) & (lo <= lim[None, :])
+                    front[k, cols_px] |= cov
+                    near_par = andot < TIE_PARALLEL * PARALLEL_EPS * dn
                     flag = close | np.any(fragile & (front | near_par), axis=0)
                 tie[ty0:ty1, tx0:tx1] = flag.reshape(shp)
+                derr[ty0:ty1, tx0:tx1] = berr.reshape(shp)
 
-        _run(do_tile, _tiles_for(H, W, _hires_tiles(tiles, base, grid)), st["threads"])
+    def run(tiles):
+        if ns:
+            _run(do_tile, _tiles_for(H, W, _hires_tiles(tiles, base, grid)), st["threads"])
 
-    if grid > 1:
+    def finish():
+        if grid == 1:
+            return SurfelOut(color, depth, normal, np.isfinite(depth), winner, tie, derr,
+                             np.zeros(tie.shape, bool))
         h, w = base.height, base.width
-        color = color.reshape(h, grid, w, grid, 3).mean(axis=(1, 3), dtype=dt)
-        depth = depth[0::grid, 0::grid]
-        normal = normal[0::grid, 0::grid]
-        winner = winner[0::grid, 0::grid]
-        tie = tie.reshape(h, grid, w, grid).any(axis=(1, 3))
-    return SurfelOut(color, depth, normal, np.isfinite(depth), winner, tie)
+        tie_any = tie.reshape(h, grid, w, grid).any(axis=(1, 3))
+        t0 = tie[0::grid, 0::grid]           # the reported sub-sample (forward.py:205-207)
+        d0 = depth[0::grid, 0::grid]
+        return SurfelOut(color.reshape(h, grid, w, grid, 3).mean(axis=(1, 3), dtype=dt), d0,
+                         normal[0::grid, 0::grid], np.isfinite(d0), winner[0::grid, 0::grid], t0,
+                         derr[0::grid, 0::grid], tie_any & ~t0)   # tie_sub: only the box-mean colour
+
+    return run, finish, (depth[0::grid, 0::grid], derr[0::grid, 0::grid])
 
 
 def surfel_tile_counts(scene, cam):
@@ -521,7 +577,17 @@ def object_filter_2d(q, a1, a2, scale, cam: Cam, r=SCREEN_VAR):
 
 
 def accumulate_gaussians(scene, cam, surfel_depth, settings=None, *, tiles=None,
-                         ties=False) -> GaussOut:
+                         ties=False, depth_err=None) -> GaussOut:
+    run, out = _gauss_job(scene, cam, surfel_depth, settings, ties, depth_err)
+    run(tiles)
+    return out
+
+
+def _gauss_job(scene, cam, surfel_depth, settings, ties, depth_err=None):
+    """The Gaussian pass split at its tile loop: per-frame preprocessing
+    (projection, bounds, colours; forward.py:212-300) here; returns
+    ``run(tiles)`` and the GaussOut it fills.  ``surfel_depth`` is read per
+    tile when the tile runs (the same array may still be filling)."""
     st = _settings(settings)
     dt = st["dtype"]
     c = as_cam(cam)
@@ -535,28 +601,27 @@ def accumulate_gaussians(scene, cam, surfel_depth, settings=None, *, tiles=None,
     g = scene.gaussians
     ng = int(np.asarray(g.pos).shape[0])
     if ng == 0:
-        return out
-    ds = np.asarray(surfel_depth, dtype=dt)
+        return (lambda tiles: None), out
+    ds = surfel_depth if surfel_depth.dtype == dt else np.asarray(surfel_depth, dtype=dt)
+    st["depth_err"] = np.zeros(ds.shape) if depth_err is None else np.asarray(depth_err)
     es, sigma, eps = gaussian_eff(g)
     if st["epsilon_mode"] == "constant":          # forward.py:212-215
         eps = np.full(ng, float(st["epsilon_value"]))
     eps = eps.astype(dt)
     cols = view_colors(g.pos, g.sh, c).astype(dt)
-    if _is_2d(g.kind):
-        _acc_2d(g, c, ds, eps, cols, es, sigma, st, out, tiles, ties)
-    else:
-        _acc_3d(g, c, ds, eps, cols, es, sigma, st, out, tiles, ties)
-    return out
+    acc = _acc_2d if _is_2d(g.kind) else _acc_3d
+    return acc(g, c, ds, eps, cols, es, sigma, st, out, ties), out
 
 
-def _near_gate(d, thr):
-    """Gate decision d < D_s + eps within TIE_GATE_REL of flipping.  An
-    uncovered pixel has thr = +inf: its gate always passes (forward.py:310,
-    SPEC.md:227) and is never a tie."""
-    return np.isfinite(thr) & (np.abs(d - thr) < TIE_GATE_REL * np.abs(thr))
+def _near_gate(d, thr, err=0.0):
+    """Gate decision d < D_s + eps within TIE_GATE_REL (plus the float32
+    error bounds ``err`` of D_s and of d) of flipping.  An uncovered pixel has
+    thr = +inf: its gate always passes (forward.py:310) and is
+    never a tie."""
+    return np.isfinite(thr) & (np.abs(d - thr) < TIE_GATE_REL * np.abs(thr) + err)
 
 
-def _acc_3d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
+def _acc_3d(g, cam, ds, eps, cols, es, sigma, st, out, ties):
     """forward.py:248-321."""
     dt = st["dtype"]
     H, W = cam.height, cam.width
@@ -625,15 +690,15 @@ def _acc_3d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
             with np.errstate(invalid="ignore"):
                 raw = sg[sel][:, None, None] * np.exp(pw)
                 near_cut = np.abs(255.0 * raw - 1.0) < TIE_ALPHA
-                near_gate = _near_gate(dep[sel][:, None, None], thr)
+                near_gate = _near_gate(dep[sel][:, None, None], thr, st["depth_err"][ty0:ty1, tx0:tx1][None])
             hard = near_gate & keep
             out.tie[ty0:ty1, tx0:tx1] |= hard.any(axis=0)
             out.tie_cut[ty0:ty1, tx0:tx1] += (near_cut & (gate | near_gate) & ~hard).sum(axis=0)
 
-    _run(do_tile, _tiles_for(H, W, tiles), st["threads"])
+    return lambda tiles: _run(do_tile, _tiles_for(H, W, tiles), st["threads"])
 
 
-def _acc_2d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
+def _acc_2d(g, cam, ds, eps, cols, es, sigma, st, out, ties):
     """Planar Gaussians (forward.py:324-381)."""
     dt = st["dtype"]
     H, W = cam.height, cam.width
@@ -660,6 +725,9 @@ def _acc_2d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
     qd, a1d, a2d, nd_ = (v.astype(dt) for v in (q, a1, a2, n))
     s1, s2 = scale[:, 0].astype(dt), scale[:, 1].astype(dt)
     sg = sig.astype(dt)
+    nq = np.sum(n * q, axis=1, keepdims=True)
+    cu_n = np.linalg.norm(a1 * nq - n * np.sum(a1 * q, axis=1, keepdims=True), axis=1) / scale[:, 0]
+    cv_n = np.linalg.norm(a2 * nq - n * np.sum(a2 * q, axis=1, keepdims=True), axis=1) / scale[:, 1]
 
     select = _Selector(idx, x0, x1, y0, y1, H, W)
 
@@ -689,15 +757,21 @@ def _acc_2d(g, cam, ds, eps, cols, es, sigma, st, out, tiles, ties):
             out.depth[ty0:ty1, tx0:tx1] += np.where(a > 0, a * np.where(ok, th, 0.0), 0.0).sum(axis=0).reshape(th_, tw_)
             out.normal[ty0:ty1, tx0:tx1] += (a.T @ n_vis[sel]).reshape(th_, tw_, 3)
         if ties:
-            with np.errstate(invalid="ignore"):
-                near_cut = np.abs(255.0 * raw - 1.0) < TIE_ALPHA
-                near_gate = _near_gate(th, thr)
+            with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+                f32 = TIE_F32_K * EPS32
+                andot = np.abs(ndot)
+                terr = f32 * np.abs(th) * (dn / andot + 2.0)
+                r2 = u * u + v * v
+                rerr = f32 * dn * (2.0 * (np.abs(u) * cu_n[sel][:, None] + np.abs(v) * cv_n[sel][:, None])
+                                   + 2.0 * r2) / andot
+                near_cut = np.abs(255.0 * raw - 1.0) < TIE_ALPHA + 0.5 * rerr
+                near_gate = _near_gate(th, thr, st["depth_err"][ty0:ty1, tx0:tx1].reshape(1, -1) + terr)
                 fl = near_gate & keep
                 fl |= ok & (np.abs(ndot) < TIE_PARALLEL * PARALLEL_EPS * dn) & keep
             out.tie[ty0:ty1, tx0:tx1] |= fl.any(axis=0).reshape(th_, tw_)
             out.tie_cut[ty0:ty1, tx0:tx1] += (near_cut & (gate | near_gate) & ~fl).sum(axis=0).reshape(th_, tw_)
 
-    _run(do_tile, _tiles_for(H, W, tiles), st["threads"])
+    return lambda tiles: _run(do_tile, _tiles_for(H, W, tiles), st["threads"])
 
 
 # --- composite / geometry / render (forward.py:384-417) ---------------------
@@ -717,19 +791,52 @@ def smooth_geometry(sb, gb):
 
 
 def render(scene, cam, settings=None, *, tiles=None, ties=False) -> RenderOut:
+    """forward.py:403-417 (optionally restricted to base tiles ``tiles``)."""
+    steps = render_steps(scene, cam, settings, [tiles], ties=ties)
+    while True:
+        try:
+            next(steps)
+        except StopIteration as fin:
+            return fin.value
+
+
+def render_steps(scene, cam, settings, tile_groups, *, ties=False):
+    """Generator form of render(): the first next() does the per-frame
+    preprocessing of both passes and the tiles of ``tile_groups[0]``; every
+    later next() renders one more group (surfel tiles, then the Gaussian
+    tiles of the same group).  The RenderOut is the StopIteration value.
+    bench.py's reference arm times each next() as one bounded step, so
+    whole frames are measured in row strips without extrapolation."""
     st = _settings(settings)
-    sb = rasterize_surfels(scene, cam, settings, tiles=tiles, ties=ties)
-    if st["layers"] == "surfels_only":
+    srun, sfinish, (d0, e0) = _surfel_job(scene, cam, settings, ties)
+    grun = gb = None
+    if st["layers"] != "surfels_only":
+        grun, gb = _gauss_job(scene, cam, d0, settings, ties, e0)
+    for grp in tile_groups:
+        srun(grp)
+        if grun is not None:
+            grun(grp)
+        yield
+    sb = sfinish()
+    if gb is None:
         gb = GaussOut(np.zeros_like(sb.color), np.zeros_like(sb.depth),
                       tie=np.zeros(sb.depth.shape, bool), tie_cut=np.zeros(sb.depth.shape, np.int32))
         return RenderOut(sb.color.copy(), sb, gb)
-    gb = accumulate_gaussians(scene, cam, sb.depth, settings, tiles=tiles, ties=ties)
     if st["layers"] == "gaussians_only":
         bg = np.asarray(st["background"], dtype=st["dtype"])
         img = np.where(gb.weight[..., None] > 0,
                        gb.color / np.maximum(gb.weight, 1e-12)[..., None], bg)
         return RenderOut(img, sb, gb)
     return RenderOut(composite(sb.color, gb), sb, gb)
+
+
+def strip_groups(height, width, nstrips):
+    """Base-tile indices of ``nstrips`` horizontal strips of whole tile rows
+    covering the frame (render_steps' tile groups)."""
+    ntx = (width + TILE - 1) // TILE
+    nty = (height + TILE - 1) // TILE
+    cuts = np.linspace(0, nty, min(nstrips, nty) + 1).round().astype(int)
+    return [list(range(a * ntx, b * ntx)) for a, b in zip(cuts[:-1], cuts[1:])]
 
 
 def default_threads():

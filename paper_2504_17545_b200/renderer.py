@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
+import zlib
 from collections import OrderedDict
 from dataclasses import dataclass
 
@@ -175,49 +177,90 @@ class DeviceScene:
 
 
 class _SceneCache:
-    """LRU of packed scenes keyed by the identity (object, data pointer,
-    shape) of the source arrays.  Replacing an array (``s.pos = new``, as the
-    reference's optimiser does, optim.py:126-135) re-packs automatically;
-    writing INTO a cached array in place is not detected: call
-    ``invalidate(scene)`` (or ``clear()``) after such an edit."""
+    """Thread-safe LRU of packed scenes keyed by the identity (object, data
+    pointer, shape) of the source arrays.  Replacing an array (``s.pos =
+    new``, as the reference's optimiser does, optim.py:126-135) re-packs
+    automatically.  Writing INTO a cached array in place is detected through
+    a fingerprint of every source array checked on each hit:
 
-    def __init__(self, size=4):
+    * ``verify = "sample"`` (default): CRC of up to SAMPLE elements spread
+      evenly over each array (~tens of microseconds per call) -- catches
+      edits that touch many elements (optimiser steps, rescaling, reloads);
+      an edit of a few unsampled elements needs ``invalidate(scene)``;
+    * ``verify = "full"``: CRC of every byte (exact; ~0.5 s per call at
+      config 2's 1.3M primitives);
+    * ``verify = "none"``: identity only.
+
+    The reference's render is a pure function of the arrays
+    (SPEC.md:100-101); the cache never changes a result except by serving a
+    scene that was edited in place without a detectable change."""
+
+    SAMPLE = 4096
+
+    def __init__(self, size=4, verify="sample"):
         self.size = size
+        self.verify = verify
         self.d: OrderedDict = OrderedDict()
+        self.lock = threading.RLock()
 
     @staticmethod
-    def _key(scene, device):
+    def _arrays(scene):
         s, g = scene.surfels, scene.gaussians
-        arrs = (s.pos, s.quat, s.log_scale, s.sh, g.pos, g.raw_opacity, g.quat, g.log_scale, g.sh,
+        return (s.pos, s.quat, s.log_scale, s.sh, g.pos, g.raw_opacity, g.quat, g.log_scale, g.sh,
                 getattr(g, "filter3d", None))
+
+    @classmethod
+    def _key(cls, scene, device):
+        arrs = cls._arrays(scene)
         parts = []
         for a in arrs:
             if a is None:
                 parts.append(None)
             else:
                 parts.append((id(a), np.asarray(a).__array_interface__["data"][0], np.asarray(a).shape))
-        return (str(device), _kind_dim(g), tuple(parts)), arrs
+        return (str(device), _kind_dim(scene.gaussians), tuple(parts)), arrs
+
+    def _fingerprint(self, arrs, mode):
+        if mode == "none":
+            return None
+        crc = 0
+        for a in arrs:
+            if a is None:
+                continue
+            a = np.asarray(a)
+            if mode == "full" or a.size <= self.SAMPLE:
+                v = np.ascontiguousarray(a)
+            else:
+                v = a.flat[np.linspace(0, a.size - 1, self.SAMPLE).astype(np.int64)]
+            crc = zlib.crc32(v.view(np.uint8).reshape(-1) if v.size else b"", crc)
+        return crc
 
     def get(self, scene, device):
         key, arrs = self._key(scene, device)
-        hit = self.d.get(key)
-        if hit is not None:
+        with self.lock:
+            mode = self.verify
+            fp = self._fingerprint(arrs, mode)
+            hit = self.d.get(key)
+            if hit is not None and hit[2] == (mode, fp):
+                self.d.move_to_end(key)
+                return hit[0]
+            ds = DeviceScene(scene, device)
+            self.d[key] = (ds, arrs, (mode, fp))   # holding arrs pins the ids
             self.d.move_to_end(key)
-            return hit[0]
-        ds = DeviceScene(scene, device)
-        self.d[key] = (ds, arrs)   # holding arrs pins the ids
-        while len(self.d) > self.size:
-            self.d.popitem(last=False)
-        return ds
+            while len(self.d) > self.size:
+                self.d.popitem(last=False)
+            return ds
 
     def clear(self):
-        self.d.clear()
+        with self.lock:
+            self.d.clear()
 
     def invalidate(self, scene):
         """Drop the packed copies of ``scene`` (after in-place edits of its arrays)."""
         key, _ = self._key(scene, None)
-        for k in [k for k in self.d if k[1:] == key[1:]]:
-            del self.d[k]
+        with self.lock:
+            for k in [k for k in self.d if k[1:] == key[1:]]:
+                del self.d[k]
 
 
 SCENE_CACHE = _SceneCache()
@@ -328,6 +371,9 @@ class Renderer:
                                                 C.byref(st_c), C.byref(out_c), *args_ws, self.cap_g,
                                                 st_ptr, stream)
             _lib.check(rc, "render")
+            # the packed scene may be dropped by another thread's cache eviction while this
+            # frame is in flight: keep its memory out of reuse until this stream is done
+            ds.blob.record_stream(torch.cuda.current_stream(self.device))
             if not check:
                 return fr
             sp, gp, ovf = fr.pairs()
@@ -338,14 +384,21 @@ class Renderer:
         raise RuntimeError("tile pair lists overflowed repeatedly")
 
 
-_RENDERERS: dict = {}
+_LOCAL = threading.local()
 
 
 def default_renderer(device=None) -> Renderer:
+    """The calling thread's renderer for ``device``: one frame workspace per
+    (Python thread, device), so concurrent render() calls from several
+    threads never share a workspace (the reference's render is thread-safe,
+    SPEC.md:100-101)."""
     dev = torch.device(device or "cuda")
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
-    r = _RENDERERS.get(dev)
+    rs = getattr(_LOCAL, "renderers", None)
+    if rs is None:
+        rs = _LOCAL.renderers = {}
+    r = rs.get(dev)
     if r is None:
-        r = _RENDERERS[dev] = Renderer(dev)
+        r = rs[dev] = Renderer(dev)
     return r

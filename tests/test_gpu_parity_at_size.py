@@ -19,7 +19,7 @@ import paper_2504_17545_b200 as G  # noqa: E402
 from paper_2504_17545_b200 import scenes as S  # noqa: E402
 from golden_io import settings_ns  # noqa: E402
 from oracle import ges_oracle as O  # noqa: E402
-from parity import assert_parity, compare  # noqa: E402
+from parity import assert_parity, compare_oracle  # noqa: E402
 
 THREADS = os.cpu_count() or 1
 
@@ -34,6 +34,7 @@ def _dicts(out, ora):
     g = dict(image=out.image, s_winner=out.surfels.winner, s_depth=out.surfels.depth,
              s_color=out.surfels.color, g_color=out.gaussians.color, g_weight=out.gaussians.weight)
     o = dict(image=ora.image, s_winner=ora.surfels.winner, s_depth=ora.surfels.depth,
+             s_depth_err=ora.surfels.depth_err,
              s_color=ora.surfels.color, g_color=ora.gaussians.color, g_weight=ora.gaussians.weight)
     return g, o
 
@@ -47,19 +48,21 @@ def _region(cam, tiles):
     return region
 
 
-def _check(name, scene, cam, st, tiles=None):
+def _check(name, scene, cam, st, tiles=None, **bounds):
     out = G.render(scene, cam, G.RenderSettings(dtype=np.float32, **st))
     ns = settings_ns(st, np.float64)
     ns.threads = THREADS
     ora = O.render(scene, cam, ns, tiles=tiles, ties=True)
     region = None if tiles is None else _region(cam, tiles)
     g, o = _dicts(out, ora)
-    rep = compare(g, o, ora.tie, tie_cut=ora.tie_cut, region=region)
+    rep = compare_oracle(g, o, ora, region=region)
     print(f"\n[{name}] {cam.width}x{cam.height} {st}: pixels {rep['pixels']}, excluded {rep['excluded']} "
           f"({100.0 * rep['excluded'] / rep['pixels']:.3f} %), cut-flagged {rep['cut_flagged']}, "
+          f"colour-only flagged {rep['color_flagged']}, winner mismatches on ties "
+          f"{rep['winner_mismatch_incl_ties']}, "
           f"image max abs {rep['image_maxabs']:.2e}, depth rel {rep['depth_rel_max']:.2e}, "
           f"psnr {rep['psnr']:.1f} dB")
-    assert_parity(rep)
+    assert_parity(rep, **bounds)
     return rep
 
 
@@ -69,7 +72,7 @@ def _dense_tiles(scene, cam, n_dense, n_random, seed):
     cnt = O.surfel_tile_counts(scene, cam)
     dense = np.argsort(-cnt, kind="stable")[:n_dense].tolist()
     rest = np.setdiff1d(np.arange(cnt.size), dense)
-    rnd = np.random.default_rng(seed).choice(rest, n_random, replace=False).tolist()
+    rnd = np.random.default_rng(seed).choice(rest, n_random, replace=False).tolist() if n_random else []
     return sorted(dense + rnd)
 
 
@@ -100,14 +103,28 @@ def test_config4_mip_all_scales():
     assert rep["pixels"] == 96 * 256
 
 
-def test_config5_4k_view_tiles():
-    """Config 5 (3M surfels + 1M Gaussians, 3840x2160, orbit camera 0): 96
-    tiles, the 32 densest + 64 random."""
+def test_config5_4k_view_full_frame():
+    """Config 5 (3M surfels + 1M Gaussians, 3840x2160, orbit camera 0): every
+    pixel of one 4K view (the oracle takes ~1-2 min on the box's cores)."""
     sc = S.config_scene(5)
     cam = S.config_cameras(5)[0]
-    tiles = _dense_tiles(sc, cam, 32, 64, 12)
-    rep = _check("config5", sc, cam, {}, tiles=tiles)
-    assert rep["pixels"] == 96 * 256
+    rep = _check("config5", sc, cam, {})
+    assert rep["pixels"] == 3840 * 2160
+
+
+def test_config5_densest_tiles():
+    """Config 5: the 64 densest 16x16 tiles of the 4K view (longest surfel
+    candidate lists) on their own, so their exclusion count is visible.
+    Every per-pixel check is the strict one; the frame-level bounds
+    (excluded fraction, PSNR) are asserted over the whole frame above --
+    on 16k of the densest pixels a single tie flip alone moves the PSNR by
+    several dB, so here the exclusions are bounded at 1 % and PSNR is only
+    reported."""
+    sc = S.config_scene(5)
+    cam = S.config_cameras(5)[0]
+    tiles = _dense_tiles(sc, cam, 64, 0, 12)
+    rep = _check("config5-dense", sc, cam, {}, tiles=tiles, excluded_frac=0.01, psnr_min=-np.inf)
+    assert rep["pixels"] == 64 * 256
 
 
 def test_config2_supersample4_full_frame():
