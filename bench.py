@@ -67,7 +67,18 @@ WORKLOADS = {
     4: "config4 (Mip): 1M surfels + 300k filtered Gaussians, SH3, 3840x2160, mip=True",
     5: "config5: 3M surfels + 1M Gaussians, SH3, 3840x2160 orbit views",
 }
-DEFAULT_VIEWS = {1: 32, 2: 32, 3: 32, 4: 4, 5: 8}
+DEFAULT_VIEWS = {1: 32, 2: 32, 3: 32, 4: 4, 5: None}
+ORBIT_VIEWS = 256   # config 5: the 256-camera orbit, split over the ranks (strong scaling)
+
+
+def per_rank_views(cfg, world, views):
+    """Views per rank per step: --views, else the config default; config 5
+    is the fixed 256-camera batch in contiguous blocks of ceil(256 / P)."""
+    if views:
+        return views
+    if cfg == 5:
+        return math.ceil(ORBIT_VIEWS / world)
+    return DEFAULT_VIEWS[cfg]
 
 
 def views_for(cfg, rank, world, per_rank):
@@ -75,9 +86,12 @@ def views_for(cfg, rank, world, per_rank):
     total = per_rank * world
     ks = range(rank * per_rank, (rank + 1) * per_rank)
     if cfg == 5:   # 256-camera 4K orbit, contiguous blocks per rank
-        cams = S.orbit_cameras((0, 0, 0), 4.0, 256, height=1.0, fov_deg=50.0,
+        from paper_2504_17545_b200.multiview import shard
+        cams = S.orbit_cameras((0, 0, 0), 4.0, ORBIT_VIEWS, height=1.0, fov_deg=50.0,
                                width=3840, height_px=2160)
-        return [cams[k % 256] for k in ks]
+        if per_rank * world >= ORBIT_VIEWS and per_rank == math.ceil(ORBIT_VIEWS / world):
+            return [cams[k] for k in shard(ORBIT_VIEWS, rank, world)]
+        return [cams[k % ORBIT_VIEWS] for k in ks]
     if cfg == 4:   # the 8(d) pose at 1/8, 1/4, 1/2 and full 4K resolution
         return [S.make_camera(3840 // f, 2160 // f, azim=0.3 + 2.0 * math.pi * k / total)
                 for k in ks for f in (8, 4, 2, 1)][:per_rank]
@@ -85,13 +99,20 @@ def views_for(cfg, rank, world, per_rank):
     return [S.make_camera(w, h, azim=0.3 + 2.0 * math.pi * k / total) for k in ks]
 
 
+def out_bytes_per_px(cfg):
+    """Output bytes per pixel of the bench workload: fp32 RGB image, depth and
+    winner id (20 B) -- config 5's 256-view batch keeps the RGBA8 frame the
+    gather delivers (4 B)."""
+    return 4 if cfg == 5 else 20
+
+
 def b_alg(cfg, cams):
-    """Algorithmic bytes per frame: scene read once + 20 B/px,
-    averaged over the step's views."""
+    """Algorithmic bytes per frame: scene read once + the
+    output bytes per pixel, averaged over the step's views."""
     c = S.CONFIGS[cfg]
     K = (c["deg"] + 1) ** 2
     px = sum(int(v.width) * int(v.height) for v in cams) / len(cams)
-    return c["ns"] * (36 + 12 * K) + c["ng"] * (44 + 12 * K) + px * 20
+    return c["ns"] * (36 + 12 * K) + c["ng"] * (44 + 12 * K) + px * out_bytes_per_px(cfg)
 
 
 def base_config(cfg, per_rank, world, ss):
@@ -317,7 +338,7 @@ def run_gpu(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     cfg = args.config
-    per_rank = args.views or DEFAULT_VIEWS[cfg]
+    per_rank = per_rank_views(cfg, world, args.views)
     scene = S.config_scene(cfg)
     cams = views_for(cfg, rank, world, per_rank)
     settings = G.RenderSettings(supersample=args.ss, mip=(cfg == 4), layers=args.layers)
@@ -353,12 +374,13 @@ def run_gpu(args, rank, world, local_rank):
                       file=sys.stderr)
         else:
             gather_used = "peer"
-    want = ("image", "s_depth", "s_winner") + (("image_rgba8",) if world > 1 and sink is None else ())
+    want = (() if cfg == 5 else ("image", "s_depth", "s_winner")) + \
+        (("image_rgba8",) if world > 1 and sink is None else ())
     vb = ViewBatchRenderer(rend, ds, cams, settings, want=want, streams=args.streams,
                            rgba_out=sink.slots if sink is not None else None)
     # size every workspace's pair lists from a checked frame of every view
-    for r in vb.pool:
-        for c, fr in zip(vb.cams, vb.frames):
+    for i, r in enumerate(vb.pool):   # (each lane renders views i, i + lanes, ...)
+        for c, fr in list(zip(vb.cams, vb.frames))[i::len(vb.pool)]:
             r.render(ds, c, settings, frame=fr, check=True)
     graphed = False if args.no_graph else vb.capture()
     stream = torch.cuda.current_stream(dev)
@@ -433,7 +455,7 @@ def run_gpu(args, rank, world, local_rank):
 
     # ---- end-to-end through the C ABI with host buffers (ges_render_views_host)
     e2e = e2e_u8 = None
-    if not args.no_e2e and len({(c.width, c.height) for c in cams}) == 1:
+    if not args.no_e2e and cfg != 5 and len({(c.width, c.height) for c in cams}) == 1:
         W, H = cams[0].width, cams[0].height
         cams_c = (_lib.Camera * per_rank)(*[camera_struct(c) for c in cams])
         cam_pin = torch.empty(C.sizeof(cams_c), dtype=torch.uint8, pin_memory=True)
@@ -543,7 +565,8 @@ def run_gpu(args, rank, world, local_rank):
                          "frac": ach / issue_peak, "source": "profiles/" + os.path.basename(tp)}
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if cfg == 5 and not args.views else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {**base_config(cfg, per_rank, world, args.ss),
                    **({} if gather_used != "nccl" or args.gather == "nccl" else
@@ -560,7 +583,8 @@ def run_gpu(args, rank, world, local_rank):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                      "phase_ms": phase, "dominant": max(phase, key=phase.get)},
         "cpu_baseline": cpu,
-        "e2e": e2e,
+        "e2e": e2e if cfg != 5 else {"value": None, "note": "config 5 (256 x 4K RGBA8 = 8.5 GB per step) "
+                                     "is measured device-side only; e2e is config 2's"},
         "e2e_rgba8": e2e_u8,
         "gpu_launches": frames * (5 if ds.n_gaussians else 4),
         "clocks": clk.summary(),
@@ -589,6 +613,9 @@ def main():
         torch.cuda.set_device(local_rank)
         backend = os.environ.get("GES_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator lines (nRanks, NVLS/P2P transport) on stderr for the run's log
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)

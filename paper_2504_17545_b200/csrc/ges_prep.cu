@@ -92,10 +92,18 @@ __device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1,
         lo[ax] = clo - pad;
         hi[ax] = chi + pad;
     }
-    x0 = clampi(ceilf(lo[0] - 0.5f - 0.5f), c.W);
-    x1 = clampi(floorf(hi[0] + 0.5f - 0.5f), c.W);
-    y0 = clampi(ceilf(lo[1] - 0.5f - 0.5f), c.H);
-    y1 = clampi(floorf(hi[1] + 0.5f - 0.5f), c.H);
+    const float fx0 = ceilf(lo[0] - 0.5f - 0.5f), fx1 = floorf(hi[0] + 0.5f - 0.5f);
+    const float fy0 = ceilf(lo[1] - 0.5f - 0.5f), fy1 = floorf(hi[1] + 0.5f - 0.5f);
+    // A disc whose padded box lies entirely beyond an image edge covers no
+    // pixel.  The reference's clamp turns its range into the edge row/column
+    // (forward.py:85-96), so every off-screen disc is a candidate of the
+    // edge tiles there and is rejected pixel by pixel; dropping it here gives
+    // the same pixels and keeps the edge tiles' lists short.
+    if (fx0 > c.W - 1.f || fx1 < 0.f || fy0 > c.H - 1.f || fy1 < 0.f) return false;
+    x0 = clampi(fx0, c.W);
+    x1 = clampi(fx1, c.W);
+    y0 = clampi(fy0, c.H);
+    y1 = clampi(fy1, c.H);
     return x1 >= x0 && y1 >= y0;
 }
 
@@ -335,11 +343,16 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_
             if (v > n - 1.0) return n - 1;
             return (int)v;
         };
-        x0 = clampi(ceil(mx - rx - 0.5 - 0.5), cam.W);
-        x1 = clampi(floor(mx + rx + 0.5 - 0.5), cam.W);
-        y0 = clampi(ceil(my - ry - 0.5 - 0.5), cam.H);
-        y1 = clampi(floor(my + ry + 0.5 - 0.5), cam.H);
-        valid = x1 >= x0 && y1 >= y0;
+        const double fx0 = ceil(mx - rx - 0.5 - 0.5), fx1 = floor(mx + rx + 0.5 - 0.5);
+        const double fy0 = ceil(my - ry - 0.5 - 0.5), fy1 = floor(my + ry + 0.5 - 0.5);
+        // off-screen support box: no pixel of the image reaches alpha >= 1/255
+        // (the reference clamps it onto the edge tiles and rejects it per pixel)
+        valid = !(fx0 > cam.W - 1.0 || fx1 < 0.0 || fy0 > cam.H - 1.0 || fy1 < 0.0);
+        x0 = clampi(fx0, cam.W);
+        x1 = clampi(fx1, cam.W);
+        y0 = clampi(fy0, cam.H);
+        y1 = clampi(fy1, cam.H);
+        valid = valid && x1 >= x0 && y1 >= y0;
     }
     __shared__ float shw[(GPREP_T / 32) * sh_warp_floats<DEG>()];
     const float3 col = gauss_view_colour<DEG>(sc, cam, p, shw);

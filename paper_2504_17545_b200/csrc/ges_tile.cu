@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders
 #ifdef GES_TIMING   // warp lifetimes (tuning builds only, see read_stats / tools/tile_stats.py --timing)
     const long long t_start = clock64();
-    unsigned tm_len = 0, tm_b1 = 0, tm_t1 = 0;
+    unsigned tm_len = 0, tm_b1 = 0, tm_t1 = 0, tm_b2 = 0, tm_t2 = 0;
+    long long t_p1 = 0, t_p2 = 0;
 #define GES_TM(x) (x)
 #else
 #define GES_TM(x) ((void)0)
@@ -536,6 +537,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             if (inside_px(p) && a.ds_in) ds[p] = a.ds_in[pix_of(p)];
     }
 
+    GES_TM(t_p1 = clock64());
     // ------------------------------------------------------------ pass 2
     float wsum[NP], cr[NP], cg[NP], cb[NP], dsum[NP], nx[NP], ny[NP], nz[NP];
 #pragma unroll
@@ -631,6 +633,8 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 sm.st[3][slot] = make_float4(v[12], v[13], v[14], v[15]);
             }
             uint32_t vote = __ballot_sync(0xffffffffu, live);
+            GES_TM(++tm_b2);
+            GES_TM(tm_t2 += __popc(vote));
             if (lane == 0) { GES_STAT(6, min(32u, gend - base)); GES_STAT(7, __popc(vote)); }
             __syncwarp();
             while (vote) {
@@ -702,6 +706,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
         }
     }
 
+    GES_TM(t_p2 = clock64());
     // ------------------------------------------------------------ resolve + write
     float3 cs[NP];
 #pragma unroll
@@ -807,6 +812,10 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             atomicAdd(&g_stats[12], (unsigned long long)tm_len);
             atomicAdd(&g_stats[13], (unsigned long long)tm_b1);
             atomicAdd(&g_stats[14], (unsigned long long)tm_t1);
+            atomicAdd(&g_stats[5], (unsigned long long)(t_p1 - t_start));
+            atomicAdd(&g_stats[6], (unsigned long long)(t_p2 - t_p1));
+            atomicAdd(&g_stats[7], (unsigned long long)tm_b2);
+            atomicAdd(&g_stats[8], (unsigned long long)tm_t2);
         }
     }
 #endif

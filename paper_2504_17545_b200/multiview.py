@@ -35,8 +35,10 @@ def shard(n_views: int, rank: int, world: int) -> range:
 def gather_frames(local: torch.Tensor, dst: int = 0, group=None):
     """Gather equally-shaped per-rank frame batches (V, H, W, C) to ``dst``.
     Returns the (world*V, H, W, C) batch on ``dst`` and None elsewhere."""
-    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+    if not dist.is_initialized():
         return local
+    if dist.get_world_size(group) == 1 and dist.get_backend(group) != "nccl":
+        return local   # (a one-rank NCCL communicator still runs the collective)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     if local.is_cuda and dist.get_backend(group) != "nccl":   # gloo gathers host tensors only
@@ -114,14 +116,14 @@ class PeerFrameGather:
         self.slots = [DevicePointer(base + first + k * self.frame_bytes, self.frame_bytes) for k in range(V)]
         self.frames = (torch.as_tensor(_CudaArray(base, (self.world * V, height, width, 4)), device=self.device)
                        if self.rank == dst else None)
-        self._flag = torch.zeros(1, device=self.device) if self.world > 1 else None
+        self._flag = torch.zeros(1, device=self.device) if dist.is_initialized() else None
 
     def fence(self):
         """Order every rank's frame writes of this step before the
         destination's later work: one stream-ordered one-word all-reduce with
         NCCL (a rank's all-reduce starts only after its render kernels have
         finished); host synchronisation + barrier with other backends."""
-        if self.world == 1:
+        if not dist.is_initialized():
             return
         if dist.get_backend(self.group) == "nccl":
             dist.all_reduce(self._flag, group=self.group)

@@ -81,7 +81,7 @@ def test_in_place_edit_is_seen_without_invalidate():
                                 sc.gaussians.filter3d.copy()), sc.sh_degree, Stage.FROZEN)
     c = G.render(fresh, cam)
     np.testing.assert_array_equal(b.surfels.winner, c.surfels.winner)
-    np.testing.assert_array_equal(b.image, c.image)
+    assert float(np.max(np.abs(b.image - c.image))) <= 1e-5   # fp32 sums in atomic list order
 
 
 def test_single_element_edit_full_verify_and_invalidate():

@@ -70,3 +70,52 @@ def test_peer_gather_matches_local_render(tmp_path):
     assert got.shape == ref.shape == (4, 48, 64, 4)
     assert np.abs(got - ref).max() <= 1
     assert (got[..., 3] == 255).all()
+
+
+def _nccl_worker(rank, world, port, out_path):
+    import paper_2504_17545_b200 as G
+    from paper_2504_17545_b200 import scenes as S
+    from paper_2504_17545_b200.multiview import PeerFrameGather, ViewBatchRenderer, gather_frames
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NCCL_DEBUG="INFO",
+                      NCCL_DEBUG_SUBSYS="INIT")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    try:
+        scene = S.random_scene(np.random.default_rng(6), 120, 60, degree=2)
+        cams = S.orbit_views(3, 64, 48)
+        ds = G.DeviceScene(scene)
+        settings = G.RenderSettings()
+        # peer-memory form: IPC buffer, tile kernel writes into it, NCCL fence
+        sink = PeerFrameGather(3, 48, 64, dst=0)
+        vb = ViewBatchRenderer(G.Renderer(), ds, cams, settings, want=("image_rgba8",), rgba_out=sink.slots)
+        vb.render(check=True)
+        sink.fence()
+        peer = sink.frames.cpu().numpy().copy()
+        # NCCL gather form (the bench's fallback)
+        vb2 = ViewBatchRenderer(G.Renderer(), ds, cams, settings, want=("image_rgba8",))
+        vb2.render(check=True)
+        got = gather_frames(vb2.rgba, dst=0)
+        torch.cuda.synchronize()
+        np.savez(out_path, peer=peer, gathered=got.cpu().numpy(), local=vb2.rgba.cpu().numpy(),
+                 backend=dist.get_backend(), world=dist.get_world_size())
+        sink.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_one_rank_fence_and_gather(tmp_path, capfd):
+    """The NCCL code paths of the multi-GPU bench on the one GPU this box has:
+    process-group init with device_id, the peer buffer's NCCL fence
+    (all-reduce) and the NCCL frame gather, in a one-rank communicator (the
+    collectives run; a one-GPU box cannot run two NCCL ranks)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = str(tmp_path / "nccl.npz")
+    mp.start_processes(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True, start_method="spawn")
+    z = np.load(out)
+    assert str(z["backend"]) == "nccl" and int(z["world"]) == 1
+    assert z["gathered"].shape == z["local"].shape == z["peer"].shape == (3, 48, 64, 4)
+    assert np.array_equal(z["gathered"], z["local"])
+    assert np.abs(z["peer"].astype(int) - z["local"].astype(int)).max() <= 1
+    err = capfd.readouterr().err
+    assert "NCCL INFO" in err and "nRanks 1" in err, err[-2000:]

@@ -44,11 +44,14 @@ if a.timing:
     nw = ((cam.width + 31) // 32) * ((cam.height + 31) // 32) * 8
     ntx = (cam.width + 31) // 32
     k = buf[18]
+    t = (k >> 3) % (1 << 21)
     print(f"warps {nw}: mean lifetime {buf[16] / nw:.0f} cycles, max {buf[17]} "
-          f"(tile ({(k >> 3) % (1 << 21) % ntx}, {(k >> 3) % (1 << 21) // ntx}), warp {k & 7})")
+          f"(tile ({t % ntx}, {t // ntx}), warp {k & 7})")
     n = max(buf[19], 1)
     print(f"warps over 50 us: {buf[19]}; their mean list length {buf[12] / n:.0f}, "
-          f"chunks walked {buf[13] / n:.1f}, warp tests {buf[14] / n:.1f}")
+          f"chunks walked {buf[13] / n:.1f}, warp tests {buf[14] / n:.1f}; "
+          f"cycles: pass 1 {buf[5] / n:.0f}, pass 2 {buf[6] / n:.0f} "
+          f"(Gaussian chunks {buf[7] / n:.1f}, warp tests {buf[8] / n:.1f})")
 else:
     for n, v in zip(NAMES, buf):
         print(f"{n:28s} {v:14d}")
