@@ -72,12 +72,12 @@ def test_peer_gather_matches_local_render(tmp_path):
     assert (got[..., 3] == 255).all()
 
 
-def _nccl_worker(rank, world, port, out_path):
+def _nccl_worker(rank, world, port, out_path, log_path):
     import paper_2504_17545_b200 as G
     from paper_2504_17545_b200 import scenes as S
     from paper_2504_17545_b200.multiview import PeerFrameGather, ViewBatchRenderer, gather_frames
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NCCL_DEBUG="INFO",
-                      NCCL_DEBUG_SUBSYS="INIT")
+                      NCCL_DEBUG_SUBSYS="INIT", NCCL_DEBUG_FILE=log_path)
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
     try:
@@ -103,7 +103,7 @@ def _nccl_worker(rank, world, port, out_path):
         dist.destroy_process_group()
 
 
-def test_nccl_one_rank_fence_and_gather(tmp_path, capfd):
+def test_nccl_one_rank_fence_and_gather(tmp_path):
     """The NCCL code paths of the multi-GPU bench on the one GPU this box has:
     process-group init with device_id, the peer buffer's NCCL fence
     (all-reduce) and the NCCL frame gather, in a one-rank communicator (the
@@ -111,11 +111,12 @@ def test_nccl_one_rank_fence_and_gather(tmp_path, capfd):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     out = str(tmp_path / "nccl.npz")
-    mp.start_processes(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True, start_method="spawn")
+    log = str(tmp_path / "nccl.log")
+    mp.start_processes(_nccl_worker, args=(1, _free_port(), out, log), nprocs=1, join=True, start_method="spawn")
     z = np.load(out)
     assert str(z["backend"]) == "nccl" and int(z["world"]) == 1
     assert z["gathered"].shape == z["local"].shape == z["peer"].shape == (3, 48, 64, 4)
     assert np.array_equal(z["gathered"], z["local"])
     assert np.abs(z["peer"].astype(int) - z["local"].astype(int)).max() <= 1
-    err = capfd.readouterr().err
-    assert "NCCL INFO" in err and "nRanks 1" in err, err[-2000:]
+    text = open(log).read() if os.path.exists(log) else ""
+    assert "NCCL INFO" in text and "nRanks 1" in text, text[-2000:]
