@@ -27,6 +27,41 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 inline size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
+// Side lane of a caller stream: the Gaussian preprocess runs on it, forked
+// from and joined back into the caller's stream with two events, so it
+// overlaps the surfel preprocess of the same frame (both read only the
+// scene and write disjoint records/counters).  One side stream per (caller
+// stream, device), created on first use and kept for the thread's lifetime;
+// works under stream capture (the fork/join become graph edges).
+struct SideLane {
+    cudaStream_t caller, side;
+    cudaEvent_t fork, join;
+    int device;
+};
+
+SideLane* side_lane(cudaStream_t s) {
+    static thread_local SideLane lanes[64];
+    static thread_local int n = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    for (int i = 0; i < n; ++i)
+        if (lanes[i].caller == s && lanes[i].device == dev) return &lanes[i];
+    if (n == 64) return nullptr;   // (more caller streams than lanes: run sequentially)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return nullptr;            // (lanes are made outside capture: the first call of a stream is eager)
+    SideLane& l = lanes[n];
+    if (cudaStreamCreateWithFlags(&l.side, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaEventCreateWithFlags(&l.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&l.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    l.caller = s;
+    l.device = dev;
+    return &lanes[n++];
+}
+
 struct Carve {
     char* base;
     size_t off = 0;
@@ -185,10 +220,23 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, tp * grid,
                      log2i(tp * grid), do_s ? f.order : nullptr, f.tot};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, tp, log2i(tp)};
+    // both preprocesses of a full frame run concurrently: Gaussians on the side lane
+    SideLane* lane = (do_s && do_g && scs.n_surfels && scs.n_gaussians) ? side_lane(s) : nullptr;
+    cudaStream_t gs_stream = s;
+    if (lane) {
+        if ((e = cudaEventRecord(lane->fork, s)) != cudaSuccess || (e = cudaStreamWaitEvent(lane->side, lane->fork, 0)))
+            return cuda_fail(e, "preprocess fork");
+        gs_stream = lane->side;
+    }
     if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, f.cnt_s, nullptr, f.scull}, s)))
         return cuda_fail(e, "surfel preprocess");
-    if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, f.g_nrm, f.cnt_g, nullptr, f.gcull}, s)))
+    if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, f.g_nrm, f.cnt_g, nullptr, f.gcull},
+                                       gs_stream)))
         return cuda_fail(e, "gaussian preprocess");
+    if (lane) {
+        if ((e = cudaEventRecord(lane->join, lane->side)) != cudaSuccess || (e = cudaStreamWaitEvent(s, lane->join, 0)))
+            return cuda_fail(e, "preprocess join");
+    }
     mark(2);
     if ((e = launch_scan(bs, bg, status, s)))
         return cuda_fail(e, "tile scan");

@@ -35,14 +35,16 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
     uint32_t tot = 0;
     if (t < n) {
         uint4* c = reinterpret_cast<uint4*>(p.cnt + (size_t)t * NSLAB);
+        uint4 v[NSLAB / 4];
+#pragma unroll
+        for (int q = 0; q < NSLAB / 4; ++q) v[q] = __ldcg(c + q);   // all loads in flight at once
 #pragma unroll
         for (int q = 0; q < NSLAB / 4; ++q) {
-            uint4 v = c[q];
             uint4 o;
-            o.x = tot; tot += v.x;
-            o.y = tot; tot += v.y;
-            o.z = tot; tot += v.z;
-            o.w = tot; tot += v.w;
+            o.x = tot; tot += v[q].x;
+            o.y = tot; tot += v[q].y;
+            o.z = tot; tot += v[q].z;
+            o.w = tot; tot += v[q].w;
             c[q] = o;
         }
     }
