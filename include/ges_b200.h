@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GES_ABI_VERSION 1
+#define GES_ABI_VERSION 2
 
 #define GES_OK 0
 #define GES_EINVAL 1
@@ -45,16 +45,16 @@ typedef struct ges_camera {
     double w2c[12];
 } ges_camera_t;
 
-/* RenderSettings, forward.py:36-58 (dtype is always float32 on device,
- * threads is meaningless on the GPU). */
+/* RenderSettings, forward.py:36-58 (dtype selects ges_render or
+ * ges_render_f64; threads is meaningless on the GPU). */
 typedef struct ges_settings {
     int32_t supersample;      /* 1 or 4 */
     int32_t layers;           /* GES_LAYERS_* */
     int32_t mip;              /* 0/1 */
     int32_t epsilon_mode;     /* 0 adaptive, 1 constant (forward.py:212-215) */
-    float epsilon_value;
     int32_t with_geometry;    /* 0/1 */
-    float background[3];
+    double epsilon_value;     /* (float64 like the reference; the float32 kernels round it) */
+    double background[3];
     int32_t tile_mode;        /* 0 auto; 1: 16x16-pixel tiles; 2: 32x32-pixel tiles,
                                  2x2 pixels per thread (ss=1 without geometry) */
 } ges_settings_t;
@@ -171,6 +171,43 @@ int ges_composite(const float *surfel_color, const float *g_color, const float *
 int ges_smooth_geometry(const float *s_depth, const float *s_normal, const float *g_depth,
                         const float *g_normal, const float *g_weight, float *depth_out,
                         float *normal_out, int64_t n, void *stream);
+
+/* ------------------------------------------------------------------ float64
+ * RenderSettings.dtype = float64 (forward.py:44; the reference's own tests
+ * render in float64, pkg/tests/test_forward.py:33-35).  The frame is binned
+ * exactly like ges_render (float32 records, conservative ranges and depth
+ * keys, 16x16 tiles) and the per-pixel passes then run in float64 on the
+ * SOURCE arrays `src` the scene was packed from: forward.py:127-209
+ * (surfel z-buffer, lowest source id on ties), :248-381 (depth-gated
+ * Gaussian sums) and :384-417 (composite, layers), with the reference's
+ * formulas.  Outputs are float64 (winner int32); any may be NULL. */
+typedef struct ges_outputs_f64 {
+    double *image;
+    double *s_color, *s_depth, *s_normal;
+    int32_t *s_winner;
+    double *g_color, *g_weight, *g_depth, *g_normal;
+} ges_outputs_f64_t;
+
+/* Workspace of ges_render_f64 (the float32 binning plus the float64
+ * per-primitive records). */
+size_t ges_workspace_bytes_f64(const ges_scene_t *scene, const ges_camera_t *cam,
+                               const ges_settings_t *st, int64_t surfel_pair_cap,
+                               int64_t gaussian_pair_cap);
+
+/* mode 3: render (forward.py:403-417); 1: rasterize_surfels (:127-209);
+ * 2: accumulate_gaussians (:218-245) against surfel_depth (H,W) float64. */
+int ges_render_f64(const ges_scene_t *scene, const ges_scene_src_t *src, const ges_camera_t *cam,
+                   const ges_settings_t *st, int32_t mode, const double *surfel_depth,
+                   const ges_outputs_f64_t *out, void *workspace, size_t ws_bytes,
+                   int64_t surfel_pair_cap, int64_t gaussian_pair_cap,
+                   ges_frame_status_t *status_dev, void *stream);
+
+/* float64 composite / smooth_geometry (forward.py:384-400). */
+int ges_composite_f64(const double *surfel_color, const double *g_color, const double *g_weight,
+                      double surfel_weight, double *image, int64_t n, void *stream);
+int ges_smooth_geometry_f64(const double *s_depth, const double *s_normal, const double *g_depth,
+                            const double *g_normal, const double *g_weight, double *depth_out,
+                            double *normal_out, int64_t n, void *stream);
 
 #define GES_IMAGE_F32_RGB 0   /* (H,W,3) float32: RenderResult.image */
 #define GES_IMAGE_RGBA8 1     /* (H,W,4) uint8: the saved frame, datasets.py:54-56 */

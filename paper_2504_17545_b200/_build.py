@@ -7,7 +7,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ("ges_abi.cu", "ges_prep.cu", "ges_bin.cu", "ges_tile.cu", "ges_train.cu")
+SOURCES = ("ges_abi.cu", "ges_prep.cu", "ges_bin.cu", "ges_tile.cu", "ges_train.cu", "ges_f64.cu")
 OUT = os.path.join(HERE, "libges_b200.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]

@@ -14,6 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # GES_B200_LIB overrides the library path (A/B runs of alternative builds)
 LIB_PATH = os.environ.get("GES_B200_LIB") or os.path.join(HERE, "libges_b200.so")
 
+ABI_VERSION = 2   # include/ges_b200.h GES_ABI_VERSION
 GES_OK, GES_EINVAL, GES_EDEGREE, GES_EWORKSPACE, GES_ECUDA = 0, 1, 2, 3, 4
 GES_IMAGE_F32_RGB, GES_IMAGE_RGBA8 = 0, 1
 LAYERS = {"full": 0, "surfels_only": 1, "gaussians_only": 2}
@@ -25,7 +26,8 @@ EXPORTS = ("ges_abi_version", "ges_last_error", "ges_scene_bytes", "ges_scene_pa
            "ges_render_views_host", "ges_debug_stats", "ges_surfel_colors",
            "ges_backward_scratch_bytes", "ges_backward_workspace_bytes", "ges_backward_gaussians",
            "ges_backward_surfels_frozen", "ges_gaussian_contributions",
-           "ges_frozen_surfel_buffers", "ges_peer_alloc", "ges_peer_free", "ges_peer_open", "ges_peer_close")
+           "ges_frozen_surfel_buffers", "ges_peer_alloc", "ges_peer_free", "ges_peer_open", "ges_peer_close",
+           "ges_workspace_bytes_f64", "ges_render_f64", "ges_composite_f64", "ges_smooth_geometry_f64")
 
 
 class Camera(C.Structure):
@@ -35,8 +37,8 @@ class Camera(C.Structure):
 
 class Settings(C.Structure):
     _fields_ = [("supersample", C.c_int32), ("layers", C.c_int32), ("mip", C.c_int32),
-                ("epsilon_mode", C.c_int32), ("epsilon_value", C.c_float),
-                ("with_geometry", C.c_int32), ("background", C.c_float * 3), ("tile_mode", C.c_int32)]
+                ("epsilon_mode", C.c_int32), ("with_geometry", C.c_int32), ("epsilon_value", C.c_double),
+                ("background", C.c_double * 3), ("tile_mode", C.c_int32)]
 
 
 class SceneSrc(C.Structure):
@@ -58,6 +60,11 @@ class Outputs(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("image", "s_color", "s_depth", "s_normal", "s_winner",
                                           "g_color", "g_weight", "g_depth", "g_normal",
                                           "image_rgba8")]
+
+
+class OutputsF64(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("image", "s_color", "s_depth", "s_normal", "s_winner",
+                                          "g_color", "g_weight", "g_depth", "g_normal")]
 
 
 class FrameStatus(C.Structure):
@@ -120,11 +127,18 @@ def lib():
     sig["ges_frozen_surfel_buffers"] = (C.c_int, [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p] * 6)
     sig["ges_gaussian_contributions"] = (C.c_int, [P(Scene), P(SceneSrc), P(Camera), P(Settings)] + [C.c_void_p] * 4
                                          + [C.c_size_t, C.c_int64, C.c_void_p, C.c_void_p])
+    sig["ges_workspace_bytes_f64"] = (C.c_size_t, [P(Scene), P(Camera), P(Settings), C.c_int64, C.c_int64])
+    sig["ges_render_f64"] = (C.c_int, [P(Scene), P(SceneSrc), P(Camera), P(Settings), C.c_int32, C.c_void_p,
+                                       P(OutputsF64), C.c_void_p, C.c_size_t, C.c_int64, C.c_int64, C.c_void_p,
+                                       C.c_void_p])
+    sig["ges_composite_f64"] = (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                          C.c_int64, C.c_void_p])
+    sig["ges_smooth_geometry_f64"] = (C.c_int, [C.c_void_p] * 7 + [C.c_int64, C.c_void_p])
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
-    if L.ges_abi_version() != 1:
+    if L.ges_abi_version() != ABI_VERSION:
         raise ImportError("libges_b200.so ABI version mismatch")
     _lib = L
     return L

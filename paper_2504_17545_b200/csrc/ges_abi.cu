@@ -111,6 +111,7 @@ struct Frame {
     size_t zero_bytes;   // counters + tickets, cleared by one memset per frame
     uint32_t *list_s, *list_g;
     uint32_t *order, *tot;
+    void* rec64;         // float64 mode: per-primitive float64 records
     ges_frame_status_t* status;
     size_t bytes;
     int ntx, nty, ntiles, px;
@@ -125,7 +126,7 @@ int tile_px_of(const ges_camera_t* cam, const ges_settings_t* st) {
 }
 
 Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st, int64_t cap_s,
-             int64_t cap_g) {
+             int64_t cap_g, bool f64 = false) {
     Frame f{};
     Carve c{static_cast<char*>(base)};
     f.px = tile_px_of(cam, st);
@@ -154,6 +155,7 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, const g
     f.g_nrm = c.take<float4>(ng);
     f.list_s = c.take<uint32_t>((size_t)cap_s);
     f.list_g = c.take<uint32_t>((size_t)cap_g);
+    f.rec64 = f64 ? c.take<char>(f64_record_bytes((int64_t)ns, (int64_t)ng, sc->gaussian_dim)) : nullptr;
     f.bytes = c.off;
     return f;
 }
@@ -185,16 +187,32 @@ SlabMap slab_map(const ges_scene_t& sc, const CamK& c) {
     return m;
 }
 
+// Float64 mode of a frame (ges_render_f64): the source arrays, the float64
+// outputs and the external float64 surfel depth of the pass-2-only entry.
+struct F64Ctx {
+    const ges_scene_src_t* src;
+    const ges_outputs_f64_t* out;
+    const double* ds_in;
+};
+
 // mode: 1 surfel pass, 2 Gaussian pass against ds_in, 3 both.
-int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st, const ges_outputs_t* out,
+int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st_in, const ges_outputs_t* out,
               const float* ds_in, int mode, void* ws, size_t ws_bytes, int64_t cap_s, int64_t cap_g,
-              ges_frame_status_t* status_dev, cudaStream_t s, void* const* ev = nullptr) {
+              ges_frame_status_t* status_dev, cudaStream_t s, void* const* ev = nullptr,
+              const F64Ctx* f64 = nullptr) {
     int rc;
-    if ((rc = check_scene(sc)) || (rc = check_cam(cam)) || (rc = check_settings(st))) return rc;
-    if (!out) return fail(GES_EINVAL, "outputs is NULL");
+    if ((rc = check_scene(sc)) || (rc = check_cam(cam)) || (rc = check_settings(st_in))) return rc;
+    if (!out && !f64) return fail(GES_EINVAL, "outputs is NULL");
     if (cap_s < 0 || cap_g < 0 || cap_s >= (1ll << 32) || cap_g >= (1ll << 32))
         return fail(GES_EINVAL, "pair capacity out of range");
-    Frame f = layout(ws, sc, cam, st, cap_s, cap_g);
+    ges_settings_t st64;
+    const ges_settings_t* st = st_in;
+    if (f64) {   // the float64 tile kernel works on 16x16 tiles, one thread per base pixel
+        st64 = *st_in;
+        st64.tile_mode = 1;
+        st = &st64;
+    }
+    Frame f = layout(ws, sc, cam, st, cap_s, cap_g, f64 != nullptr);
     if (!ws || ws_bytes < f.bytes) return fail(GES_EWORKSPACE, "workspace too small (see ges_workspace_bytes)");
     ges_frame_status_t* status = status_dev ? status_dev : f.status;
     const int grid = st->supersample == 4 ? 2 : 1;
@@ -244,10 +262,32 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     if ((e = launch_fill(f.scull, scs.n_surfels, bs, f.gcull, scs.n_gaussians, sc->gaussian_dim, bg, slabs, s)))
         return cuda_fail(e, "tile fill");
     mark(4);
+    if (f64) {
+        F64Launch L{};
+        L.src = *f64->src;
+        L.s_id = sc->s_id;
+        L.ns = do_s ? sc->n_surfels : 0;
+        L.ng = do_g ? sc->n_gaussians : 0;
+        L.gdim = sc->gaussian_dim; L.deg = sc->sh_degree;
+        L.mode = (do_s ? 1 : 0) | ((mode & 2) ? 2 : 0);
+        L.layers = st->layers; L.geom = st->with_geometry; L.mip = st->mip;
+        L.eps_const = st->epsilon_mode; L.eps_value = (double)st->epsilon_value;
+        for (int i = 0; i < 3; ++i) L.bg[i] = (double)st->background[i];
+        L.W = cam->width; L.H = cam->height; L.ntx = f.ntx; L.ntiles = f.ntiles; L.grid = grid;
+        L.cs = cs; L.cg = cg;
+        L.scull = f.scull; L.s_list = f.list_s; L.g_list = f.list_g; L.sbin = bs; L.gbin = bg;
+        L.ds_in = f64->ds_in;
+        L.out = *f64->out;
+        L.records = f.rec64;
+        L.status = status;
+        if ((e = launch_f64(L, s))) return cuda_fail(e, "float64 tile kernel");
+        mark(5);
+        return GES_OK;
+    }
     TileArgs a{};
     a.W = cam->width; a.H = cam->height; a.ntx = f.ntx; a.nty = f.nty;
     a.layers = st->layers;
-    for (int i = 0; i < 3; ++i) a.bg[i] = st->background[i];
+    for (int i = 0; i < 3; ++i) a.bg[i] = (float)st->background[i];
     a.rcx = (float)cs.cx; a.rcy = (float)cs.cy; a.rifx = (float)(1.0 / cs.fx); a.rify = (float)(1.0 / cs.fy);
     a.srec = f.srec; a.scull = f.scull; a.s_list = f.list_s; a.sbin = bs;
     a.order = bs.order;
@@ -366,6 +406,52 @@ int ges_accumulate_gaussians(const ges_scene_t* sc, const ges_camera_t* cam, con
     if (st && s2.layers == GES_LAYERS_SURFELS_ONLY) s2.layers = GES_LAYERS_FULL;
     return run_frame(sc, cam, st ? &s2 : nullptr, out, surfel_depth, 2, ws, ws_bytes, 0, cap_g, status_dev,
                      (cudaStream_t)stream);
+}
+
+size_t ges_workspace_bytes_f64(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings_t* st,
+                               int64_t cap_s, int64_t cap_g) {
+    if (check_scene(sc) || check_cam(cam) || check_settings(st) || cap_s < 0 || cap_g < 0) return 0;
+    ges_settings_t s2 = *st;
+    s2.tile_mode = 1;
+    return layout(nullptr, sc, cam, &s2, cap_s, cap_g, true).bytes;
+}
+
+int ges_render_f64(const ges_scene_t* sc, const ges_scene_src_t* src, const ges_camera_t* cam,
+                   const ges_settings_t* st, int32_t mode, const double* surfel_depth,
+                   const ges_outputs_f64_t* out, void* ws, size_t ws_bytes, int64_t cap_s, int64_t cap_g,
+                   ges_frame_status_t* status_dev, void* stream) {
+    if (!src) return fail(GES_EINVAL, "float64 render needs the source scene");
+    if (!out) return fail(GES_EINVAL, "outputs is NULL");
+    if (mode < 1 || mode > 3) return fail(GES_EINVAL, "mode must be 1, 2 or 3");
+    if (mode == 2 && !surfel_depth) return fail(GES_EINVAL, "mode 2 needs the surfel depth");
+    if (sc && (src->n_surfels != sc->n_surfels || src->n_gaussians != sc->n_gaussians ||
+               src->sh_degree != sc->sh_degree || src->gaussian_dim != sc->gaussian_dim))
+        return fail(GES_EINVAL, "source scene does not match the packed scene");
+    if (sc && ((sc->n_surfels && (!src->s_pos || !src->s_quat || !src->s_log_scale || !src->s_sh)) ||
+               (sc->n_gaussians && (!src->g_pos || !src->g_raw_opacity || !src->g_quat || !src->g_log_scale ||
+                                    !src->g_sh))))
+        return fail(GES_EINVAL, "source scene arrays missing");
+    F64Ctx ctx{src, out, surfel_depth};
+    ges_settings_t s2 = st ? *st : ges_settings_t{};
+    // accumulate_gaussians ignores `layers` (forward.py:218-245): mode 2 always accumulates
+    if (mode == 2 && st && st->layers == GES_LAYERS_SURFELS_ONLY) s2.layers = GES_LAYERS_FULL;
+    return run_frame(sc, cam, st ? &s2 : nullptr, nullptr, nullptr, mode, ws, ws_bytes, mode & 1 ? cap_s : 0,
+                     mode & 2 ? cap_g : 0, status_dev, (cudaStream_t)stream, nullptr, &ctx);
+}
+
+int ges_composite_f64(const double* sc, const double* gc, const double* gw, double sw, double* img, int64_t n,
+                      void* stream) {
+    if (n < 0 || (n && (!sc || !gc || !gw || !img))) return fail(GES_EINVAL, "bad composite arguments");
+    cudaError_t e = launch_composite64(sc, gc, gw, sw, img, n, (cudaStream_t)stream);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "composite");
+}
+
+int ges_smooth_geometry_f64(const double* sd, const double* sn, const double* gd, const double* gn, const double* gw,
+                            double* d_out, double* n_out, int64_t n, void* stream) {
+    if (n < 0 || (n && (!sd || !sn || !gd || !gn || !gw || !d_out || !n_out)))
+        return fail(GES_EINVAL, "bad smooth_geometry arguments");
+    cudaError_t e = launch_smooth64(sd, sn, gd, gn, gw, d_out, n_out, n, (cudaStream_t)stream);
+    return e == cudaSuccess ? GES_OK : cuda_fail(e, "smooth_geometry");
 }
 
 int ges_composite(const float* sc, const float* gc, const float* gw, float sw, float* img, int64_t n, void* stream) {

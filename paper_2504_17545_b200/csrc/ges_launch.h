@@ -74,6 +74,31 @@ cudaError_t launch_composite(const float* sc, const float* gc, const float* gw, 
 cudaError_t launch_smooth(const float* sd, const float* sn, const float* gd, const float* gn,
                           const float* gw, float* d_out, float* n_out, int64_t n, cudaStream_t s);
 
+// ---------------------------------------------------------------- float64 mode (ges_f64.cu)
+struct F64Launch {
+    ges_scene_src_t src;
+    const int32_t* s_id;          // packed -> source surfel
+    int64_t ns, ng;
+    int gdim, deg, mode, layers, geom, mip, eps_const;
+    double eps_value;
+    double bg[3];
+    int W, H, ntx, ntiles, grid;
+    CamK cs, cg;
+    const float4* scull;
+    const uint32_t *s_list, *g_list;
+    BinPass sbin, gbin;
+    const double* ds_in;
+    ges_outputs_f64_t out;
+    void* records;                // f64_record_bytes(ns, ng, gdim)
+    const ges_frame_status_t* status;
+};
+size_t f64_record_bytes(int64_t ns, int64_t ng, int gdim);
+cudaError_t launch_f64(const F64Launch& L, cudaStream_t s);
+cudaError_t launch_composite64(const double* sc, const double* gc, const double* gw, double sw, double* img,
+                               int64_t n, cudaStream_t s);
+cudaError_t launch_smooth64(const double* sd, const double* sn, const double* gd, const double* gn, const double* gw,
+                            double* d_out, double* n_out, int64_t n, cudaStream_t s);
+
 // ---------------------------------------------------------------- training (ges_train.cu)
 struct BwdArgs {
     int W, H, ntx, nty;           // base resolution, 16x16 tiles

@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss2_prep(ges_
 cudaError_t launch_gauss_prep(const ges_scene_t& sc, const CamK& cam, const Grid& g,
                               const ges_settings_t& st, const PrepOut& o, cudaStream_t s) {
     if (sc.n_gaussians == 0) return cudaSuccess;
-    GaussCfg cfg{st.mip, st.epsilon_mode == 1, st.with_geometry, st.epsilon_value};
+    GaussCfg cfg{st.mip, st.epsilon_mode == 1, st.with_geometry, (float)st.epsilon_value};
     unsigned nb = (unsigned)((sc.n_gaussians + GPREP_T - 1) / GPREP_T);
 #define GES_G(KER)                                                              \
     switch (sc.sh_degree) {                                                     \

@@ -6,9 +6,10 @@ sm_100a kernels of ``libges_b200.so``.  By default results are NumPy arrays
 like the reference's (``to_numpy=True``); pass ``to_numpy=False`` to keep
 torch CUDA tensors.  Differences, all deliberate and documented in DESIGN.md:
 
-* ``settings.dtype`` must be ``np.float32``: the kernels compute per-pixel
-  math in float32 like the reference's default; ``np.float64`` raises
-  ``NotImplementedError``.
+* ``settings.dtype`` selects the kernels: ``np.float32`` (the reference's
+  default; the fused float32 tile kernel) or ``np.float64`` (the float64
+  per-pixel kernels of ``ges_render_f64``, outputs float64 like the
+  reference's); any other dtype raises ``NotImplementedError``.
 * ``settings.threads`` is accepted and ignored.
 * In supersample-4 mode depth/normal/winner are materialised arrays, not
   strided views of hi-res buffers (forward.py:205-207).
@@ -87,9 +88,20 @@ class RenderResult:
 
 def _check_settings(settings):
     settings = settings or RenderSettings()
-    if np.dtype(getattr(settings, "dtype", np.float32)) != np.float32:
-        raise NotImplementedError("the B200 kernels compute in float32; use RenderSettings(dtype=np.float32)")
+    if np.dtype(getattr(settings, "dtype", np.float32)) not in (np.float32, np.float64):
+        raise NotImplementedError("the B200 kernels compute in float32 or float64")
     return settings
+
+
+def _is_f64(settings) -> bool:
+    return np.dtype(getattr(settings, "dtype", np.float32)) == np.float64
+
+
+def _render_f64(scene, cam, settings, mode, surfel_depth=None):
+    from .renderer import render_f64
+    dev = _device()
+    ds = SCENE_CACHE.get(scene, dev, need_source=True)
+    return render_f64(default_renderer(dev), ds, cam, settings, mode=mode, surfel_depth=surfel_depth)
 
 
 def _host(t):
@@ -145,6 +157,15 @@ def render(scene, cam, settings: RenderSettings | None = None, *, to_numpy: bool
     """forward.py:403-417: both passes and the layer-selected image in one
     device frame (fused tile kernel)."""
     settings = _check_settings(settings)
+    if _is_f64(settings):
+        fr = _render_f64(scene, cam, settings, 3)
+        if not to_numpy:
+            return RenderResult(fr.image, _surfel_buffers(fr, False), _gauss_buffers(fr, False))
+        cov = torch.isfinite(fr.s_depth)
+        hs = [_host(t) for t in (fr.image, fr.s_color, fr.s_depth, fr.s_normal, cov, fr.s_winner,
+                                 fr.g_color, fr.g_weight, fr.g_depth, fr.g_normal)]
+        a = _numpy(*hs)
+        return RenderResult(a[0], SurfelBuffers(*a[1:6]), GaussianBuffers(*a[6:10]))
     dev = _device()
     ds = SCENE_CACHE.get(scene, dev)
     fr = default_renderer(dev).render(ds, cam, settings, mode=3)
@@ -161,6 +182,8 @@ def render(scene, cam, settings: RenderSettings | None = None, *, to_numpy: bool
 def rasterize_surfels(scene, cam, settings: RenderSettings | None = None, *, to_numpy: bool = True) -> SurfelBuffers:
     """forward.py:127-209."""
     settings = _check_settings(settings)
+    if _is_f64(settings):
+        return _surfel_buffers(_render_f64(scene, cam, settings, 1), to_numpy)
     dev = _device()
     ds = SCENE_CACHE.get(scene, dev)
     fr = default_renderer(dev).render(ds, cam, settings, mode=1,
@@ -173,6 +196,12 @@ def accumulate_gaussians(scene, cam, surfel_depth, settings: RenderSettings | No
     """forward.py:218-245 against a given (H, W) surfel depth map."""
     settings = _check_settings(settings)
     dev = _device()
+    if _is_f64(settings):
+        dep = torch.as_tensor(np.asarray(surfel_depth, dtype=np.float64) if not torch.is_tensor(surfel_depth)
+                              else surfel_depth, dtype=torch.float64).to(dev).contiguous()
+        if tuple(dep.shape) != (int(cam.height), int(cam.width)):
+            raise ValueError("surfel_depth must have shape (height, width)")
+        return _gauss_buffers(_render_f64(scene, cam, settings, 2, dep), to_numpy)
     ds = SCENE_CACHE.get(scene, dev)
     dep = torch.as_tensor(np.asarray(surfel_depth, dtype=np.float32) if not torch.is_tensor(surfel_depth)
                           else surfel_depth, dtype=torch.float32).to(dev).contiguous()
@@ -189,10 +218,30 @@ def _dev_f32(a, dev):
     return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).to(dev)
 
 
+def _dev_f64(a, dev):
+    if torch.is_tensor(a):
+        return a.to(dev, torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).to(dev)
+
+
+def _float64_inputs(*arrays) -> bool:
+    """float64 buffers in -> the float64 kernels (as the reference keeps the dtype)."""
+    return all((a.dtype == torch.float64) if torch.is_tensor(a) else (np.asarray(a).dtype == np.float64)
+               for a in arrays)
+
+
 def composite(surfel_color, gaussian: GaussianBuffers, surfel_weight: float = 1.0):
-    """forward.py:384-388: (C_s * w_s + C_G) / (w_s + W_G) on the device."""
+    """forward.py:384-388: (C_s * w_s + C_G) / (w_s + W_G) on the device
+    (float64 kernels when the buffers are float64)."""
     dev = _device()
     as_np = not torch.is_tensor(surfel_color)
+    if _float64_inputs(surfel_color, gaussian.color, gaussian.weight):
+        sc, gc, gw = (_dev_f64(x, dev) for x in (surfel_color, gaussian.color, gaussian.weight))
+        img = torch.empty_like(sc)
+        _lib.check(_lib.lib().ges_composite_f64(sc.data_ptr(), gc.data_ptr(), gw.data_ptr(), float(surfel_weight),
+                                                img.data_ptr(), gw.numel(),
+                                                torch.cuda.current_stream(dev).cuda_stream), "ges_composite_f64")
+        return _np(img) if as_np else img
     sc = _dev_f32(surfel_color, dev)
     gc = _dev_f32(gaussian.color, dev)
     gw = _dev_f32(gaussian.weight, dev)
@@ -210,6 +259,17 @@ def smooth_geometry(surfel_buffers: SurfelBuffers, gaussian: GaussianBuffers):
         raise ValueError("gaussian buffers were rendered without geometry accumulation")
     dev = _device()
     as_np = not torch.is_tensor(surfel_buffers.depth)
+    if _float64_inputs(surfel_buffers.depth, surfel_buffers.normal, gaussian.depth, gaussian.normal,
+                       gaussian.weight):
+        sd, sn, gd, gn, gw = (_dev_f64(x, dev) for x in (surfel_buffers.depth, surfel_buffers.normal,
+                                                          gaussian.depth, gaussian.normal, gaussian.weight))
+        d = torch.empty_like(sd)
+        nrm = torch.empty_like(sn)
+        _lib.check(_lib.lib().ges_smooth_geometry_f64(sd.data_ptr(), sn.data_ptr(), gd.data_ptr(), gn.data_ptr(),
+                                                      gw.data_ptr(), d.data_ptr(), nrm.data_ptr(), sd.numel(),
+                                                      torch.cuda.current_stream(dev).cuda_stream),
+                   "ges_smooth_geometry_f64")
+        return _numpy(_host(d), _host(nrm)) if as_np else (d, nrm)
     sd = _dev_f32(surfel_buffers.depth, dev)
     sn = _dev_f32(surfel_buffers.normal, dev)
     gd = _dev_f32(gaussian.depth, dev)

@@ -235,16 +235,18 @@ class _SceneCache:
             crc = zlib.crc32(v.view(np.uint8).reshape(-1) if v.size else b"", crc)
         return crc
 
-    def get(self, scene, device):
+    def get(self, scene, device, *, need_source: bool = False):
+        """The packed scene; ``need_source``: with its float64 source arrays
+        kept on the device (float64 render mode)."""
         key, arrs = self._key(scene, device)
         with self.lock:
             mode = self.verify
             fp = self._fingerprint(arrs, mode)
             hit = self.d.get(key)
-            if hit is not None and hit[2] == (mode, fp):
+            if hit is not None and hit[2] == (mode, fp) and (not need_source or hit[0].src is not None):
                 self.d.move_to_end(key)
                 return hit[0]
-            ds = DeviceScene(scene, device)
+            ds = DeviceScene(scene, device, keep_source=need_source)
             self.d[key] = (ds, arrs, (mode, fp))   # holding arrs pins the ids
             self.d.move_to_end(key)
             while len(self.d) > self.size:
@@ -382,6 +384,81 @@ class Renderer:
             self.cap_s = max(self.cap_s, int(sp * 1.25) + 1024)
             self.cap_g = max(self.cap_g, int(gp * 1.25) + 1024)
         raise RuntimeError("tile pair lists overflowed repeatedly")
+
+
+@dataclass
+class FrameF64:
+    """Float64 device outputs of one render_f64 call (any field may be None)."""
+    image: torch.Tensor = None
+    s_color: torch.Tensor = None
+    s_depth: torch.Tensor = None
+    s_normal: torch.Tensor = None
+    s_winner: torch.Tensor = None
+    g_color: torch.Tensor = None
+    g_weight: torch.Tensor = None
+    g_depth: torch.Tensor = None
+    g_normal: torch.Tensor = None
+    status: torch.Tensor = None
+
+    def pairs(self):
+        st = self.status.cpu()
+        return int(st[0]), int(st[1]), int(st[2] & 0xFFFFFFFF)
+
+
+def render_f64(r: "Renderer", ds: DeviceScene, cam, settings, *, mode: int = 3,
+               surfel_depth: torch.Tensor = None) -> FrameF64:
+    """Float64 render (ges_render_f64): mode 3 render, 1 rasterize_surfels,
+    2 accumulate_gaussians against ``surfel_depth`` (H, W) float64 on the
+    device.  ``ds`` must keep its float64 source arrays."""
+    if ds.src is None:
+        raise ValueError("the float64 render needs DeviceScene(keep_source=True)")
+    cam_c = camera_struct(cam)
+    st_c = settings_struct(settings)
+    H, W = int(cam.height), int(cam.width)
+    f64 = dict(dtype=torch.float64, device=r.device)
+    fr = FrameF64(status=torch.zeros(STATUS_WORDS, dtype=torch.int64, device=r.device))
+    if mode & 1:
+        fr.s_color = torch.empty((H, W, 3), **f64)
+        fr.s_depth = torch.empty((H, W), **f64)
+        fr.s_normal = torch.empty((H, W, 3), **f64)
+        fr.s_winner = torch.empty((H, W), dtype=torch.int32, device=r.device)
+    if mode & 2 or (mode == 3):
+        fr.g_color = torch.empty((H, W, 3), **f64)
+        fr.g_weight = torch.empty((H, W), **f64)
+        if settings.with_geometry and (mode & 2):
+            fr.g_depth = torch.empty((H, W), **f64)
+            fr.g_normal = torch.empty((H, W, 3), **f64)
+    if mode == 3:
+        fr.image = torch.empty((H, W, 3), **f64)
+    out = _lib.OutputsF64()
+    for k in ("image", "s_color", "s_depth", "s_normal", "s_winner", "g_color", "g_weight", "g_depth", "g_normal"):
+        t = getattr(fr, k)
+        setattr(out, k, t.data_ptr() if t is not None else None)
+    dep = None
+    if mode == 2:
+        dep = surfel_depth.to(r.device, torch.float64).contiguous()
+    L = _lib.lib()
+    for attempt in range(3):
+        r._caps(ds, settings.supersample)
+        need = L.ges_workspace_bytes_f64(C.byref(ds.c), C.byref(cam_c), C.byref(st_c), r.cap_s, r.cap_g)
+        if need == 0:
+            _lib.check(_lib.GES_EINVAL, "ges_workspace_bytes_f64")
+        if r._ws is None or r._ws.numel() < need:
+            r._ws = None
+            r._ws = torch.empty(need, dtype=torch.uint8, device=r.device)
+        stream = C.c_void_p(torch.cuda.current_stream(r.device).cuda_stream)
+        rc = L.ges_render_f64(C.byref(ds.c), C.byref(ds.src), C.byref(cam_c), C.byref(st_c), mode,
+                              C.c_void_p(dep.data_ptr()) if dep is not None else None, C.byref(out),
+                              C.c_void_p(r._ws.data_ptr()), need, r.cap_s, r.cap_g,
+                              C.c_void_p(fr.status.data_ptr()), stream)
+        _lib.check(rc, "render_f64")
+        ds.blob.record_stream(torch.cuda.current_stream(r.device))
+        sp, gp, ovf = fr.pairs()
+        if not ovf:
+            return fr
+        r.cap_s = max(r.cap_s, int(sp * 1.25) + 1024)
+        r.cap_g = max(r.cap_g, int(gp * 1.25) + 1024)
+    raise RuntimeError("tile pair lists overflowed repeatedly")
 
 
 _LOCAL = threading.local()

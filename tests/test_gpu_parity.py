@@ -273,7 +273,7 @@ def test_settings_validation():
         G.RenderSettings(epsilon_mode="x")
     sc = S.random_scene(np.random.default_rng(0), 3, 3)
     with pytest.raises(NotImplementedError):
-        G.render(sc, S.make_camera(), G.RenderSettings(dtype=np.float64))
+        G.render(sc, S.make_camera(), G.RenderSettings(dtype=np.float16))
     bad = Scene(S.random_surfels(np.random.default_rng(0), 3, 1), GaussianSet.empty(1), 1, Stage.FROZEN)
     bad.surfels.sh = np.zeros((3, 5, 3))
     with pytest.raises(ValueError):
