@@ -187,6 +187,10 @@ SlabMap slab_map(const ges_scene_t& sc, const CamK& c) {
     return m;
 }
 
+#ifndef GES_TILE_ORDER
+#define GES_TILE_ORDER 1   // tile kernel CTAs in descending pair-count order (k_scan computes it)
+#endif
+
 // Float64 mode of a frame (ges_render_f64): the source arrays, the float64
 // outputs and the external float64 surfel depth of the pass-2-only entry.
 struct F64Ctx {
@@ -236,7 +240,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     if (!do_g) scs.n_gaussians = 0;
     auto log2i = [](int v) { int k = 0; while ((1 << k) < v) ++k; return k; };
     const BinPass bs{f.cnt_s, f.off_s, f.chunk_s, f.tickets, f.list_s, cap_s, f.ntiles, f.ntx, tp * grid,
-                     log2i(tp * grid), do_s ? f.order : nullptr, f.tot};
+                     log2i(tp * grid), (do_s && GES_TILE_ORDER) ? f.order : nullptr, f.tot};
     const BinPass bg{f.cnt_g, f.off_g, f.chunk_g, f.tickets + 32, f.list_g, cap_g, f.ntiles, f.ntx, tp, log2i(tp)};
     // both preprocesses of a full frame run concurrently: Gaussians on the side lane
     SideLane* lane = (do_s && do_g && scs.n_surfels && scs.n_gaussians) ? side_lane(s) : nullptr;
