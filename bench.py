@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--cpu-tiles", type=int, default=1 << 30,
                    help="tiles in the CPU sample (default: the whole frame, about 12 s of CPU work at config 2)")
     p.add_argument("--profile-only", action="store_true", help="render a few frames, no JSON (for ncu)")
+    p.add_argument("--strips", action="store_true",
+                   help="one frame per step split into row strips over the ranks (SURVEY 8(e) single huge frame)")
     return p.parse_args()
 
 
@@ -341,6 +343,13 @@ def run_gpu(args, rank, world, local_rank):
     per_rank = per_rank_views(cfg, world, args.views)
     scene = S.config_scene(cfg)
     cams = views_for(cfg, rank, world, per_rank)
+    strips = None
+    if args.strips:   # one frame per step: this rank's band of rows as a camera of its own
+        from paper_2504_17545_b200.multiview import strip_bounds, strip_camera
+        full_cam = views_for(cfg, 0, 1, 1)[0]
+        strips = strip_bounds(int(full_cam.height), world)
+        cams = [strip_camera(full_cam, *strips[rank])]
+        per_rank = 1
     settings = G.RenderSettings(supersample=args.ss, mip=(cfg == 4), layers=args.layers)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -358,7 +367,11 @@ def run_gpu(args, rank, world, local_rank):
         # (no peer access), all of them fall back to the NCCL gather
         err = None
         try:
-            sink = PeerFrameGather(per_rank, int(cams[0].height), int(cams[0].width), dst=0, device=dev)
+            if strips is not None:
+                sink = PeerFrameGather(1, int(full_cam.height), int(full_cam.width), dst=0, device=dev,
+                                       strips=strips)
+            else:
+                sink = PeerFrameGather(per_rank, int(cams[0].height), int(cams[0].width), dst=0, device=dev)
             if os.environ.get("GES_BENCH_PEER_FAIL") == str(rank):   # test-only: exercise the fallback
                 raise RuntimeError("peer mapping disabled by GES_BENCH_PEER_FAIL")
         except RuntimeError as e:
@@ -376,8 +389,15 @@ def run_gpu(args, rank, world, local_rank):
             gather_used = "peer"
     want = (() if cfg == 5 else ("image", "s_depth", "s_winner")) + \
         (("image_rgba8",) if world > 1 and sink is None else ())
-    vb = ViewBatchRenderer(rend, ds, cams, settings, want=want, streams=args.streams,
-                           rgba_out=sink.slots if sink is not None else None)
+    rgba_out = sink.slots if sink is not None else None
+    strip_pad = None
+    if strips is not None and sink is None and world > 1:
+        # NCCL form of the strip gather: every rank's band padded to the tallest one
+        from paper_2504_17545_b200.multiview import DevicePointer
+        hmax = max(y1 - y0 for y0, y1 in strips)
+        strip_pad = torch.zeros((1, hmax, int(full_cam.width), 4), dtype=torch.uint8, device=dev)
+        rgba_out = [DevicePointer(strip_pad.data_ptr(), strip_pad.numel())]
+    vb = ViewBatchRenderer(rend, ds, cams, settings, want=want, streams=args.streams, rgba_out=rgba_out)
     # size every workspace's pair lists from a checked frame of every view
     for i, r in enumerate(vb.pool):   # (each lane renders views i, i + lanes, ...)
         for c, fr in list(zip(vb.cams, vb.frames))[i::len(vb.pool)]:
@@ -389,6 +409,8 @@ def run_gpu(args, rank, world, local_rank):
         vb.render(check=False)
         if sink is not None:
             sink.fence()
+        elif strip_pad is not None:
+            gather_frames(strip_pad, dst=0)
         elif world > 1 and torch.is_tensor(vb.rgba):
             gather_frames(vb.rgba, dst=0)
 
@@ -424,7 +446,7 @@ def run_gpu(args, rank, world, local_rank):
         elapsed = float(t.item())
     if vb.overflowed():
         raise RuntimeError("tile pair lists overflowed inside the timed region")
-    frames = per_rank * world * args.steps
+    frames = args.steps if strips is not None else per_rank * world * args.steps
     fps = frames / elapsed
     ms_step = elapsed * 1e3 / args.steps
     s_pairs, g_pairs, _ = vb.frames[0].pairs()
@@ -455,7 +477,7 @@ def run_gpu(args, rank, world, local_rank):
 
     # ---- end-to-end through the C ABI with host buffers (ges_render_views_host)
     e2e = e2e_u8 = None
-    if not args.no_e2e and cfg != 5 and len({(c.width, c.height) for c in cams}) == 1:
+    if not args.no_e2e and cfg != 5 and strips is None and len({(c.width, c.height) for c in cams}) == 1:
         W, H = cams[0].width, cams[0].height
         cams_c = (_lib.Camera * per_rank)(*[camera_struct(c) for c in cams])
         cam_pin = torch.empty(C.sizeof(cams_c), dtype=torch.uint8, pin_memory=True)
@@ -539,7 +561,7 @@ def run_gpu(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    balg = b_alg(cfg, cams)
+    balg = b_alg(cfg, [full_cam] if strips is not None else cams)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -566,9 +588,11 @@ def run_gpu(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if cfg == 5 and not args.views else "weak",
+        "scaling": "strong" if (cfg == 5 and not args.views) or strips is not None else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {**base_config(cfg, per_rank, world, args.ss),
+                   **({"parallelism": f"row strips x{world}", "strips": strips,
+                       "views_per_rank_per_step": "one band of one frame"} if strips is not None else {}),
                    **({} if gather_used != "nccl" or args.gather == "nccl" else
                       {"frame_gather": "NCCL gather of RGBA8 frames (peer buffer unavailable)"})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

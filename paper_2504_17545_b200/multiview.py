@@ -14,12 +14,21 @@ traffic is the frame gather to the destination rank.  Two forms:
   destination reads them.
 * ``gather_frames``: the plain NCCL ``gather`` of per-rank send buffers
   (baseline, also used on CPU/gloo).
+
+One huge frame is split into screen strips instead (``strip_bounds`` /
+``strip_camera``): rank r renders rows [y0, y1) as a camera of its own (the
+principal point moved up by y0) -- preprocessing is repeated per rank, the
+binning is clipped to the strip -- and ``PeerFrameGather(..., strips=...)``
+lets each rank's tile kernel write its rows straight into the destination's
+frame.
 """
 
 from __future__ import annotations
 
 import ctypes as C
 import math
+
+import numpy as np
 
 import torch
 import torch.distributed as dist
@@ -30,6 +39,40 @@ def shard(n_views: int, rank: int, world: int) -> range:
     per = math.ceil(n_views / world) if world else 0
     lo = min(n_views, rank * per)
     return range(lo, min(n_views, lo + per))
+
+
+def strip_bounds(height: int, world: int, weights=None, align: int = 32) -> list:
+    """Screen-strip partition of one frame (single huge frame):
+    ``world`` bands of whole rows [y0, y1), cut at multiples of ``align``
+    rows (the tile height) where possible.  ``weights``: optional per-row
+    cost estimate (e.g. the pair counts of a previous frame's tile rows,
+    repeated per row); the cuts then balance the summed weight instead of
+    the row count."""
+    if world <= 1:
+        return [(0, height)]
+    if weights is None:
+        w = np.ones(height)
+    else:
+        w = np.asarray(weights, dtype=np.float64).reshape(-1)
+        if w.size != height:
+            raise ValueError("one weight per row")
+        w = np.maximum(w, 0.0) + 1e-9
+    c = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = [0]
+    for r in range(1, world):
+        y = int(np.searchsorted(c, c[-1] * r / world))
+        y = int(round(y / align)) * align if align > 1 else y
+        cuts.append(min(max(y, cuts[-1]), height))
+    cuts.append(height)
+    return [(cuts[i], cuts[i + 1]) for i in range(world)]
+
+
+def strip_camera(cam, y0: int, y1: int):
+    """The camera of rows [y0, y1) of ``cam``'s frame: same intrinsics and
+    pose with the principal point moved up by y0, so every pixel centre ray
+    (cameras.py:59-73) is the full frame's, and the strip renders exactly the
+    full frame's rows (the per-pixel tests do not depend on the tiling)."""
+    return type(cam)(cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.width, y1 - y0, cam.world_to_camera)
 
 
 def gather_frames(local: torch.Tensor, dst: int = 0, group=None):
@@ -78,7 +121,11 @@ class PeerFrameGather:
     ``slots`` to ``ViewBatchRenderer(rgba_out=...)``; after each step call
     ``fence()`` on every rank; ``frames`` (dst only) is the gathered batch."""
 
-    def __init__(self, frames_per_rank: int, height: int, width: int, *, dst: int = 0, group=None, device=None):
+    def __init__(self, frames_per_rank: int, height: int, width: int, *, dst: int = 0, group=None, device=None,
+                 strips=None):
+        """``strips``: screen-strip form instead of view batches -- one
+        (height, width, 4) frame on ``dst``, this rank's slot the rows
+        strips[rank] = (y0, y1) (``frames_per_rank`` must be 1)."""
         from . import _lib
         self.L = _lib.lib()
         self.group = group
@@ -89,7 +136,9 @@ class PeerFrameGather:
             else torch.device(device)
         self.frame_bytes = height * width * 4
         V = frames_per_rank
-        total = self.world * V * self.frame_bytes
+        if strips is not None and V != 1:
+            raise ValueError("the strip form gathers one frame")
+        total = (1 if strips is not None else self.world * V) * self.frame_bytes
         handle = None
         self._owned = self._opened = None
         if self.rank == dst:
@@ -112,9 +161,15 @@ class PeerFrameGather:
             _lib.check(self.L.ges_peer_open(handle, self.device.index, C.byref(ptr)), "peer buffer open")
             self._opened = base = ptr.value
         self.base = base
-        first = self.rank * V * self.frame_bytes
-        self.slots = [DevicePointer(base + first + k * self.frame_bytes, self.frame_bytes) for k in range(V)]
-        self.frames = (torch.as_tensor(_CudaArray(base, (self.world * V, height, width, 4)), device=self.device)
+        if strips is not None:
+            y0, y1 = strips[self.rank]
+            self.slots = [DevicePointer(base + y0 * width * 4, (y1 - y0) * width * 4)]
+            nf = 1
+        else:
+            first = self.rank * V * self.frame_bytes
+            self.slots = [DevicePointer(base + first + k * self.frame_bytes, self.frame_bytes) for k in range(V)]
+            nf = self.world * V
+        self.frames = (torch.as_tensor(_CudaArray(base, (nf, height, width, 4)), device=self.device)
                        if self.rank == dst else None)
         self._flag = torch.zeros(1, device=self.device) if dist.is_initialized() else None
 

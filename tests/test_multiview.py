@@ -76,3 +76,29 @@ def test_gather_frames_gloo_world2():
     expect = np.stack([_render_rgba(scene, c) for c in cams])
     assert got.shape == expect.shape
     assert np.array_equal(got, expect)
+
+
+def test_strip_bounds_and_cameras_tile_the_frame():
+    """Screen strips (SURVEY 8(e) single huge frame): the bands cover the
+    rows exactly once, and each strip camera's pixel-centre rays are the
+    full camera's rays of those rows (cameras.py:59-73)."""
+    import numpy as np
+    from oracle import ges_oracle as O
+    from paper_2504_17545_b200 import scenes as S
+    from paper_2504_17545_b200.multiview import strip_bounds, strip_camera
+    cam = S.make_camera(200, 150)
+    full = O.as_cam(cam).rays()
+    for world in (1, 2, 3, 4, 8):
+        b = strip_bounds(cam.height, world, align=16)
+        assert b[0][0] == 0 and b[-1][1] == cam.height and len(b) == world
+        assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+        assert all(y0 % 16 == 0 for y0, _ in b)
+        for y0, y1 in b:
+            if y1 > y0:
+                sc = strip_camera(cam, y0, y1)
+                assert (sc.height, sc.width) == (y1 - y0, cam.width)
+                np.testing.assert_array_equal(O.as_cam(sc).rays(), full[y0:y1])
+    # cost-weighted cuts: all the weight in the bottom half moves the cut down
+    w = np.r_[np.zeros(75), np.ones(75)]
+    (a0, a1), (b0, b1) = strip_bounds(150, 2, weights=w, align=1)
+    assert a1 > 100
