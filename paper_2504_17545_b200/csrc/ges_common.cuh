@@ -66,7 +66,7 @@ struct __align__(16) SurfRec {
 //   r0 = (mx_int, mx_frac, my_int, my_frac)       mean2d split for precision
 //   r1 = (pa, pb, pc, sigma)  log2(e) * power = pa dx^2 + pb dx dy + pc dy^2,
 //                             alpha = sigma * 2^(pa dx^2 + ...)
-//   r2 = (pmin, r, g, b)      pmin: log2(e) * power below which alpha < 1/255
+//   r2 = (0, r, g, b)         view colour (x unused)
 struct __align__(16) GaussRec {
     float4 r0, r1, r2;
 };

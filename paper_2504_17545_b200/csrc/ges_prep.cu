@@ -287,11 +287,12 @@ constexpr int GPREP_T = 128;
 // coefficient blocks loaded coalesced (sh_color_warp); all lanes call it.
 template <int DEG>
 __device__ __forceinline__ float3 gauss_view_colour(const ges_scene_t& sc, const CamK& cam, d3 p, float* shw) {
-    const d3 dv = mk(cam.pos[0] - p.x, cam.pos[1] - p.y, cam.pos[2] - p.z);
-    const double inv = 1.0 / fmax(sqrt(dot(dv, dv)), 1e-12);
+    // (the colour is evaluated in float32: the direction is too)
+    const float dx = (float)(cam.pos[0] - p.x), dy = (float)(cam.pos[1] - p.y), dz = (float)(cam.pos[2] - p.z);
+    const float inv = 1.0f / fmaxf(sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))), 1e-12f);
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31u);
     return sh_color_warp<DEG>(sc.g_sh, i0, sc.n_gaussians, shw + (threadIdx.x >> 5) * sh_warp_floats<DEG>(),
-                              (float)(dv.x * inv), (float)(dv.y * inv), (float)(dv.z * inv));
+                              dx * inv, dy * inv, dz * inv);
 }
 
 // 3D EWA: geometry.py:114-132 + forward.py:252-290.
@@ -327,13 +328,17 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_
     double raw_det = cv00 * cv11 - cv01 * cv01;
     double c00 = cv00 + SCREEN_VAR, c11 = cv11 + SCREEN_VAR, c01 = cv01;
     double det = c00 * c11 - c01 * c01;
+    const double idet = 1.0 / det;
     double sig = po.w;
-    if (cfg.mip) sig *= sqrt(fmax(raw_det, 0.0) / det);
+    if (cfg.mip) sig *= sqrt(fmax(raw_det, 0.0) * idet);
     valid = valid && det > 0.0;
-    double la = c11 / det, lb = -c01 / det, lc = c00 / det;
-    double m2max = 2.0 * log(fmax(255.0 * sig, 1e-12));
-    valid = valid && m2max > 0.0;
-    double rx = sqrt(fmax(m2max * c00, 0.0)), ry = sqrt(fmax(m2max * c11, 0.0));
+    double la = c11 * idet, lb = -c01 * idet, lc = c00 * idet;
+    // m2max = 2 ln(max(255 sig, 1e-12)) > 0  <=>  255 sig > 1 (exactly, ln is monotone with
+    // ln 1 = 0); the support box only culls, so its radius is evaluated in float32 and widened
+    valid = valid && 255.0 * sig > 1.0;
+    const float m2 = fmaxf(2.0f * logf((float)(255.0 * sig)), 0.f) * 1.0001f + 1e-6f;
+    const double rx = (double)(sqrtf(m2 * (float)c00) * 1.0001f) + 1e-3;
+    const double ry = (double)(sqrtf(m2 * (float)c11) * 1.0001f) + 1e-3;
     double mx = cam.fx * ts.x * iz + cam.cx, my = cam.fy * ts.y * iz + cam.cy;
     GaussRec rec;
     int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
@@ -366,8 +371,7 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_
         // conic pre-scaled by log2(e): the tile kernel evaluates exp as one ex2
         const double L2E = 1.4426950408889634;
         rec.r1 = make_float4((float)(-0.5 * L2E * la), (float)(-L2E * lb), (float)(-0.5 * L2E * lc), (float)sig);
-        const float pmin = (float)(-0.5 * L2E * m2max) - 1e-4f;
-        rec.r2 = make_float4(pmin, col.x, col.y, col.z);
+        rec.r2 = make_float4(0.f, col.x, col.y, col.z);
         if (cfg.geom) {   // forward.py:277-284: shortest eff_scale axis, camera-facing
             int k = 0;
             double smin = se.x;
