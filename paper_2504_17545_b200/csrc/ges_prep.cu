@@ -285,20 +285,46 @@ constexpr int GPREP_T = 128;
 
 // View colour of this lane's Gaussian (forward.py:99-109) with the warp's
 // coefficient blocks loaded coalesced (sh_color_warp); all lanes call it.
+// Shared state of the warp's SH fetch: TMA rows + mbarrier (degrees 1, 3) or
+// the coalesced-load slice of sh_color_warp (degrees 0, 2).
 template <int DEG>
-__device__ __forceinline__ float3 gauss_view_colour(const ges_scene_t& sc, const CamK& cam, d3 p, float* shw) {
+struct GaussShSmem {
+    static constexpr int FLOATS = sh_bulk_ok<DEG>() ? 32 * sh_bulk_stride<DEG>() : sh_warp_floats<DEG>();
+    alignas(16) float rows[GPREP_T / 32][FLOATS];
+    uint64_t bar[GPREP_T / 32];
+};
+
+// Start the warp's coefficient fetch (TMA bulk copies) at kernel entry.
+template <int DEG>
+__device__ __forceinline__ void gauss_sh_prefetch(const ges_scene_t& sc, GaussShSmem<DEG>& sm) {
+    if constexpr (sh_bulk_ok<DEG>()) {
+        const int w = threadIdx.x >> 5;
+        const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31u);
+        sh_bulk_issue<DEG>(sc.g_sh, i0, sc.n_gaussians, sm.rows[w], &sm.bar[w]);
+    }
+}
+
+template <int DEG>
+__device__ __forceinline__ float3 gauss_view_colour(const ges_scene_t& sc, const CamK& cam, d3 p,
+                                                    GaussShSmem<DEG>& sm) {
     // (the colour is evaluated in float32: the direction is too)
     const float dx = (float)(cam.pos[0] - p.x), dy = (float)(cam.pos[1] - p.y), dz = (float)(cam.pos[2] - p.z);
     const float inv = 1.0f / fmaxf(sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))), 1e-12f);
+    const int w = threadIdx.x >> 5;
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31u);
-    return sh_color_warp<DEG>(sc.g_sh, i0, sc.n_gaussians, shw + (threadIdx.x >> 5) * sh_warp_floats<DEG>(),
-                              dx * inv, dy * inv, dz * inv);
+    if constexpr (sh_bulk_ok<DEG>()) {
+        return sh_color_bulk<DEG>(sm.rows[w], &sm.bar[w], i0, sc.n_gaussians, dx * inv, dy * inv, dz * inv);
+    } else {
+        return sh_color_warp<DEG>(sc.g_sh, i0, sc.n_gaussians, sm.rows[w], dx * inv, dy * inv, dz * inv);
+    }
 }
 
 // 3D EWA: geometry.py:114-132 + forward.py:252-290.
 template <int DEG>
 __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
+    __shared__ GaussShSmem<DEG> shsm;
+    gauss_sh_prefetch<DEG>(sc, shsm);   // TMA: the warp's SH blocks fly during the geometry
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_gaussians;
     if (!valid_thread) i = sc.n_gaussians - 1;
@@ -359,8 +385,7 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_
         y1 = clampi(fy1, cam.H);
         valid = valid && x1 >= x0 && y1 >= y0;
     }
-    __shared__ float shw[(GPREP_T / 32) * sh_warp_floats<DEG>()];
-    const float3 col = gauss_view_colour<DEG>(sc, cam, p, shw);
+    const float3 col = gauss_view_colour<DEG>(sc, cam, p, shsm);
     const float depf = (float)t.z, epsf = cfg.eps_const ? cfg.eps_value : se.w;
     count_tiles(o.bin_count, g, valid, x0, x1, y0, y1, gauss_key(depf, epsf));
     if (!valid_thread) return;
@@ -391,6 +416,8 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_
 template <int DEG>
 __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
+    __shared__ GaussShSmem<DEG> shsm;
+    gauss_sh_prefetch<DEG>(sc, shsm);   // TMA: the warp's SH blocks fly during the geometry
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid_thread = i < sc.n_gaussians;
     if (!valid_thread) i = sc.n_gaussians - 1;
@@ -431,8 +458,7 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss2_prep(ges_
     double zsup = q.z - rmax * sqrt(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z);
     zsup -= 1e-5 * fabs(zsup) + 1e-6;
     const float gkey = (float)zsup - epsf;
-    __shared__ float shw[(GPREP_T / 32) * sh_warp_floats<DEG>()];
-    const float3 col = gauss_view_colour<DEG>(sc, cam, p, shw);
+    const float3 col = gauss_view_colour<DEG>(sc, cam, p, shsm);
     count_tiles(o.bin_count, g, valid, x0, x1, y0, y1, gkey);
     if (!valid_thread) return;
     Gauss2Rec rec;

@@ -105,6 +105,63 @@ __device__ __forceinline__ float3 sh_color_warp(const float* __restrict__ sh, in
     return sh_color_regs<DEG>(c, x, y, z);
 }
 
+// ---- TMA form of the warp's coefficient fetch (degrees 1 and 3: 48 / 192-byte
+// blocks, multiples of 16 B).  sh_bulk_issue: every lane starts a bulk copy
+// (cp.async.bulk, the Blackwell/Hopper TMA engine) of its primitive's block
+// into its own shared row, all completing on one mbarrier; the row stride
+// (K*3 rounded up to 4 floats + 4) keeps the rows' 16-byte reads
+// conflict-free.  Issued at kernel entry, so the loads fly while the caller
+// does its float64 geometry; sh_color_bulk waits on the barrier and evaluates
+// from the row with 16-byte shared loads (no per-lane global loads or
+// shared stores).  Both must be called by all 32 lanes.
+template <int DEG>
+__host__ __device__ constexpr int sh_bulk_stride() { return ((3 * (DEG + 1) * (DEG + 1) + 3) & ~3) + 4; }
+template <int DEG>
+__host__ __device__ constexpr bool sh_bulk_ok() { return (3 * (DEG + 1) * (DEG + 1)) % 4 == 0; }
+
+template <int DEG>
+__device__ __forceinline__ void sh_bulk_issue(const float* __restrict__ sh, int64_t i0, int64_t n, float* smw,
+                                              uint64_t* bar) {
+    constexpr int K3 = 3 * (DEG + 1) * (DEG + 1), STR = sh_bulk_stride<DEG>();
+    const int lane = threadIdx.x & 31;
+    const int cnt = n - i0 < 32 ? (int)(n - i0) : 32;
+    if (cnt <= 0) return;   // a warp past the end has nothing to fetch (and never waits)
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(cnt * K3 * 4) : "memory");
+    }
+    __syncwarp();
+    if (lane < cnt) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smw + lane * STR);
+        const float* src = sh + (i0 + lane) * K3;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(src), "r"(K3 * 4), "r"(b) : "memory");
+    }
+}
+
+template <int DEG>
+__device__ __forceinline__ float3 sh_color_bulk(const float* smw, uint64_t* bar, int64_t i0, int64_t n, float x,
+                                                float y, float z) {
+    constexpr int K3 = 3 * (DEG + 1) * (DEG + 1), STR = sh_bulk_stride<DEG>();
+    if (n - i0 <= 0) return make_float3(0.f, 0.f, 0.f);   // (no fetch was issued for this warp)
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(b) : "memory");
+    }
+    const float4* row = reinterpret_cast<const float4*>(smw + (threadIdx.x & 31) * STR);
+    float c[K3];
+#pragma unroll
+    for (int j = 0; j < K3 / 4; ++j) {
+        const float4 v = row[j];
+        c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
+    }
+    return sh_color_regs<DEG>(c, x, y, z);
+}
+
 __device__ __forceinline__ float3 sh_color_dyn(int deg, const float* __restrict__ sh, float x, float y,
                                                float z) {
     switch (deg) {
