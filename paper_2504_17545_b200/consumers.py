@@ -17,14 +17,21 @@ from .renderer import SCENE_CACHE, default_renderer
 
 
 def covering_counts(scene, cams, dtype=np.float32, *, to_numpy: bool = True):
+    """optim.py:219-230; ``dtype`` selects the float32 or float64 surfel pass
+    like the reference's ``RenderSettings(dtype=dtype)``."""
     settings = _check_settings(RenderSettings(supersample=1, dtype=dtype))
+    f64 = np.dtype(dtype) == np.float64
     dev = _device()
-    ds = SCENE_CACHE.get(scene, dev)
+    ds = SCENE_CACHE.get(scene, dev, need_source=f64)
     r = default_renderer(dev)
     n = ds.n_surfels
     best = torch.zeros(n, dtype=torch.int64, device=dev)
     for cam in cams:
-        fr = r.render(ds, cam, settings, mode=1, want=("s_winner",))
+        if f64:
+            from .renderer import render_f64
+            fr = render_f64(r, ds, cam, settings, mode=1)
+        else:
+            fr = r.render(ds, cam, settings, mode=1, want=("s_winner",))
         w = fr.s_winner.reshape(-1)
         counts = torch.bincount(w[w >= 0].long(), minlength=n)
         best = torch.maximum(best, counts)

@@ -100,6 +100,9 @@ def test_covering_counts_match_oracle_winners():
     assert ties <= 2
     assert int(np.abs(got - best).sum()) <= 2 * ties
     assert got.sum() > 0
+    # in float64 (the reference's covering_counts(..., dtype=np.float64)) the counts are exact
+    got64 = covering_counts(scene, cams, dtype=np.float64)
+    assert np.array_equal(got64, best)
 
 
 def test_covering_counts_exact_like_reference():

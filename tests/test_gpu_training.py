@@ -32,17 +32,43 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
-def _fwd_close(name, a, b, tol=TOL_FWD, frac_ok=0.002):
+def _flags(scene, cam, st):
+    """The parity rule's per-pixel flags (tests/parity.py) for the training
+    forward of this case: the frozen surfel pass is the supersampled opaque
+    z-buffer and the Gaussian pass is gated by sub-sample (0,0)'s depth, as in
+    render() with the same settings (training.py:358-392)."""
+    from golden_io import settings_ns
+    from oracle import ges_oracle as O
+    w = np.asarray(scene.surfels.w)
+    ss = st.get("supersample") or (4 if (w.size == 0 or w.min() >= 30.0) else 1)
+    keys = ("mip", "with_geometry", "epsilon_mode", "epsilon_value", "background")
+    o = O.render(scene, cam, settings_ns(dict({k: st[k] for k in keys if k in st}, supersample=ss)), ties=True)
+    return o.tie, o.tie_color, o.tie_cut
+
+
+def _fwd_close(name, a, b, flags, tol=TOL_FWD):
+    """Every pixel within tol except the oracle's hard ties (excluded, at most
+    0.5 %) and colour-only sub-sample ties; pixels holding fragments at the
+    1/255 cutoff within tol + one flipped fragment's change per flagged
+    fragment (alpha <= CUT_FLIP times the value range)."""
+    from parity import CUT_FLIP
     a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
     assert a.shape == b.shape, name
+    tie, tie_color, cut = flags
+    assert tie.sum() <= max(0.005 * tie.size, 2), (name, int(tie.sum()))
+    keep = ~tie & ~(tie_color if name in ("image", "surfel_color") else np.zeros_like(tie))
     inf = np.isinf(b)
-    assert np.array_equal(np.isinf(a), inf), name
-    err = np.abs(a[~inf] - b[~inf])
-    if err.size == 0:
-        return
-    # a handful of pixels may hold a fragment that sits on a float32/float64 threshold
-    bad = err > tol
-    assert bad.mean() <= frac_ok and err.max() < 0.05, (name, float(err.max()), int(bad.sum()))
+    assert np.array_equal(np.isinf(a)[keep], inf[keep]), name
+    m = keep & ~(inf.any(-1) if inf.ndim == 3 else inf)
+    with np.errstate(invalid="ignore"):
+        err = np.abs(a - b)
+    if err.ndim == 3:
+        err = err.max(axis=-1)
+    fin = np.isfinite(b)
+    span = float(np.abs(b[fin]).max()) if fin.any() else 1.0
+    allow = tol + cut * CUT_FLIP * 2.0 * max(span, 1.0)
+    bad = m & (err > allow)
+    assert not bad.any(), (name, float(err[m].max()), int(bad.sum()))
 
 
 def _grad_close(name, a, b, rel=REL_GRAD):
@@ -59,8 +85,9 @@ def test_training_step_matches_reference(name):
     scene, cam, st, g_img, cot, fwd, grads = load_train(name)
     settings = train_settings(st, TR.TrainSettings)
     frame = TR.render_training(scene, cam, settings, cache_key=0)
+    flags = _flags(scene, cam, st)
     for k, v in fwd.items():
-        _fwd_close(k, getattr(frame, k), v)
+        _fwd_close(k, getattr(frame, k), v, flags)
     out = TR.backward(frame, g_img, **cot)
     for k in TRAIN_GRADS:
         _grad_close(k, getattr(out, k), grads[k])
@@ -96,8 +123,9 @@ def test_training_step_matches_oracle_random(kind, mip, geom):
     rout = TO.backward(scene, cam, so, ref, g_img, **cot)
     sg = train_settings(st, TR.TrainSettings)
     frame = TR.render_training(scene, cam, sg, cache_key=1)
-    _fwd_close("image", frame.image, ref["image"])
-    _fwd_close("gauss_weight", frame.gauss_weight, ref["gauss_weight"])
+    flags = _flags(scene, cam, st)
+    _fwd_close("image", frame.image, ref["image"], flags)
+    _fwd_close("gauss_weight", frame.gauss_weight, ref["gauss_weight"], flags)
     out = TR.backward(frame, g_img, **cot)
     for k in TRAIN_GRADS:
         _grad_close(k, getattr(out, k), rout[k])
