@@ -228,7 +228,10 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
     };
     mark(0);
     if ((e = cudaMemsetAsync(f.cnt_s, 0, f.zero_bytes, s)) != cudaSuccess) return cuda_fail(e, "memset counts");
-    if ((e = cudaMemsetAsync(status, 0, sizeof(ges_frame_status_t), s)) != cudaSuccess)
+    // the surfel preprocess zeroes the status word (it is first read by the scan); without
+    // surfel work a memset does
+    const bool prep_zeroes = (mode & 1) && sc->n_surfels > 0;
+    if (!prep_zeroes && (e = cudaMemsetAsync(status, 0, sizeof(ges_frame_status_t), s)) != cudaSuccess)
         return cuda_fail(e, "memset status");
     mark(1);
     CamK cs = make_cam(*cam, grid), cg = make_cam(*cam, 1);
@@ -250,7 +253,9 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
             return cuda_fail(e, "preprocess fork");
         gs_stream = lane->side;
     }
-    if (do_s && (e = launch_surfel_prep(scs, cs, gs, PrepOut{f.srec, nullptr, f.cnt_s, nullptr, f.scull}, s)))
+    if (do_s && (e = launch_surfel_prep(scs, cs, gs,
+                                        PrepOut{f.srec, nullptr, f.cnt_s, nullptr, f.scull, prep_zeroes ? status : nullptr},
+                                        s)))
         return cuda_fail(e, "surfel preprocess");
     if (do_g && (e = launch_gauss_prep(scs, cg, gg, *st, PrepOut{f.grec, f.g_nrm, f.cnt_g, nullptr, f.gcull},
                                        gs_stream)))

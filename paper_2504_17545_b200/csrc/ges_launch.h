@@ -14,6 +14,7 @@ struct PrepOut {
     float4* aux;            // 2D Gaussians, training backward only: (a1/s1).d and (a2/s2).d
                             // as affine functions of the pixel (2 per Gaussian), or NULL
     float4* cull;           // dense cull records (see SurfRec, GaussRec)
+    ges_frame_status_t* zero_status;   // or NULL: zeroed by the kernel's first thread (replaces a memset)
 };
 
 // Tile grid for the pass: ntx x nty tiles of `tile_px` pixels at resolution W x H.

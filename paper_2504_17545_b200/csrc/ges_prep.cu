@@ -224,6 +224,7 @@ cudaError_t launch_pack(const ges_scene_src_t& src, const ges_scene_t& dst, cuda
 template <int DEG>
 __global__ void __launch_bounds__(256, GES_PREP_MINB) k_surfel_prep(ges_scene_t sc, CamK cam, Grid g, PrepOut o) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i == 0 && o.zero_status) *o.zero_status = ges_frame_status_t{0, 0, 0, 0};
     const bool valid_thread = i < sc.n_surfels;
     if (!valid_thread) i = sc.n_surfels - 1;   // idle lanes still join the warp-wide count
     float4 ps = __ldg(reinterpret_cast<const float4*>(sc.s_pos_s1) + i);
