@@ -141,7 +141,7 @@ Frame layout(void* base, const ges_scene_t* sc, const ges_camera_t* cam, const g
     f.cnt_g = f.cnt_s ? f.cnt_s + nbins : nullptr;
     f.tickets = f.cnt_s ? f.cnt_s + 2 * nbins : nullptr;
     f.zero_bytes = (2 * nbins + 64) * sizeof(uint32_t);
-    const size_t nchunk = (size_t)(f.ntiles + 255) / 256 + 1;
+    const size_t nchunk = ((size_t)f.ntiles >> SCAN_CHUNK_SHIFT) + 2;
     f.order = c.take<uint32_t>(f.ntiles);
     f.tot = c.take<uint32_t>(f.ntiles);
     f.off_s = c.take<uint32_t>(f.ntiles);

@@ -17,77 +17,92 @@
 
 namespace ges {
 
-constexpr int SCAN_T = 256;   // tiles per scan block (one thread per tile)
+constexpr int SCAN_T = 256;                   // threads per scan block
+constexpr int SCAN_W = 1 << SCAN_CHUNK_SHIFT; // tiles per scan block, SCAN_TPW per warp
+constexpr int SCAN_TPW = SCAN_W / (SCAN_T / 32);
+static_assert(SCAN_TPW >= 1 && SCAN_TPW * (SCAN_T / 32) == SCAN_W, "tiles per warp");
+static_assert(NSLAB <= 64, "a warp scans a tile's slab counters in two rounds");
 
-// Grid (nchunks, 2): y selects the pass (0 = surfels, 1 = Gaussians).  Each
-// block turns its tiles' slab counts into slab prefixes (the fill cursors)
-// and writes the block-local exclusive prefix of the tile totals; the last
-// block of a pass to finish scans the chunk totals into chunk bases, so
-// tile_off(t) = chunk_base[t / SCAN_T] + local_off[t].  One launch, no host
+// Grid (ceil(ntiles / SCAN_W), 2): y selects the pass (0 = surfels, 1 =
+// Gaussians).  Each warp turns SCAN_TPW tiles' slab counts into slab prefixes
+// (the fill cursors) with two coalesced loads and a shuffle scan per tile; each block
+// writes the block-local exclusive prefix of its tiles' totals and its sum;
+// the last block of a pass to finish scans the block sums into chunk bases,
+// so tile_off(t) = chunk_base[t / SCAN_W] + local_off[t].  One launch, no host
 // sync; the ticket is reset with the per-frame counter memset.
 __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_frame_status_t* st) {
     using Scan = cub::BlockScan<uint32_t, SCAN_T>;
     __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t wtot[SCAN_W];
     __shared__ bool last;
     const BinPass& p = blockIdx.y ? p1 : p0;
     const int n = p.ntiles;
-    const int t = blockIdx.x * SCAN_T + threadIdx.x;
-    uint32_t tot = 0;
-    if (t < n) {
-        uint4* c = reinterpret_cast<uint4*>(p.cnt + (size_t)t * NSLAB);
-        uint4 v[NSLAB / 4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t v0[SCAN_TPW], v1[SCAN_TPW];
 #pragma unroll
-        for (int q = 0; q < NSLAB / 4; ++q) v[q] = __ldcg(c + q);   // all loads in flight at once
+    for (int k = 0; k < SCAN_TPW; ++k) {   // all loads in flight first
+        const int t = blockIdx.x * SCAN_W + w * SCAN_TPW + k;
+        const uint32_t* c = p.cnt + (size_t)t * NSLAB;
+        v0[k] = t < n ? __ldcg(c + lane) : 0u;
+        v1[k] = (t < n && lane + 32 < NSLAB) ? __ldcg(c + 32 + lane) : 0u;
+    }
 #pragma unroll
-        for (int q = 0; q < NSLAB / 4; ++q) {
-            uint4 o;
-            o.x = tot; tot += v[q].x;
-            o.y = tot; tot += v[q].y;
-            o.z = tot; tot += v[q].z;
-            o.w = tot; tot += v[q].w;
-            c[q] = o;
+    for (int k = 0; k < SCAN_TPW; ++k) {
+        const int t = blockIdx.x * SCAN_W + w * SCAN_TPW + k;
+        uint32_t i0 = v0[k], i1 = v1[k];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, i0, o), b = __shfl_up_sync(0xffffffffu, i1, o);
+            if (lane >= o) { i0 += a; i1 += b; }
         }
+        const uint32_t s0 = __shfl_sync(0xffffffffu, i0, 31), s1 = __shfl_sync(0xffffffffu, i1, 31);
+        if (t < n) {
+            uint32_t* c = p.cnt + (size_t)t * NSLAB;
+            c[lane] = i0 - v0[k];
+            if (lane + 32 < NSLAB) c[32 + lane] = s0 + i1 - v1[k];
+        }
+        if (lane == 0) wtot[w * SCAN_TPW + k] = s0 + s1;
     }
-    uint32_t ex, blk;
-    Scan(tmp).ExclusiveSum(tot, ex, blk);
-    if (t < n) {
-        p.off[t] = ex;
-        if (p.order) p.tot[t] = tot;
+    __syncthreads();
+    if (w == 0) {   // block-local exclusive prefix of the SCAN_W (<= 32) tile totals
+        static_assert(SCAN_W <= 32, "one warp scans the block's tile totals");
+        const uint32_t v = lane < SCAN_W ? wtot[lane] : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < SCAN_W; o <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += a;
+        }
+        const int tl = blockIdx.x * SCAN_W + lane;
+        if (lane < SCAN_W && tl < n) {
+            p.off[tl] = inc - v;
+            if (p.order) p.tot[tl] = v;
+        }
+        if (lane == SCAN_W - 1) p.chunk[blockIdx.x] = inc;
     }
-    // every thread's off/tot stores must be ordered before the ticket: the
-    // last block reads p.tot (twice, for the order's bucket counts and its
-    // scatter) as soon as the ticket says all blocks are done
+    // every off/tot/chunk store must be ordered before the ticket: the last
+    // block reads them as soon as the ticket says all blocks are done
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-        p.chunk[blockIdx.x] = blk;
         __threadfence();
         last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // last block: exclusive scan of the chunk totals (<= SCAN_T * 8 chunks)
+    // last block: exclusive scan of the block sums, `per` consecutive ones per thread
     const int nc = gridDim.x;
     const int per = (nc + SCAN_T - 1) / SCAN_T;
+    const int c0 = threadIdx.x * per, c1 = min(c0 + per, nc);
     uint32_t run = 0;
-    uint32_t vals[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = threadIdx.x * per + k;
-        vals[k] = (k < per && i < nc) ? *((volatile uint32_t*)p.chunk + i) : 0u;
-        run += vals[k];
-    }
+    for (int i = c0; i < c1; ++i) run += *((volatile uint32_t*)p.chunk + i);
     uint32_t base, total;
-    __syncthreads();
     Scan(tmp).ExclusiveSum(run, base, total);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = threadIdx.x * per + k;
-        if (k < per && i < nc) {
-            p.chunk[i] = base;
-            base += vals[k];
-        }
+    for (int i = c0; i < c1; ++i) {
+        const uint32_t v = *((volatile uint32_t*)p.chunk + i);
+        p.chunk[i] = base;
+        base += v;
     }
     if (threadIdx.x == 0) {
         p.chunk[nc] = total;
@@ -102,7 +117,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
     __shared__ uint32_t bucket[33];
     if (threadIdx.x < 33) bucket[threadIdx.x] = 0;
     constexpr int PER = 8;   // tiles per thread (n <= 2048 here; larger grids loop)
-    const unsigned lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    const unsigned ln = threadIdx.x & 31, lt = (1u << ln) - 1u;
     for (int c0 = 0; c0 < n; c0 += SCAN_T * PER) {
         int bk[PER];
 #pragma unroll
@@ -143,7 +158,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
             const unsigned peers = __match_any_sync(0xffffffffu, b);
             const int leader = __ffs(peers) - 1;
             uint32_t pos = 0;
-            if (b >= 0 && (int)lane == leader) pos = atomicAdd(&bucket[b], (uint32_t)__popc(peers));
+            if (b >= 0 && (int)ln == leader) pos = atomicAdd(&bucket[b], (uint32_t)__popc(peers));
             pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(peers & lt);
             if (b >= 0) p.order[pos] = (uint32_t)i;
         }
@@ -151,8 +166,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
 }
 
 cudaError_t launch_scan(const BinPass& s, const BinPass& g, ges_frame_status_t* status, cudaStream_t st) {
-    const int nc = (s.ntiles + SCAN_T - 1) / SCAN_T;
-    if (nc > SCAN_T * 8) return cudaErrorInvalidValue;   // > 524288 tiles
+    const int nc = (s.ntiles + SCAN_W - 1) / SCAN_W;
+    if (nc == 0) return cudaSuccess;
     k_scan<<<dim3(nc, 2), SCAN_T, 0, st>>>(s, g, status);
     return cudaGetLastError();
 }

@@ -118,18 +118,24 @@ struct SlabMap {
 // D_s > d - eps (forward.py:310).
 __device__ __forceinline__ float gauss_key(float depth, float eps) { return depth - eps; }
 
+// Tiles per scan chunk (k_scan block: 8 warps, 2^SCAN_CHUNK_SHIFT / 8 tiles each).
+#ifndef GES_SCAN_CHUNK_SHIFT
+#define GES_SCAN_CHUNK_SHIFT 5
+#endif
+constexpr int SCAN_CHUNK_SHIFT = GES_SCAN_CHUNK_SHIFT;
+
 // One binning pass (surfels or Gaussians).
 struct BinPass {
     uint32_t* cnt;      // ntiles * NSLAB: counts -> slab prefix -> slab ends
     uint32_t* off;      // ntiles: first list slot of each tile within its scan chunk
-    uint32_t* chunk;    // nchunks + 1: first list slot of each chunk of 256 tiles; [nchunks] = total
+    uint32_t* chunk;    // nchunks + 1: first list slot of each chunk of 2^SCAN_CHUNK_SHIFT tiles; [nchunks] = total
     uint32_t* ticket;   // scan completion counter (zeroed per frame)
     uint32_t* list;     // cap primitive ids (packed indices)
     int64_t cap;
     int ntiles, ntx, tile_px, tile_shift;
     uint32_t* order;    // or NULL; surfel pass: tiles by descending pair count (tile kernel launch order)
     uint32_t* tot;      // with order: per-tile pair totals (scan scratch)
-    __device__ __forceinline__ uint32_t tile_off(int t) const { return chunk[t >> 8] + off[t]; }
+    __device__ __forceinline__ uint32_t tile_off(int t) const { return chunk[t >> SCAN_CHUNK_SHIFT] + off[t]; }
 };
 
 __device__ __forceinline__ uint32_t pack_span(int lo, int hi) {
