@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    p.add_argument("--no-others", action="store_true",
+                   help="skip the short measurements of configs 3, 4, 5 in the default run")
     p.add_argument("--cpu-tiles", type=int, default=1 << 30,
                    help="tiles in the CPU sample (default: the whole frame, about 12 s of CPU work at config 2)")
     p.add_argument("--profile-only", action="store_true", help="render a few frames, no JSON (for ncu)")
@@ -326,6 +328,62 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- GPU
+def measure_config(cfg, dev, streams, steps=5, warmup=3):
+    """One other BASELINE configuration, device-timed like the main line (its
+    default views per step in one CUDA graph over `streams` streams, CUDA
+    events around `steps` steps): frames/s, ms/step and the isolated-frame
+    time are reported as extra keys of the default run's line so they are
+    observed by the driver's run."""
+    import torch
+
+    import paper_2504_17545_b200 as G
+    from paper_2504_17545_b200.multiview import ViewBatchRenderer
+
+    t0 = time.perf_counter()
+    per = per_rank_views(cfg, 1, None)
+    cams = views_for(cfg, 0, 1, per)
+    scene = S.config_scene(cfg)
+    settings = G.RenderSettings(mip=(cfg == 4))
+    ds = G.DeviceScene(scene, dev)
+    rend = G.Renderer(dev)
+    vb = ViewBatchRenderer(rend, ds, cams, settings, want=() if cfg == 5 else ("image", "s_depth", "s_winner"),
+                           streams=streams)
+    for i, r in enumerate(vb.pool):
+        for c, fr in list(zip(vb.cams, vb.frames))[i::len(vb.pool)]:
+            r.render(ds, c, settings, frame=fr, check=True)
+    vb.capture()
+    for _ in range(warmup):
+        vb.render()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        vb.render()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    el = e0.elapsed_time(e1) / 1e3
+    if vb.overflowed():
+        raise RuntimeError(f"config {cfg}: tile pair lists overflowed inside the timed region")
+    # isolated frame: the last view alone, eager, on the main stream, through the
+    # renderer (workspace) that rendered it inside the graph
+    lane = vb.pool[(len(cams) - 1) % len(vb.pool)]
+    lane.render(ds, cams[-1], settings, frame=vb.frames[-1], check=False)   # (warm)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    lane.render(ds, cams[-1], settings, frame=vb.frames[-1], check=False)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    out = {"workload": WORKLOADS[cfg], "value": per * steps / el, "unit": "frames/s",
+           "scaling": "strong" if cfg == 5 else "weak", "views_per_step": per, "steps": steps,
+           "warmup": warmup, "ms_per_step": el * 1e3 / steps,
+           "isolated_frame_ms": f0.elapsed_time(f1), "b_alg_bytes_per_frame": b_alg(cfg, cams),
+           "setup_s": time.perf_counter() - t0}
+    del vb, rend, ds
+    return out
+
+
 def run_gpu(args, rank, world, local_rank):
     import ctypes as C
 
@@ -547,6 +605,14 @@ def run_gpu(args, rank, world, local_rank):
                   "path": f"same, RGBA8 frames (the saved 8-bit image, datasets.py:54-56) out, "
                           f"views on {lanes} render streams"}
 
+    # ---- the other BASELINE configurations, measured in the same run (rank 0, N=1, default workload)
+    others = None
+    if rank == 0 and world == 1 and cfg == 2 and args.ss == 1 and not args.strips and not args.no_others:
+        others = {}
+        for oc in (3, 4, 5):
+            others[f"config{oc}"] = measure_config(oc, dev, args.streams, steps=5, warmup=3)
+            torch.cuda.empty_cache()
+
     # ---- CPU baseline sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -615,6 +681,7 @@ def run_gpu(args, rank, world, local_rank):
         "scene_upload_ms": upload_ms,
         "pairs_per_frame": {"surfel": s_pairs, "gaussian": g_pairs},
         "cuda_graph_captured": graphed,
+        "other_configs": others,
     }
     print(json.dumps(line), flush=True)
 
