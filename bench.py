@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    p.add_argument("--tile-mode", type=int, default=0, choices=[0, 1, 2],
+                   help="tile kernel layout: 0 auto, 1 16x16 tiles (1 px/thread), 2 32x32 tiles (2x2 px/thread)")
     p.add_argument("--no-others", action="store_true",
                    help="skip the short measurements of configs 3, 4, 5 in the default run")
     p.add_argument("--cpu-tiles", type=int, default=1 << 30,
@@ -409,6 +411,7 @@ def run_gpu(args, rank, world, local_rank):
         cams = [strip_camera(full_cam, *strips[rank])]
         per_rank = 1
     settings = G.RenderSettings(supersample=args.ss, mip=(cfg == 4), layers=args.layers)
+    settings.tile_mode = args.tile_mode   # (not a reference field: 0 auto, 1 16x16, 2 32x32 tiles)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ds = G.DeviceScene(scene, dev)
