@@ -466,14 +466,15 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                             if (inside && cov && bid[s] == ~0u) GES_STAT(15, 1);
                         }
 #endif
-                        // coverage u^2+v^2 <= R^2, |n.d| > eps|d| and t no later than the
-                        // current best (all multiplied out, den > 0 <=> t > 0); the exact
-                        // t > 0.01 and packed-key comparison run only for candidates
-                        if (den > pe && r2 <= den * den && Awf <= bt[s] * den) {
-                            const float t = A.w * rcp_ftz(den);   // den > 1e-8|d|; 2 ulp: ties are flagged
+                        // coverage u^2+v^2 <= R^2 and t no later than the current best (all
+                        // multiplied out, den > 0 <=> t > 0: with den <= 0 the product
+                        // bt*den is <= 0 or NaN and the filter fails); |n.d| > eps|d|, the
+                        // exact t > 0.01 and the packed-key comparison run only for candidates
+                        if (r2 <= den * den && Awf <= bt[s] * den) {
+                            const float t = A.w * rcp_ftz(den);   // 2 ulp: ties are flagged
                             const uint32_t sid = __float_as_uint(C.z);
                             GES_STAT(4, 1);
-                            if (t > NEAR_F && (t < bt[s] || (t == bt[s] && sid < bid[s]))) {
+                            if (den > pe && t > NEAR_F && (t < bt[s] || (t == bt[s] && sid < bid[s]))) {
                                 bt[s] = t;
                                 bid[s] = sid;
                             }
