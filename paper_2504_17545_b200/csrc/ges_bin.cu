@@ -250,11 +250,14 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
 __global__ void __launch_bounds__(256) k_fill(const float4* __restrict__ scull, int64_t ns, BinPass ps,
                                               const float4* __restrict__ gcull, int64_t ng, int g_kind, BinPass pg,
                                               SlabMap sm) {
+    // launched as a dependent of the scan: the cull records (preprocess output) are read
+    // before pdl_wait, the scan's offsets and cursors only after it
     const unsigned sblocks = (unsigned)((ns + 255) >> 8);   // blockDim.x == 256
     if (blockIdx.x < sblocks) {
         const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
         const bool live = i < ns;
         const float4 r3 = live ? __ldg(scull + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        pdl_wait();
         fill_one(live, (uint32_t)i, __float_as_uint(r3.y), __float_as_uint(r3.z), sm.slab(r3.x), ps);
     } else {
         const int64_t j = (int64_t)(blockIdx.x - sblocks) * 256 + threadIdx.x;
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(256) k_fill(const float4* __restrict__ scull, 
             sx = __float_as_uint(c.z); sy = __float_as_uint(c.w);
             key = g_kind == 2 ? c.x : gauss_key(c.x, c.y);
         }
+        pdl_wait();
         fill_one(live, (uint32_t)j, sx, sy, sm.slab(key), pg);
     }
 }
@@ -274,8 +278,8 @@ cudaError_t launch_fill(const float4* scull, int64_t ns, const BinPass& ps, cons
                         const BinPass& pg, const SlabMap& sm, cudaStream_t s) {
     const int64_t nb = (ns + 255) / 256 + (ng + 255) / 256;
     if (nb == 0) return cudaSuccess;
-    k_fill<<<(unsigned)nb, 256, 0, s>>>(scull, ns, ps, gcull, ng, g_kind, pg, sm);
-    return cudaGetLastError();
+    cudaError_t e = launch_pdl(k_fill, dim3((unsigned)nb), dim3(256), s, scull, ns, ps, gcull, ng, g_kind, pg, sm);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace ges

@@ -7,6 +7,31 @@
 
 namespace ges {
 
+// Programmatic dependent launch (Hopper/Blackwell): the scan -> fill -> tile
+// kernels of a frame are launched so the next one's launch overlaps the
+// previous one's last CTAs; each dependent waits (griddepcontrol.wait) before
+// its first read of the previous kernel's output.
+#ifndef GES_PDL
+#define GES_PDL 1
+#endif
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    if (GES_PDL) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct PrepOut {
     void* rec;              // SurfRec / GaussRec / Gauss2Rec per primitive
     float4* nrm;            // per-primitive camera-facing normal (surfels; Gaussians if geometry)

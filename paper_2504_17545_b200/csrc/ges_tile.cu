@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
     constexpr int G = SS * PX, NS = G * G, NP = PX * PX, TP = TILE * PX;
     constexpr int WPC = tile_wpc<SS, PX>(), TPB = 32 * WPC;
     __shared__ TileSmem<WPC> sm;
+    pdl_wait();   // (launched as a dependent of the fill: lists, offsets, status)
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders
 #ifdef GES_TIMING   // warp lifetimes (tuning builds only, see read_stats / tools/tile_stats.py --timing)
     const long long t_start = clock64();
@@ -826,12 +827,13 @@ template <int SS, int PX, int MODE>
 static void launch_kind(const TileArgs& a, int g_kind, bool geom, cudaStream_t s) {
     constexpr int WPC = tile_wpc<SS, PX>();
     const dim3 nt((unsigned)(a.ntx * (NWARP / WPC)), (unsigned)a.nty);
+    const dim3 tb(32 * WPC);
     if (g_kind == 2) {
-        if (geom) k_tile<SS, PX, MODE, 2, true><<<nt, 32 * WPC, 0, s>>>(a);
-        else k_tile<SS, PX, MODE, 2, false><<<nt, 32 * WPC, 0, s>>>(a);
+        if (geom) launch_pdl(k_tile<SS, PX, MODE, 2, true>, nt, tb, s, a);
+        else launch_pdl(k_tile<SS, PX, MODE, 2, false>, nt, tb, s, a);
     } else {
-        if (geom) k_tile<SS, PX, MODE, 3, true><<<nt, 32 * WPC, 0, s>>>(a);
-        else k_tile<SS, PX, MODE, 3, false><<<nt, 32 * WPC, 0, s>>>(a);
+        if (geom) launch_pdl(k_tile<SS, PX, MODE, 3, true>, nt, tb, s, a);
+        else launch_pdl(k_tile<SS, PX, MODE, 3, false>, nt, tb, s, a);
     }
 }
 

@@ -1,6 +1,6 @@
 # A/B the bench over alternative builds of the library: bash tools/ab_libs.sh lib1.so lib2.so ...
 for lib in "$@"; do
   for i in 1 2; do
-    GES_B200_LIB=$lib python bench.py --steps 40 --warmup 3 --no-cpu --no-e2e --no-others 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('$lib', round(d['value']), {k:round(v*1000,1) for k,v in d['roofline']['phase_ms'].items()})"
+    GES_B200_LIB=$lib python bench.py --steps 40 --warmup 3 --no-cpu --no-e2e --no-others 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('$lib', round(d['value']), round(d['roofline']['frame_ms']*1000,1), {k:round(v*1000,1) for k,v in d['roofline']['phase_ms'].items()})"
   done
 done
