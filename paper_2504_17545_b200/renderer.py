@@ -385,6 +385,61 @@ class Renderer:
             self.cap_g = max(self.cap_g, int(gp * 1.25) + 1024)
         raise RuntimeError("tile pair lists overflowed repeatedly")
 
+    def render_f64(self, ds: DeviceScene, cam, settings, *, mode: int = 3,
+                   surfel_depth: torch.Tensor = None) -> FrameF64:
+        """Float64 render (ges_render_f64): mode 3 render, 1 rasterize_surfels,
+        2 accumulate_gaussians against ``surfel_depth`` (H, W) float64 on the
+        device.  ``ds`` must keep its float64 source arrays."""
+        if ds.src is None:
+            raise ValueError("the float64 render needs DeviceScene(keep_source=True)")
+        cam_c = camera_struct(cam)
+        st_c = settings_struct(settings)
+        H, W = int(cam.height), int(cam.width)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        fr = FrameF64(status=torch.zeros(STATUS_WORDS, dtype=torch.int64, device=self.device))
+        if mode & 1:
+            fr.s_color = torch.empty((H, W, 3), **f64)
+            fr.s_depth = torch.empty((H, W), **f64)
+            fr.s_normal = torch.empty((H, W, 3), **f64)
+            fr.s_winner = torch.empty((H, W), dtype=torch.int32, device=self.device)
+        if mode & 2:
+            fr.g_color = torch.empty((H, W, 3), **f64)
+            fr.g_weight = torch.empty((H, W), **f64)
+            if settings.with_geometry:
+                fr.g_depth = torch.empty((H, W), **f64)
+                fr.g_normal = torch.empty((H, W, 3), **f64)
+        if mode == 3:
+            fr.image = torch.empty((H, W, 3), **f64)
+        out = _lib.OutputsF64()
+        for k in ("image", "s_color", "s_depth", "s_normal", "s_winner", "g_color", "g_weight", "g_depth", "g_normal"):
+            t = getattr(fr, k)
+            setattr(out, k, t.data_ptr() if t is not None else None)
+        dep = None
+        if mode == 2:
+            dep = surfel_depth.to(self.device, torch.float64).contiguous()
+        L = _lib.lib()
+        for attempt in range(3):
+            self._caps(ds, settings.supersample)
+            need = L.ges_workspace_bytes_f64(C.byref(ds.c), C.byref(cam_c), C.byref(st_c), self.cap_s, self.cap_g)
+            if need == 0:
+                _lib.check(_lib.GES_EINVAL, "ges_workspace_bytes_f64")
+            if self._ws is None or self._ws.numel() < need:
+                self._ws = None
+                self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+            rc = L.ges_render_f64(C.byref(ds.c), C.byref(ds.src), C.byref(cam_c), C.byref(st_c), mode,
+                                  C.c_void_p(dep.data_ptr()) if dep is not None else None, C.byref(out),
+                                  C.c_void_p(self._ws.data_ptr()), need, self.cap_s, self.cap_g,
+                                  C.c_void_p(fr.status.data_ptr()), stream)
+            _lib.check(rc, "render_f64")
+            ds.blob.record_stream(torch.cuda.current_stream(self.device))
+            sp, gp, ovf = fr.pairs()
+            if not ovf:
+                return fr
+            self.cap_s = max(self.cap_s, int(sp * 1.25) + 1024)
+            self.cap_g = max(self.cap_g, int(gp * 1.25) + 1024)
+        raise RuntimeError("tile pair lists overflowed repeatedly")
+
 
 @dataclass
 class FrameF64:
@@ -407,58 +462,8 @@ class FrameF64:
 
 def render_f64(r: "Renderer", ds: DeviceScene, cam, settings, *, mode: int = 3,
                surfel_depth: torch.Tensor = None) -> FrameF64:
-    """Float64 render (ges_render_f64): mode 3 render, 1 rasterize_surfels,
-    2 accumulate_gaussians against ``surfel_depth`` (H, W) float64 on the
-    device.  ``ds`` must keep its float64 source arrays."""
-    if ds.src is None:
-        raise ValueError("the float64 render needs DeviceScene(keep_source=True)")
-    cam_c = camera_struct(cam)
-    st_c = settings_struct(settings)
-    H, W = int(cam.height), int(cam.width)
-    f64 = dict(dtype=torch.float64, device=r.device)
-    fr = FrameF64(status=torch.zeros(STATUS_WORDS, dtype=torch.int64, device=r.device))
-    if mode & 1:
-        fr.s_color = torch.empty((H, W, 3), **f64)
-        fr.s_depth = torch.empty((H, W), **f64)
-        fr.s_normal = torch.empty((H, W, 3), **f64)
-        fr.s_winner = torch.empty((H, W), dtype=torch.int32, device=r.device)
-    if mode & 2 or (mode == 3):
-        fr.g_color = torch.empty((H, W, 3), **f64)
-        fr.g_weight = torch.empty((H, W), **f64)
-        if settings.with_geometry and (mode & 2):
-            fr.g_depth = torch.empty((H, W), **f64)
-            fr.g_normal = torch.empty((H, W, 3), **f64)
-    if mode == 3:
-        fr.image = torch.empty((H, W, 3), **f64)
-    out = _lib.OutputsF64()
-    for k in ("image", "s_color", "s_depth", "s_normal", "s_winner", "g_color", "g_weight", "g_depth", "g_normal"):
-        t = getattr(fr, k)
-        setattr(out, k, t.data_ptr() if t is not None else None)
-    dep = None
-    if mode == 2:
-        dep = surfel_depth.to(r.device, torch.float64).contiguous()
-    L = _lib.lib()
-    for attempt in range(3):
-        r._caps(ds, settings.supersample)
-        need = L.ges_workspace_bytes_f64(C.byref(ds.c), C.byref(cam_c), C.byref(st_c), r.cap_s, r.cap_g)
-        if need == 0:
-            _lib.check(_lib.GES_EINVAL, "ges_workspace_bytes_f64")
-        if r._ws is None or r._ws.numel() < need:
-            r._ws = None
-            r._ws = torch.empty(need, dtype=torch.uint8, device=r.device)
-        stream = C.c_void_p(torch.cuda.current_stream(r.device).cuda_stream)
-        rc = L.ges_render_f64(C.byref(ds.c), C.byref(ds.src), C.byref(cam_c), C.byref(st_c), mode,
-                              C.c_void_p(dep.data_ptr()) if dep is not None else None, C.byref(out),
-                              C.c_void_p(r._ws.data_ptr()), need, r.cap_s, r.cap_g,
-                              C.c_void_p(fr.status.data_ptr()), stream)
-        _lib.check(rc, "render_f64")
-        ds.blob.record_stream(torch.cuda.current_stream(r.device))
-        sp, gp, ovf = fr.pairs()
-        if not ovf:
-            return fr
-        r.cap_s = max(r.cap_s, int(sp * 1.25) + 1024)
-        r.cap_g = max(r.cap_g, int(gp * 1.25) + 1024)
-    raise RuntimeError("tile pair lists overflowed repeatedly")
+    """Module-level form of :meth:`Renderer.render_f64`."""
+    return r.render_f64(ds, cam, settings, mode=mode, surfel_depth=surfel_depth)
 
 
 _LOCAL = threading.local()
