@@ -411,6 +411,34 @@ def test_planar_gaussians_dense_with_geometry():
     assert rep["g_depth_maxabs"] < 1e-3 and rep["g_normal_maxabs"] < 1e-3, rep
 
 
+@pytest.mark.parametrize("kind,tile_mode", [("3d", 2), ("3d", 1), ("2d", 2)])
+def test_offscreen_and_edge_straddling_primitives(kind, tile_mode):
+    """The preprocess drops primitives whose (padded) support box misses the
+    image, where the reference clamps them onto the edge tiles and rejects
+    them pixel by pixel (forward.py:85-96): a close, narrow view of the cloud
+    leaves most primitives off-screen on every side and many straddling the
+    edges; every pixel, both tile layouts, against the oracle."""
+    r = np.random.default_rng(46)
+    gk = GaussianKind.TWO_D if kind == "2d" else GaussianKind.THREE_D
+    sc = Scene(S.random_surfels(r, 20000, 2, scale_range=(0.005, 0.03)),
+               S.random_gaussians(r, 8000, 2, kind=gk, scale_range=(0.004, 0.03), extent=1.2), 2, Stage.FROZEN)
+    cam = S.make_camera(640, 120, dist=2.2, fov=20.0)   # wide, short frame: top/bottom edges cut the cloud
+    s32 = settings32({})
+    s32.tile_mode = tile_mode
+    out = G.render(sc, cam, s32)
+    ora = O.render(sc, cam, settings_ns({}), ties=True)
+    assert_parity(compare_oracle(gpu_dict(out), ora_dict(ora), ora))
+    # most candidates really were off-screen: the pair count stays far below the reference's
+    # clamped candidate lists' total
+    full = int(O.surfel_tile_counts(sc, cam).sum()) if tile_mode == 1 else None
+    if full is not None:
+        from paper_2504_17545_b200.renderer import SCENE_CACHE, default_renderer
+        ds = SCENE_CACHE.get(sc, torch.device("cuda", torch.cuda.current_device()))
+        fr = default_renderer().render(ds, cam, s32, mode=1, want=("s_winner",))
+        sp, _, _ = fr.pairs()
+        assert sp < full, (sp, full)
+
+
 def test_odd_sizes_and_aspect():
     sc = S.random_scene(np.random.default_rng(45), 400, 200, degree=1)
     for w, h in ((17, 33), (1, 1), (257, 3)):
