@@ -612,11 +612,26 @@ def run_gpu(args, rank, world, local_rank):
 
         # fp32 frames saturate PCIe with one render stream (more streams only contend)
         v32, b32 = e2e_run(_lib.GES_IMAGE_F32_RGB, 1)
+        # the e2e path's roofline: this box's pinned device->host copy bandwidth
+        probe_n = int(W) * int(H) * 12
+        psrc = torch.empty(probe_n, dtype=torch.uint8, device=dev)
+        pdst = torch.empty(probe_n, dtype=torch.uint8, pin_memory=True)
+        pdst.copy_(psrc)
+        torch.cuda.synchronize()
+        tp = time.perf_counter()
+        for _ in range(16):
+            pdst.copy_(psrc, non_blocking=True)
+        torch.cuda.synchronize()
+        d2h_gbs = 16 * probe_n / (time.perf_counter() - tp) / 1e9
+        del psrc, pdst
         e2e = {"value": v32, "unit": "frames/s", "h2d_bytes_per_step": per_rank * C.sizeof(_lib.Camera),
                "d2h_bytes_per_step": b32,
                "path": "ges_render_views_host (C ABI): host camera structs in, pinned fp32 RGB frames "
                        "(RenderResult.image) out on a copy stream overlapped with the next render; "
-                       "PCIe-bound at 1080p (24.9 MB per frame)"}
+                       "PCIe-bound at 1080p (24.9 MB per frame)",
+               "roofline": {"bound": "pcie_d2h", "achieved": v32 * b32 / per_rank / 1e9,
+                            "peak": d2h_gbs, "unit": "GB/s", "frac": v32 * b32 / per_rank / 1e9 / d2h_gbs,
+                            "peak_source": "measured here: 16 pinned device->host copies of one frame"}}
         v8, b8 = e2e_run(_lib.GES_IMAGE_RGBA8, lanes)
         e2e_u8 = {"value": v8, "unit": "frames/s", "h2d_bytes_per_step": per_rank * C.sizeof(_lib.Camera),
                   "d2h_bytes_per_step": b8,
