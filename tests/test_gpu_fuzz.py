@@ -29,11 +29,13 @@ def _case(seed):
     r = np.random.default_rng(1000 + seed)
     kind = GaussianKind.TWO_D if r.random() < 0.4 else GaussianKind.THREE_D
     deg = int(r.integers(0, 4))
-    ns = int(r.integers(50, 3000))
+    ns = int(r.integers(50, 3000)) if seed % 16 else 0   # every 16th case: Gaussians only
     ng = int(r.integers(0, 1500)) if r.random() < 0.9 else 0
     s_lo = float(r.uniform(0.005, 0.05))
     g_lo = float(r.uniform(0.004, 0.05))
     surf = S.random_surfels(r, ns, deg, scale_range=(s_lo, s_lo * r.uniform(1.5, 4.0)))
+    if seed % 16 == 8:   # ... and every 16th a single surfel
+        surf = surf.select(np.arange(1))
     gs = (S.random_gaussians(r, ng, deg, kind=kind, scale_range=(g_lo, g_lo * r.uniform(1.5, 4.0)), extent=1.2)
           if ng else GaussianSet.empty(deg))
     w, h = int(r.integers(16, 200)), int(r.integers(16, 150))
