@@ -183,11 +183,11 @@ class _SceneCache:
     automatically.  Writing INTO a cached array in place is detected through
     a fingerprint of every source array checked on each hit:
 
-    * ``verify = "sample"`` (default): CRC of up to SAMPLE elements spread
-      evenly over each array (~tens of microseconds per call) -- catches
+    * ``verify = "sample"`` (default): checksum of up to SAMPLE elements spread
+      evenly over each array (~0.15 ms per call at config 2) -- catches
       edits that touch many elements (optimiser steps, rescaling, reloads);
       an edit of a few unsampled elements needs ``invalidate(scene)``;
-    * ``verify = "full"``: CRC of every byte (exact; ~0.5 s per call at
+    * ``verify = "full"``: checksum of every byte (exact; ~0.2 s per call at
       config 2's 1.3M primitives);
     * ``verify = "none"``: identity only.
 
@@ -195,7 +195,7 @@ class _SceneCache:
     (SPEC.md:100-101); the cache never changes a result except by serving a
     scene that was edited in place without a detectable change."""
 
-    SAMPLE = 4096
+    SAMPLE = 1024
 
     def __init__(self, size=4, verify="sample"):
         self.size = size
@@ -220,6 +220,9 @@ class _SceneCache:
                 parts.append((id(a), np.asarray(a).__array_interface__["data"][0], np.asarray(a).shape))
         return (str(device), _kind_dim(scene.gaussians), tuple(parts)), arrs
 
+    _IDX: dict = {}   # array size -> the SAMPLE evenly spaced flat indices
+    _W: dict = {}     # sample length -> odd 64-bit position weights
+
     def _fingerprint(self, arrs, mode):
         if mode == "none":
             return None
@@ -231,8 +234,23 @@ class _SceneCache:
             if mode == "full" or a.size <= self.SAMPLE:
                 v = np.ascontiguousarray(a)
             else:
-                v = a.flat[np.linspace(0, a.size - 1, self.SAMPLE).astype(np.int64)]
-            crc = zlib.crc32(v.view(np.uint8).reshape(-1) if v.size else b"", crc)
+                idx = self._IDX.get(a.size)
+                if idx is None:
+                    idx = self._IDX[a.size] = np.linspace(0, a.size - 1, self.SAMPLE).astype(np.intp)
+                flat = a.reshape(-1) if a.flags.c_contiguous else a.ravel()
+                v = flat.take(idx)
+            b = v.view(np.uint8).reshape(-1)
+            if mode != "full" and b.size % 8 == 0 and b.size:
+                # a position-weighted wrapping sum of the sampled 64-bit words (~10 us per array)
+                u = b.view(np.uint64)
+                w = self._W.get(u.size)
+                if w is None:
+                    w = self._W[u.size] = np.random.default_rng(u.size).integers(
+                        1, 2 ** 63, u.size, dtype=np.uint64) | np.uint64(1)
+                with np.errstate(over="ignore"):
+                    crc = (crc * 1000003 + int((u * w).sum(dtype=np.uint64))) & 0xFFFFFFFFFFFFFFFF
+            else:
+                crc = zlib.adler32(b if b.size else b"", crc & 0xFFFFFFFF)
         return crc
 
     def get(self, scene, device, *, need_source: bool = False):
