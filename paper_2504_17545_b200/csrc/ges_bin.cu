@@ -21,7 +21,6 @@ constexpr int SCAN_T = 256;                   // threads per scan block
 constexpr int SCAN_W = 1 << SCAN_CHUNK_SHIFT; // tiles per scan block, SCAN_TPW per warp
 constexpr int SCAN_TPW = SCAN_W / (SCAN_T / 32);
 static_assert(SCAN_TPW >= 1 && SCAN_TPW * (SCAN_T / 32) == SCAN_W, "tiles per warp");
-static_assert(NSLAB <= 64, "a warp scans a tile's slab counters in two rounds");
 
 // Grid (ceil(ntiles / SCAN_W), 2): y selects the pass (0 = surfels, 1 =
 // Gaussians).  Each warp turns SCAN_TPW tiles' slab counts into slab prefixes
@@ -38,30 +37,31 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(BinPass p0, BinPass p1, ges_fra
     const BinPass& p = blockIdx.y ? p1 : p0;
     const int n = p.ntiles;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t v0[SCAN_TPW], v1[SCAN_TPW];
+    constexpr int R = (NSLAB + 31) / 32;   // 32-slab rounds per tile
+    uint32_t v[SCAN_TPW][R];
 #pragma unroll
     for (int k = 0; k < SCAN_TPW; ++k) {   // all loads in flight first
         const int t = blockIdx.x * SCAN_W + w * SCAN_TPW + k;
         const uint32_t* c = p.cnt + (size_t)t * NSLAB;
-        v0[k] = t < n ? __ldcg(c + lane) : 0u;
-        v1[k] = (t < n && lane + 32 < NSLAB) ? __ldcg(c + 32 + lane) : 0u;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[k][r] = (t < n && 32 * r + lane < NSLAB) ? __ldcg(c + 32 * r + lane) : 0u;
     }
 #pragma unroll
     for (int k = 0; k < SCAN_TPW; ++k) {
         const int t = blockIdx.x * SCAN_W + w * SCAN_TPW + k;
-        uint32_t i0 = v0[k], i1 = v1[k];
+        uint32_t run = 0;   // slabs of the earlier rounds
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t a = __shfl_up_sync(0xffffffffu, i0, o), b = __shfl_up_sync(0xffffffffu, i1, o);
-            if (lane >= o) { i0 += a; i1 += b; }
+        for (int r = 0; r < R; ++r) {
+            uint32_t inc = v[k][r];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += a;
+            }
+            if (t < n && 32 * r + lane < NSLAB) p.cnt[(size_t)t * NSLAB + 32 * r + lane] = run + inc - v[k][r];
+            run += __shfl_sync(0xffffffffu, inc, 31);
         }
-        const uint32_t s0 = __shfl_sync(0xffffffffu, i0, 31), s1 = __shfl_sync(0xffffffffu, i1, 31);
-        if (t < n) {
-            uint32_t* c = p.cnt + (size_t)t * NSLAB;
-            c[lane] = i0 - v0[k];
-            if (lane + 32 < NSLAB) c[32 + lane] = s0 + i1 - v1[k];
-        }
-        if (lane == 0) wtot[w * SCAN_TPW + k] = s0 + s1;
+        if (lane == 0) wtot[w * SCAN_TPW + k] = run;
     }
     __syncthreads();
     if (w == 0) {   // block-local exclusive prefix of the SCAN_W (<= 32) tile totals

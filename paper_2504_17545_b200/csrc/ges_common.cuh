@@ -81,7 +81,7 @@ struct __align__(16) Gauss2Rec {
 // Depth slabs of the (tile, slab) bins: NSLAB equal slabs over the view's
 // depth range [zlo, zlo + NSLAB/inv_dz); keys outside clamp to the end slabs.
 #ifndef GES_NSLAB
-#define GES_NSLAB 48
+#define GES_NSLAB 32
 #endif
 constexpr int NSLAB = GES_NSLAB;   // multiple of 4
 static_assert(NSLAB % 4 == 0, "scan reads slab counters as uint4");
