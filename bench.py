@@ -191,34 +191,26 @@ def strips_for(cfg, steps):
 
 def single_thread_sample(cfg, scene, cam, ss):
     """BASELINE.md section 2 variant (b): threads=1 with default (multi-
-    threaded) OpenBLAS.  Bounded: the per-frame preprocessing + every 16th
-    tile row, extrapolated to the frame (rows x 16)."""
+    threaded) OpenBLAS, one whole frame (config 2: ~15 s on the box)."""
     from oracle import ges_oracle as O
     try:
         from threadpoolctl import threadpool_limits
     except ImportError:   # pragma: no cover
         threadpool_limits = None
     st = _oracle_settings(cfg, 1, ss)
-    ntx = (cam.width + 15) // 16
-    nty = (cam.height + 15) // 16
-    tiles = [r * ntx + c for r in range(0, nty, 16) for c in range(ntx)]
     ctx = threadpool_limits(limits=os.cpu_count() or 1, user_api="blas") if threadpool_limits else None
     try:
         if ctx is not None:
             ctx.__enter__()
-        O.TILE_SECONDS[0] = 0.0
         t0 = time.perf_counter()
-        O.render(scene, cam, st, tiles=tiles)
+        O.render(scene, cam, st)
         wall = time.perf_counter() - t0
     finally:
         if ctx is not None:
             ctx.__exit__(None, None, None)
-    tile_s = O.TILE_SECONDS[0]
-    frame_s = (wall - tile_s) + tile_s * (ntx * nty) / len(tiles)
-    return {"value": 1.0 / frame_s, "unit": "frames/s", "cores": 1, "kind": "port",
-            "sample": f"threads=1, default OpenBLAS threading (BASELINE.md 2(b)): per-frame preprocessing "
-                      f"+ {len(tiles)} of {ntx * nty} tiles (every 16th tile row), extrapolated to the frame",
-            "frame_s": frame_s, "measured_wall_s": wall}
+    return {"value": 1.0 / wall, "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": "threads=1, default OpenBLAS threading (BASELINE.md 2(b)): one whole frame",
+            "frame_s": wall, "measured_wall_s": wall}
 
 
 def run_reference(args, rank, world):

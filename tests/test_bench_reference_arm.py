@@ -22,4 +22,4 @@ def test_reference_arm_json_line():
     assert d["e2e"] == {"value": d["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("config1")
     assert d["steps"] == 2 and d["ms_per_step"] > 0
-    assert d["cpu_baseline"]["single_thread"]["cores"] == 1
+    assert d["cpu_baseline"]["single_thread"]["cores"] == 1 and d["cpu_baseline"]["single_thread"]["frame_s"] > 0
