@@ -213,6 +213,42 @@ def single_thread_sample(cfg, scene, cam, ss):
             "frame_s": wall, "measured_wall_s": wall}
 
 
+def reference_other(cfg, threads):
+    """The reference algorithm on the other BASELINE configurations (the
+    default reference run carries them, next to the GPU line's
+    other_configs): configs 3 and 4 in whole frames (config 4: one frame at
+    each of its four scales); config 5 (3M + 1M at 4K, ~1 min per frame on
+    the box) as its per-frame preprocessing plus 4 of 32 row strips spread
+    over the frame, extrapolated to the frame and labelled so."""
+    from oracle import ges_oracle as O
+    scene = S.config_scene(cfg)
+    cams = views_for(cfg, 0, 1, 4 if cfg == 4 else 1)
+    st = _oracle_settings(cfg, threads, 1)
+    if cfg != 5:
+        t0 = time.perf_counter()
+        for c in cams:
+            O.render(scene, c, st)
+        wall = time.perf_counter() - t0
+        return {"workload": WORKLOADS[cfg], "value": len(cams) / wall, "unit": "frames/s", "cores": threads,
+                "kind": "port", "sample": f"{len(cams)} whole frame(s)", "measured_wall_s": wall}
+    cam = cams[0]
+    groups = O.strip_groups(cam.height, cam.width, 32)
+    sample = [groups[k] for k in (0, 8, 16, 24)]   # strips spread over the frame
+    steps = O.render_steps(scene, cam, st, sample)
+    t0 = time.perf_counter()
+    next(steps)                       # preprocessing + strip 0
+    t1 = time.perf_counter()
+    for _ in range(3):                # strips 8, 16, 24
+        next(steps)
+    t2 = time.perf_counter()
+    strip_s = (t2 - t1) / 3
+    frame_s = (t1 - t0) + strip_s * (len(groups) - 1)
+    return {"workload": WORKLOADS[cfg], "value": 1.0 / frame_s, "unit": "frames/s", "cores": threads,
+            "kind": "port", "sample": f"preprocessing + 4 of {len(groups)} row strips (0, 8, 16, 24) of one "
+                                      f"3840x2160 view, extrapolated to the frame", "frame_s": frame_s,
+            "measured_wall_s": t2 - t0}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm (oracle/ges_oracle.py, the
     NumPy restatement pinned to the reference's goldens; float32 like the
@@ -247,6 +283,9 @@ def run_reference(args, rank, world):
     frames = args.steps / nstrips
     fps = frames / wall
     single = None if args.no_cpu else single_thread_sample(cfg, scene, cam, args.ss)
+    others = None
+    if cfg == 2 and args.ss == 1 and not args.no_others:
+        others = {f"config{oc}": reference_other(oc, threads) for oc in (3, 4, 5)}
     sample = (f"{args.steps} steps = {frames:g} whole {cam.width}x{cam.height} frames, each rendered as "
               f"{nstrips} strips of tile rows (one strip per step, the frame's preprocessing in its first "
               f"strip); oracle/ges_oracle.py float32 with per-tile candidate lists (faster than the "
@@ -261,7 +300,8 @@ def run_reference(args, rank, world):
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
                              "cpu_model": cpu_model(), "sample": sample, "measured_wall_s": wall,
                              "frame_s": wall / frames, "single_thread": single},
-            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "other_configs": others}
     print(json.dumps(line), flush=True)
 
 
