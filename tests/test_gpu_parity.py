@@ -397,6 +397,24 @@ def test_4k_supersampled_config2_scene_tile_sample():
     assert_parity(rep)
 
 
+def test_8k_frame_tile_sample_and_consistency():
+    """7680x4320 (and its 15360x8640 supersampled surfel pass): span packing,
+    tile counts and pair capacities at 8K; sampled tiles against the oracle
+    and, over every pixel, coverage == finite depth == winner >= 0."""
+    sc = S.config_scene(2, scale_down=4)
+    cam = S.make_camera(7680, 4320)
+    for ss in (1, 4):
+        st = {"supersample": ss}
+        out = G.render(sc, cam, settings32(st))
+        cov = out.surfels.winner >= 0
+        assert np.array_equal(cov, np.isfinite(out.surfels.depth)) and np.isfinite(out.image).all()
+        assert cov.mean() > 0.1
+        nt = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+        tiles = sorted(np.random.default_rng(10 + ss).choice(nt, 6, replace=False).tolist() + [nt // 2 + 240])
+        ora = O.render(sc, cam, settings_ns(st), tiles=tiles, ties=True)
+        assert_parity(compare_oracle(gpu_dict(out), ora_dict(ora), ora, region=_tile_region(cam, tiles)))
+
+
 def test_planar_gaussians_dense_with_geometry():
     r = np.random.default_rng(44)
     sc = Scene(S.random_surfels(r, 8000, 1, scale_range=(0.008, 0.03)),
