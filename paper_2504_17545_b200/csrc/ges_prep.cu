@@ -10,7 +10,10 @@
 #include "ges_sh.cuh"
 
 #ifndef GES_PREP_MINB
-#define GES_PREP_MINB 3   // resident 256-thread blocks per SM of the preprocess kernels
+#define GES_PREP_MINB 3   // resident 256-thread blocks per SM of the surfel preprocess
+#endif
+#ifndef GES_GPREP_MINB
+#define GES_GPREP_MINB (2 * GES_PREP_MINB)   // resident 128-thread blocks per SM, Gaussian preprocess
 #endif
 
 namespace ges {
@@ -322,7 +325,7 @@ __device__ __forceinline__ float3 gauss_view_colour(const ges_scene_t& sc, const
 
 // 3D EWA: geometry.py:114-132 + forward.py:252-290.
 template <int DEG>
-__global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+__global__ void __launch_bounds__(GPREP_T, GES_GPREP_MINB) k_gauss3_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     __shared__ GaussShSmem<DEG> shsm;
     gauss_sh_prefetch<DEG>(sc, shsm);   // TMA: the warp's SH blocks fly during the geometry
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss3_prep(ges_
 
 // Planar 2D Gaussians: forward.py:324-351 (+ filters.py:84-109 when mip).
 template <int DEG>
-__global__ void __launch_bounds__(GPREP_T, 2 * GES_PREP_MINB) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
+__global__ void __launch_bounds__(GPREP_T, GES_GPREP_MINB) k_gauss2_prep(ges_scene_t sc, CamK cam, Grid g, GaussCfg cfg,
                                                      PrepOut o) {
     __shared__ GaussShSmem<DEG> shsm;
     gauss_sh_prefetch<DEG>(sc, shsm);   // TMA: the warp's SH blocks fly during the geometry
