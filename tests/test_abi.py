@@ -86,3 +86,35 @@ def test_missing_library_fails_loudly(tmp_path):
     p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
     assert p.returncode != 0
     assert "ImportError" in p.stderr or "RuntimeError" in p.stderr
+
+
+def test_float64_entry_validation():
+    """ges_render_f64 / ges_workspace_bytes_f64 argument checks (no compute):
+    missing source scene, bad mode, missing depth for mode 2, mismatched
+    source, workspace too small."""
+    L = _lib.lib()
+    sc = _lib.Scene(n_surfels=10, n_gaussians=5, sh_degree=1, gaussian_dim=3)
+    src = _lib.SceneSrc(n_surfels=10, n_gaussians=5, sh_degree=1, gaussian_dim=3)
+    cam = _lib.Camera(fx=100.0, fy=100.0, cx=64.0, cy=64.0, width=128, height=128)
+    st = _lib.Settings(supersample=1)
+    out = _lib.OutputsF64()
+    need = L.ges_workspace_bytes_f64(C.byref(sc), C.byref(cam), C.byref(st), 1 << 10, 1 << 10)
+    assert need > L.ges_workspace_bytes(C.byref(sc), C.byref(cam), C.byref(st), 1 << 10, 1 << 10)
+    args = (None, 0, 1 << 10, 1 << 10, None, None)
+    assert L.ges_render_f64(C.byref(sc), None, C.byref(cam), C.byref(st), 3, None, C.byref(out), *args) \
+        == _lib.GES_EINVAL
+    assert L.ges_render_f64(C.byref(sc), C.byref(src), C.byref(cam), C.byref(st), 4, None, C.byref(out), *args) \
+        == _lib.GES_EINVAL
+    assert L.ges_render_f64(C.byref(sc), C.byref(src), C.byref(cam), C.byref(st), 2, None, C.byref(out), *args) \
+        == _lib.GES_EINVAL
+    rc = L.ges_render_f64(C.byref(sc), C.byref(src), C.byref(cam), C.byref(st), 3, None, C.byref(out), *args)
+    assert rc == _lib.GES_EINVAL and "source scene arrays missing" in L.ges_last_error().decode()
+    src2 = _lib.SceneSrc(n_surfels=11, n_gaussians=5, sh_degree=1, gaussian_dim=3)
+    rc = L.ges_render_f64(C.byref(sc), C.byref(src2), C.byref(cam), C.byref(st), 3, None, C.byref(out), *args)
+    assert rc == _lib.GES_EINVAL and "does not match" in L.ges_last_error().decode()
+    empty = _lib.Scene(n_surfels=0, n_gaussians=0, sh_degree=1, gaussian_dim=3)
+    esrc = _lib.SceneSrc(n_surfels=0, n_gaussians=0, sh_degree=1, gaussian_dim=3)
+    rc = L.ges_render_f64(C.byref(empty), C.byref(esrc), C.byref(cam), C.byref(st), 3, None, C.byref(out), *args)
+    assert rc == _lib.GES_EWORKSPACE
+    with pytest.raises(RuntimeError):
+        _lib.check(rc, "render_f64")
