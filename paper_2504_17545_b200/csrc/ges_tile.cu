@@ -445,6 +445,9 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 GES_TM(++tm_t1);
                 const float4 A = sm.st[0][j], B = sm.st[1][j];
                 const float Awf = A.w * 0.99999f;   // candidate filter t <= 1.00001 bt (margin vs rounding)
+#ifdef GES_STATS
+                bool st_any = false;
+#endif
                 // den, U, V at the thread's first sample, then stepped by the
                 // per-sample increments across its G x G block
                 const float den0 = fmaf(A.z, ly0, fmaf(A.y, lx0, A.x));
@@ -465,6 +468,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                             const bool cov = den > pe && r2 <= den * den;
                             if (inside) GES_STAT(cov ? 14 : 13, 1);
                             if (inside && cov && bid[s] == ~0u) GES_STAT(15, 1);
+                            st_any = st_any || (inside && cov);
                         }
 #endif
                         // coverage u^2+v^2 <= R^2 and t no later than the current best (all
@@ -481,6 +485,9 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                             }
                         }
                     }
+#ifdef GES_STATS
+                if (__ballot_sync(0xffffffffu, st_any) == 0u && lane == 0) GES_STAT(16, 1);
+#endif
             }
             wmx = patch_depth();
             __syncwarp();   // the slots are rewritten by the next chunk

@@ -20,7 +20,7 @@ NAMES = ["surfel batches", "surfel entries staged", "  with live mask", "surfel 
          "candidate lanes", "gauss batches", "gauss entries walked (x warps)", "  surviving the warp cull",
          "gauss warp tests", "contributing lanes", "tiles", "tiles with uncovered px",
          "surfel warp tests at wmx=inf", "sample tests: not covered", "sample tests: covered",
-         "  covered, sample still empty", "-", "-", "-", "-"]
+         "  covered, sample still empty", "surfel warp tests covering no sample", "-", "-", "-"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
