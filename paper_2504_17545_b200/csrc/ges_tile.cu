@@ -53,9 +53,6 @@ __device__ unsigned long long g_stats[20];
 #ifndef GES_TILE_WPC1
 #define GES_TILE_WPC1 2  // 16x16-pixel tiles (40 registers: 24 two-warp CTAs per SM)
 #endif
-#ifndef GES_CULL_TMA
-#define GES_CULL_TMA 0   // cull records prefetched one chunk ahead by TMA: bit 0 pass 1, bit 1 pass 2
-#endif
 
 template <int WPC>
 struct __align__(16) TileSmem {
@@ -67,33 +64,7 @@ struct __align__(16) TileSmem {
                                 // 2 x 2 lanes (pass-1 culling)
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
     uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
-#if GES_CULL_TMA
-    float4 cbuf[WPC][32];       // per warp: the next list chunk's 16-byte cull records (TMA)
-    uint64_t cbar[WPC];         // their mbarrier (one phase per chunk)
-#endif
 };
-
-#if GES_CULL_TMA
-// Pass-1 cull-record prefetch: one 16-byte cp.async.bulk per list entry of the
-// next chunk into the warp's shared buffer, completing on the warp's mbarrier
-// (expect_tx armed by lane 0).  All lanes call it.
-__device__ __forceinline__ void cull_issue(float4* buf, uint32_t bar, const float4* __restrict__ cull, uint32_t id,
-                                           int cnt) {
-    const int lane = threadIdx.x & 31;
-    if (lane == 0)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(cnt * 16) : "memory");
-    __syncwarp();
-    if (lane < cnt)
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];"
-                     ::"r"((uint32_t)__cvta_generic_to_shared(buf + lane)), "l"(cull + id), "r"(bar) : "memory");
-}
-__device__ __forceinline__ void cull_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done)
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-}
-#endif
 
 // Lower depth bound of the slab holding relative list position `rel` (slab
 // ends are non-decreasing, so the slab index is the number of ends <= rel:
@@ -354,16 +325,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
         if (gbeg + warp * 32 + lane < gend) gid = a.g_list[gbeg + warp * 32 + lane];
     }
 
-#if GES_CULL_TMA
-    const uint32_t cbar = (uint32_t)__cvta_generic_to_shared(&sm.cbar[wl]);
-    uint32_t cph = 0;   // parity of the barrier's next phase
-    if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cbar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-#endif
-
     // bid[s]: source id of the nearest surfel hit so far (~0u: none); with
     // bt[s] (its hit depth) the pair (bt, bid) is compared lexicographically,
     // == np.argmin with lowest-index ties (forward.py:187); bp[s]: the
@@ -433,36 +394,15 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
         // of its hits.  No CTA barriers: a warp never waits for the others.
         constexpr int PW = 8 * G, PH = 4 * G;   // patch size in surfel-pass pixels
         const int wx0 = ox + (warp & 1) * PW, wy0 = oy + (warp >> 1) * PH;
-#if GES_CULL_TMA & 1
-        // the cull records travel one chunk ahead by TMA, so the ids run two ahead
-        bool inflight = end > beg;
-        if (inflight) cull_issue(sm.cbuf[wl], cbar, a.scull, nid, (int)min(32u, end - beg));
-        uint32_t nid2 = beg + 32 + lane < end ? a.s_list[beg + 32 + lane] : 0u;
-#endif
         for (uint32_t base = beg; base < end; base += 32) {
             // slabs are near-to-far: stop once the next slab lies behind every hit so far
             if (slab_floor(sm.slab_end, a.slabs, base - beg, lane) > wmx) break;
             const uint32_t e = base + lane;
             const uint32_t id = nid;   // this chunk's ids were loaded one chunk ahead
-#if GES_CULL_TMA & 1
-            cull_wait(cbar, cph);
-            cph ^= 1u;
-            const float4 r3t = sm.cbuf[wl][lane];
-            __syncwarp();   // (every lane has its record before the buffer is refilled)
-            inflight = base + 32 < end;
-            if (inflight) cull_issue(sm.cbuf[wl], cbar, a.scull, nid2, (int)min(32u, end - base - 32));
-            nid = nid2;
-            if (e + 64 < end) nid2 = a.s_list[e + 64];
-#else
             if (e + 32 < end) nid = a.s_list[e + 32];
-#endif
             bool live = false;
             if (e < end) {
-#if GES_CULL_TMA & 1
-                const float4 r3 = r3t;
-#else
                 const float4 r3 = __ldg(a.scull + id);
-#endif
                 const uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
                 live = span_lo(sxr) < wx0 + PW && span_hi(sxr) >= wx0 && span_lo(syr) < wy0 + PH &&
                        span_hi(syr) >= wy0 && !(r3.x > wmx);
@@ -552,12 +492,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             wmx = patch_depth();
             __syncwarp();   // the slots are rewritten by the next chunk
         }
-#if GES_CULL_TMA & 1
-        if (inflight) {   // no bulk copy may land after the CTA exits
-            cull_wait(cbar, cph);
-            cph ^= 1u;
-        }
-#endif
         // the winners' SH blocks are read at the end (deferred colour): find
         // their packed indices and start pulling them into L2 now, overlapping
         // the Gaussian pass
@@ -653,43 +587,17 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             lxs[i] = (float)(PX * plx + i); lys[i] = (float)(PX * ply + i);
             asm volatile("" : "+f"(lxs[i]), "+f"(lys[i]));
         }
-#if GES_CULL_TMA & 2
-        // cull records one chunk ahead by TMA, ids two ahead
-        bool ginflight = gend > gbeg;
-        uint32_t gid0 = gbeg + lane < gend ? a.g_list[gbeg + lane] : 0u;
-        if (ginflight) cull_issue(sm.cbuf[wl], cbar, a.gcull, gid0, (int)min(32u, gend - gbeg));
-        uint32_t gid1 = gbeg + 32 + lane < gend ? a.g_list[gbeg + 32 + lane] : 0u;
-#endif
         for (uint32_t base = gbeg; base < gend; base += 32) {
             // keys (depth - eps) are binned near-to-far: the rest fail every gate of the patch
             if (slab_floor(sm.gslab_end, a.slabs, base - gbeg, lane) > wdmax) break;
             const uint32_t e = base + lane;
             bool live = false;
             float v[16];
-#if GES_CULL_TMA & 2
-            cull_wait(cbar, cph);
-            cph ^= 1u;
-            const float4 ct = sm.cbuf[wl][lane];
-            const uint32_t gidc = gid0;
-            __syncwarp();
-            ginflight = base + 32 < gend;
-            if (ginflight) cull_issue(sm.cbuf[wl], cbar, a.gcull, gid1, (int)min(32u, gend - base - 32));
-            gid0 = gid1;
-            if (e + 64 < gend) gid1 = a.g_list[e + 64];
-#endif
             if (e < gend) {
-#if GES_CULL_TMA & 2
-                const uint32_t id = gidc;
-#else
                 const uint32_t id = a.g_list[e];
-#endif
                 if constexpr (GK == 3) {
                     const GaussRec* r = reinterpret_cast<const GaussRec*>(a.grec) + id;
-#if GES_CULL_TMA & 2
-                    const float4 c = ct;
-#else
                     const float4 c = __ldg(a.gcull + id);
-#endif
                     const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
                     // exact conservative cull: d < fl(max_ds + eps) is necessary for the gate
                     live = span_lo(sxr) - ox <= px0 + 8 * PX - 1 && span_hi(sxr) - ox >= px0 &&
@@ -708,11 +616,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                     }
                 } else {
                     const Gauss2Rec* r = reinterpret_cast<const Gauss2Rec*>(a.grec) + id;
-#if GES_CULL_TMA & 2
-                    const float4 c = ct;
-#else
                     const float4 c = __ldg(a.gcull + id);
-#endif
                     const uint32_t sxr = __float_as_uint(c.z), syr = __float_as_uint(c.w);
                     live = span_lo(sxr) - ox <= px0 + 8 * PX - 1 && span_hi(sxr) - ox >= px0 &&
                            span_lo(syr) - oy <= py0 + 4 * PX - 1 && span_hi(syr) - oy >= py0 && !(c.x > wdmax);
@@ -809,9 +713,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             }
             __syncwarp();   // the slots are rewritten by the next step
         }
-#if GES_CULL_TMA & 2
-        if (ginflight) cull_wait(cbar, cph);   // no bulk copy may land after the CTA exits
-#endif
     }
 
     GES_TM(t_p2 = clock64());
