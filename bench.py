@@ -456,7 +456,9 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     cfg = args.config
     per_rank = per_rank_views(cfg, world, args.views)
-    scene = S.config_scene(cfg)
+    # N > 1: rank 0 builds and packs the scene, the other ranks receive the packed
+    # blob by one broadcast (SURVEY 8(e) scene replication)
+    scene = S.config_scene(cfg) if (world == 1 or rank == 0) else None
     cams = views_for(cfg, rank, world, per_rank)
     strips = None
     if args.strips:   # one frame per step: this rank's band of rows as a camera of its own
@@ -469,7 +471,11 @@ def run_gpu(args, rank, world, local_rank):
     settings.tile_mode = args.tile_mode   # (not a reference field: 0 auto, 1 16x16, 2 32x32 tiles)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ds = G.DeviceScene(scene, dev)
+    if world == 1:
+        ds = G.DeviceScene(scene, dev)
+    else:
+        from paper_2504_17545_b200.multiview import broadcast_scene
+        ds = broadcast_scene(scene, src=0, device=dev)
     torch.cuda.synchronize()
     upload_ms = (time.perf_counter() - t0) * 1e3
     rend = G.Renderer(dev)
@@ -768,6 +774,8 @@ def run_gpu(args, rank, world, local_rank):
         "gpu_launches": frames * (5 if ds.n_gaussians else 4),
         "clocks": clk.summary(),
         "scene_upload_ms": upload_ms,
+        "scene_replication": "one scene per rank" if world == 1 else
+                             f"rank 0 packs, packed blob ({ds.nbytes / 1e6:.0f} MB) broadcast over {dist.get_backend()}",
         "pairs_per_frame": {"surfel": s_pairs, "gaussian": g_pairs},
         "cuda_graph_captured": graphed,
         "other_configs": others,

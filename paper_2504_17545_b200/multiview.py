@@ -41,6 +41,37 @@ def shard(n_views: int, rank: int, world: int) -> range:
     return range(lo, min(n_views, lo + per))
 
 
+def broadcast_scene(scene=None, src: int = 0, group=None, device=None):
+    """Scene replication: rank ``src`` loads and packs the scene
+    once (K0; ``scene`` is a reference ``Scene`` or an already packed
+    ``DeviceScene``), every other rank receives the packed blob through one
+    ``broadcast`` (NCCL over NVLink: ~0.3 GB at config 2, instead of each
+    rank uploading the float64 source arrays and packing its own copy).
+    Other ranks pass ``scene=None``.  Returns this rank's ``DeviceScene``
+    (render-only on the receivers: the float64 source arrays stay on
+    ``src``)."""
+    from .renderer import DeviceScene
+
+    if not dist.is_initialized():
+        return scene if isinstance(scene, DeviceScene) else DeviceScene(scene, device)
+    rank = dist.get_rank()   # (src is a global rank, as in dist.broadcast)
+    ds = None
+    hdr = [None]
+    if rank == src:
+        if scene is None:
+            raise ValueError("the source rank needs the scene")
+        ds = scene if isinstance(scene, DeviceScene) else DeviceScene(scene, device)
+        hdr = [ds.header()]
+    dist.broadcast_object_list(hdr, src=src, group=group)
+    if rank == src:
+        blob = ds.blob
+    else:
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        blob = torch.empty(int(hdr[0]["nbytes"]), dtype=torch.uint8, device=dev)
+    dist.broadcast(blob, src=src, group=group)
+    return ds if rank == src else DeviceScene.from_blob(hdr[0], blob)
+
+
 def strip_bounds(height: int, world: int, weights=None, align: int = 32) -> list:
     """Screen-strip partition of one frame (single huge frame):
     ``world`` bands of whole rows [y0, y1), cut at multiples of ``align``

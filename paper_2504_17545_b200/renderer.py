@@ -175,6 +175,50 @@ class DeviceScene:
     def nbytes(self) -> int:
         return self.blob.numel()
 
+    _PTRS = ("s_pos_s1", "s_quat", "s_s2", "s_sh", "s_id", "s_pack", "g_pos_op", "g_quat", "g_scale_eps", "g_sh")
+
+    def header(self) -> dict:
+        """The packed blob's layout (counts, array offsets from the blob
+        base, slab bounds): with the blob's bytes it rebuilds the scene on
+        another device (``from_blob``; ``multiview.broadcast_scene``)."""
+        base = self.blob.data_ptr()
+        offs = {}
+        for n in self._PTRS:
+            p = getattr(self.c, n)
+            offs[n] = None if not p else int(p) - base
+        return {"n_surfels": self.n_surfels, "n_gaussians": self.n_gaussians, "sh_degree": self.sh_degree,
+                "dim": self.dim, "nbytes": self.blob.numel(), "offsets": offs,
+                "bounds": [float(b) for b in self.c.bounds], "any_filter": bool(self.any_filter)}
+
+    @classmethod
+    def from_blob(cls, header: dict, blob: torch.Tensor) -> "DeviceScene":
+        """A packed scene over ``blob`` (uint8, ``header["nbytes"]`` bytes)
+        holding a copy of the bytes another DeviceScene packed; no upload, no
+        pack kernel.  The float64 source arrays do not travel (``src`` is
+        None: render only, not the float64 mode or the training backward)."""
+        if blob.dtype != torch.uint8 or blob.dim() != 1 or not blob.is_contiguous() \
+                or blob.numel() != int(header["nbytes"]):
+            raise ValueError("blob must be a contiguous uint8 vector of header['nbytes'] bytes")
+        self = cls.__new__(cls)
+        self.device = blob.device
+        self.n_surfels, self.n_gaussians = int(header["n_surfels"]), int(header["n_gaussians"])
+        self.sh_degree, self.dim = int(header["sh_degree"]), int(header["dim"])
+        self.any_filter = bool(header["any_filter"])
+        self.blob = blob
+        c = _lib.Scene()
+        c.n_surfels, c.n_gaussians = self.n_surfels, self.n_gaussians
+        c.sh_degree, c.gaussian_dim = self.sh_degree, self.dim
+        base = blob.data_ptr()
+        for n in cls._PTRS:
+            o = header["offsets"][n]
+            if o is not None and not 0 <= int(o) < blob.numel():
+                raise ValueError(f"offset of {n} outside the blob")
+            setattr(c, n, None if o is None else base + int(o))
+        c.bounds[:] = [float(b) for b in header["bounds"]]
+        self.c = c
+        self.src, self._src = None, None
+        return self
+
 
 class _SceneCache:
     """Thread-safe LRU of packed scenes keyed by the identity (object, data

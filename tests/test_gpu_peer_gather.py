@@ -92,6 +92,9 @@ def _nccl_worker(rank, world, port, out_path, log_path):
         sink.fence()
         peer = sink.frames.cpu().numpy().copy()
         # NCCL gather form (the bench's fallback)
+        # scene replication by NCCL broadcast (one rank: the source keeps its own scene)
+        from paper_2504_17545_b200.multiview import broadcast_scene
+        assert broadcast_scene(ds, src=0) is ds
         vb2 = ViewBatchRenderer(G.Renderer(), ds, cams, settings, want=("image_rgba8",))
         vb2.render(check=True)
         got = gather_frames(vb2.rgba, dst=0)
@@ -172,3 +175,69 @@ def test_screen_strips_assemble_the_full_frame(tmp_path):
     d = np.abs(got - ref).max(axis=-1)
     assert (d > 1).mean() <= 1e-3, int((d > 1).sum())   # (a winner flip on a depth tie can exceed 1 LSB)
     assert (got[..., 3] == 255).all()
+
+
+def _bcast_worker(rank, world, port, out_path):
+    import paper_2504_17545_b200 as G
+    from paper_2504_17545_b200 import scenes as S
+    from paper_2504_17545_b200.multiview import broadcast_scene
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        r = np.random.default_rng(12)
+        cam = S.make_camera(160, 120)
+        scene = None
+        if rank == 0:
+            scene = G.Scene(S.random_surfels(r, 3000, 3, scale_range=(0.01, 0.04)),
+                            S.random_gaussians(r, 1500, 3, scale_range=(0.01, 0.05), extent=1.2), 3, G.Stage.FROZEN)
+        ds = broadcast_scene(scene, src=0, device="cuda:0")
+        fr = G.Renderer().render(ds, cam, G.RenderSettings(), want=("image", "s_winner"))
+        img, win = fr.image.cpu().numpy(), fr.s_winner.cpu().numpy()
+        torch.cuda.synchronize()
+        objs = [None, None]
+        dist.all_gather_object(objs, (img, win))
+        if rank == 0:
+            np.savez(out_path, img0=objs[0][0], win0=objs[0][1], img1=objs[1][0], win1=objs[1][1])
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_scene_renders_like_the_source(tmp_path):
+    """Scene replication (multiview.broadcast_scene): rank 0
+    packs, rank 1 receives the packed blob by broadcast and renders the same
+    frame from it (winners identical, image within float rounding of the
+    order-free Gaussian sums)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = str(tmp_path / "bcast.npz")
+    mp.start_processes(_bcast_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+    z = np.load(out)
+    assert np.array_equal(z["win0"], z["win1"]) and (z["win0"] >= 0).any()
+    assert np.abs(z["img0"] - z["img1"]).max() <= 1e-5
+
+
+def test_from_blob_copy_renders_identically():
+    """DeviceScene.from_blob over a copy of a packed scene's bytes: every
+    array pointer rebased, same frame."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_17545_b200 as G
+    from paper_2504_17545_b200 import scenes as S
+    r = np.random.default_rng(13)
+    scene = G.Scene(S.random_surfels(r, 3000, 2, scale_range=(0.01, 0.04)),
+                    S.random_gaussians(r, 1500, 2, kind=G.GaussianKind.TWO_D, scale_range=(0.01, 0.05), extent=1.2),
+                    2, G.Stage.FROZEN)
+    ds = G.DeviceScene(scene)
+    cp = G.DeviceScene.from_blob(ds.header(), ds.blob.clone())
+    assert cp.blob.data_ptr() != ds.blob.data_ptr()
+    cam = S.make_camera(200, 150)
+    rend = G.Renderer()
+    a = rend.render(ds, cam, G.RenderSettings(), want=("image", "s_winner"))
+    a_img, a_win = a.image.cpu().numpy(), a.s_winner.cpu().numpy()
+    del ds   # the copy must not read the source blob
+    torch.cuda.empty_cache()
+    b = rend.render(cp, cam, G.RenderSettings(), want=("image", "s_winner"))
+    assert np.array_equal(a_win, b.s_winner.cpu().numpy()) and (a_win >= 0).any()
+    assert np.abs(a_img - b.image.cpu().numpy()).max() <= 1e-5

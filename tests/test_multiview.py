@@ -102,3 +102,66 @@ def test_strip_bounds_and_cameras_tile_the_frame():
     w = np.r_[np.zeros(75), np.ones(75)]
     (a0, a1), (b0, b1) = strip_bounds(150, 2, weights=w, align=1)
     assert a1 > 100
+
+
+def _fake_header(nbytes):
+    offs = {n: 256 * i for i, n in enumerate(("s_pos_s1", "s_quat", "s_s2", "s_sh", "s_id", "s_pack", "g_pos_op",
+                                              "g_quat", "g_scale_eps", "g_sh"))}
+    offs["g_sh"] = None   # (an array the pack left unset)
+    return {"n_surfels": 5, "n_gaussians": 3, "sh_degree": 1, "dim": 3, "nbytes": nbytes, "offsets": offs,
+            "bounds": [0.5, -1.0, 2.0, 3.0, 4.0, 5.0, 0.25], "any_filter": True}
+
+
+def _bcast_worker(rank, world, port, q):
+    from paper_2504_17545_b200.multiview import broadcast_scene
+    from paper_2504_17545_b200.renderer import DeviceScene
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 4096
+        src = None
+        if rank == 0:   # a host blob stands in for the packed device scene (gloo moves host tensors)
+            src = DeviceScene.from_blob(_fake_header(n), (torch.arange(n) * 7 % 251).to(torch.uint8))
+        ds = broadcast_scene(src, src=0, device="cpu")
+        base = ds.blob.data_ptr()
+        ptrs = {k: getattr(ds.c, k) for k in DeviceScene._PTRS}
+        q.put((rank, ds.blob.numpy().copy(), {k: (None if v is None else v - base) for k, v in ptrs.items()},
+               (ds.c.n_surfels, ds.c.n_gaussians, ds.c.sh_degree, ds.c.gaussian_dim, list(ds.c.bounds),
+                ds.any_filter, ds.header())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_scene_gloo_world2():
+    """rank 0 packs, the other ranks rebuild the scene from the
+    broadcast blob -- same bytes, every array pointer rebased onto the
+    receiver's own blob, same counts and slab bounds."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((r, rest) for r, *rest in (q.get(timeout=120) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    hdr = _fake_header(4096)
+    for r in (0, 1):
+        blob, offs, (ns, ng, deg, dim, bounds, anyf, h) = got[r]
+        assert np.array_equal(blob, (np.arange(4096) * 7 % 251).astype(np.uint8))
+        assert offs == hdr["offsets"]
+        assert (ns, ng, deg, dim, bounds, anyf) == (5, 3, 1, 3, hdr["bounds"], True)
+        assert h == hdr
+
+
+def test_from_blob_rejects_bad_blobs():
+    from paper_2504_17545_b200.renderer import DeviceScene
+    with pytest.raises(ValueError):
+        DeviceScene.from_blob(_fake_header(4096), torch.zeros(100, dtype=torch.uint8))
+    with pytest.raises(ValueError):
+        DeviceScene.from_blob(_fake_header(4096), torch.zeros(4096, dtype=torch.float32))
+    bad = _fake_header(4096)
+    bad["offsets"]["s_quat"] = 5000
+    with pytest.raises(ValueError):
+        DeviceScene.from_blob(bad, torch.zeros(4096, dtype=torch.uint8))
