@@ -284,7 +284,7 @@ int run_frame(const ges_scene_t* sc, const ges_camera_t* cam, const ges_settings
         for (int i = 0; i < 3; ++i) L.bg[i] = (double)st->background[i];
         L.W = cam->width; L.H = cam->height; L.ntx = f.ntx; L.ntiles = f.ntiles; L.grid = grid;
         L.cs = cs; L.cg = cg;
-        L.scull = f.scull; L.s_list = f.list_s; L.g_list = f.list_g; L.sbin = bs; L.gbin = bg;
+        L.scull = f.scull; L.gcull = f.gcull; L.slabs = slabs; L.s_list = f.list_s; L.g_list = f.list_g; L.sbin = bs; L.gbin = bg;
         L.ds_in = f64->ds_in;
         L.out = *f64->out;
         L.records = f.rec64;

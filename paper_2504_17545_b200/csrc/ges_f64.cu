@@ -194,6 +194,10 @@ __global__ void k_gauss3_rec64(ges_scene_src_t src, int64_t ng, CamK cam, GaussC
     valid = valid && m2max > 0.0;
     double* r = rec + GREC3 * j;
     r[0] = valid ? 1.0 : 0.0;
+    // r[15]: exponent below which sig * exp(pw) < 1/255 beyond any rounding (a
+    // pre-screen only: the kept cases take the exact test)
+    const double lt = log(ALPHA_CUTOFF / fmax(sig, 1e-300));
+    r[15] = lt - 1e-9 * (1.0 + fabs(lt));
     r[1] = mx; r[2] = my;
     r[3] = c11 / det; r[4] = -c01 / det; r[5] = c00 / det;
     r[6] = sig; r[7] = t.z; r[8] = eps;
@@ -204,7 +208,6 @@ __global__ void k_gauss3_rec64(ges_scene_src_t src, int64_t ng, CamK cam, GaussC
     const dv3 nv = col_cam(R, k, cam);
     const double sg = dot3(nv, t) < 0.0 ? 1.0 : -1.0;
     r[12] = nv.x * sg; r[13] = nv.y * sg; r[14] = nv.z * sg;
-    r[15] = 0.0;
 }
 
 // ---------------------------------------------------------------- K4d: planar records
@@ -259,7 +262,9 @@ __global__ void k_gauss2_rec64(ges_scene_src_t src, int64_t ng, CamK cam, GaussC
     const double sg = nq < 0.0 ? 1.0 : -1.0;
     r[19] = n.x * sg; r[20] = n.y * sg; r[21] = n.z * sg;
     r[22] = valid ? 1.0 : 0.0;
-    r[23] = 0.0;
+    // r[23]: u^2 + v^2 beyond which sig * exp(-q/2) < 1/255 beyond any rounding (pre-screen)
+    const double qm = 2.0 * log(fmax(255.0 * sig, 1e-300));
+    r[23] = qm + 1e-9 * (1.0 + fabs(qm));
 }
 
 // ---------------------------------------------------------------- K6d: the tile
@@ -267,6 +272,7 @@ struct Tile64Args {
     int W, H, ntx, grid, mode, layers, gk, geom, deg;
     double bg[3];
     CamK cs, cg;                  // surfel-pass camera (scaled by grid) and base camera
+    SlabMap slabs;
     const double* srec;
     const float4* scull;
     const uint32_t* s_list;
@@ -274,6 +280,7 @@ struct Tile64Args {
     const int32_t* s_id;          // packed -> source surfel
     ges_scene_src_t src;
     const double* grec;
+    const float4* gcull;
     const uint32_t* g_list;
     BinPass gbin;
     const double* ds_in;          // mode 2: surfel depth (H, W)
@@ -281,10 +288,33 @@ struct Tile64Args {
     const ges_frame_status_t* status;
 };
 
+__device__ __forceinline__ double warp_max64(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ bool span_hits(uint32_t sx, uint32_t sy, int x0, int x1, int y0, int y1) {
+    return span_lo(sx) <= x1 && span_hi(sx) >= x0 && span_lo(sy) <= y1 && span_hi(sy) >= y0;
+}
+
+// Each warp (16 x 2 pixels of the tile) walks the tile's near-to-far lists 32
+// entries at a time: the lanes load the chunk's ids and float32 cull records
+// together; entries whose pixel range misses the warp's rows, or whose
+// conservative depth key lies behind every pixel's current best, are skipped
+// by the whole warp; the walk stops at the first slab behind all of the
+// warp's pixels.  That is the float32 path's culling (all bounds
+// conservative), so every float64 decision is still the per-pixel test's.
 template <int G>   // sub-samples per axis of the surfel pass (1, or 2 at supersample=4)
 __global__ void __launch_bounds__(256) k_tile64(Tile64Args a) {
+    __shared__ uint32_t s_end[NSLAB], g_end[NSLAB];
     if (a.status->overflow) return;
     const int tile = blockIdx.x;
+    for (int k = threadIdx.x; k < NSLAB; k += blockDim.x) {
+        if (a.mode & 1) s_end[k] = a.sbin.cnt[tile * NSLAB + k];
+        if (a.mode & 2) g_end[k] = a.gbin.cnt[tile * NSLAB + k];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wrow = 2 * (threadIdx.x >> 5);   // the warp's first tile row
     const int tx = tile % a.ntx, ty = tile / a.ntx;
     const int x = tx * TILE + (threadIdx.x & 15), y = ty * TILE + (threadIdx.x >> 4);
     const bool inside = x < a.W && y < a.H;
@@ -308,29 +338,54 @@ __global__ void __launch_bounds__(256) k_tile64(Tile64Args a) {
             dvec[s] = {((double)X + 0.5 - a.cs.cx) / a.cs.fx, ((double)Y + 0.5 - a.cs.cy) / a.cs.fy, 1.0};
             dn[s] = sqrt(dot3(dvec[s], dvec[s]));
         }
-        const uint32_t beg = a.sbin.tile_off(tile), end = beg + a.sbin.cnt[tile * NSLAB + NSLAB - 1];
-        for (uint32_t e = beg; inside && e < end; ++e) {
-            const uint32_t i = __ldg(a.s_list + e);
-            const float4 cr = __ldg(a.scull + i);
-            double worst = bt[0];
+        auto worst_of = [&]() {   // the thread's max best depth (-inf outside the image)
+            double wv = bt[0];
 #pragma unroll
-            for (int s = 1; s < G * G; ++s) worst = fmax(worst, bt[s]);
-            if ((double)cr.x > worst) continue;   // conservative disc depth behind every sample's best
-            const double* r = a.srec + SREC * (size_t)i;
-            if (r[14] == 0.0) continue;          // q_z <= NEAR
-            const dv3 n = {r[0], r[1], r[2]}, a1 = {r[3], r[4], r[5]}, a2 = {r[6], r[7], r[8]};
-            const int32_t sid = a.s_id[i];
+            for (int s = 1; s < G * G; ++s) wv = fmax(wv, bt[s]);
+            return inside ? wv : -INFINITY;
+        };
+        const int wx0 = tx * TILE * G, wx1 = wx0 + TILE * G - 1;   // the warp's rows in the sample grid
+        const int wy0 = (ty * TILE + wrow) * G, wy1 = wy0 + 2 * G - 1;
+        const uint32_t beg = a.sbin.tile_off(tile), end = beg + s_end[NSLAB - 1];
+        for (uint32_t e0 = beg; e0 < end; e0 += 32) {
+            const double wmax = warp_max64(worst_of());
+            if ((double)a.slabs.lower(slab_of_pos(s_end, e0 - beg, lane)) > wmax) break;
+            uint32_t id = 0;
+            float key = INFINITY;
+            bool live = false;
+            if (e0 + lane < end) {
+                id = __ldg(a.s_list + e0 + lane);
+                const float4 c = __ldg(a.scull + id);
+                key = c.x;
+                live = span_hits(__float_as_uint(c.y), __float_as_uint(c.z), wx0, wx1, wy0, wy1) &&
+                       !((double)key > wmax);
+            }
+            uint32_t vote = __ballot_sync(0xffffffffu, live);
+            while (vote) {
+                const int j = __ffs(vote) - 1;
+                vote &= vote - 1;
+                const uint32_t i = __shfl_sync(0xffffffffu, id, j);
+                const float kj = __shfl_sync(0xffffffffu, key, j);
+                if ((double)kj > worst_of()) continue;   // behind every sample's best (-inf: outside)
+                const double* r = a.srec + SREC * (size_t)i;
+                if (r[14] == 0.0) continue;              // q_z <= NEAR
+                const dv3 n = {r[0], r[1], r[2]}, a1 = {r[3], r[4], r[5]}, a2 = {r[6], r[7], r[8]};
+                const int32_t sid = a.s_id[i];
 #pragma unroll
-            for (int s = 0; s < G * G; ++s) {
-                const double ndot = dot3(n, dvec[s]);
-                const double th = r[9] / ndot;
-                const double u = (th * dot3(a1, dvec[s]) - r[10]) / r[12];
-                const double v = (th * dot3(a2, dvec[s]) - r[11]) / r[13];
-                const bool ok = fabs(ndot) > PARALLEL_EPS * dn[s] && th > NEAR && u * u + v * v <= R2;
-                if (ok && (th < bt[s] || (th == bt[s] && sid < bid[s]))) {
-                    bt[s] = th;
-                    bid[s] = sid;
-                    bpk[s] = i;
+                for (int s = 0; s < G * G; ++s) {
+                    const double ndot = dot3(n, dvec[s]);
+                    const double th = r[9] / ndot;
+                    // the reference's conditions (geometry.py:216-226, forward.py:183-187),
+                    // the depth comparison first: u, v only for samples it would win
+                    if (!(th < bt[s] || (th == bt[s] && sid < bid[s]))) continue;
+                    if (!(fabs(ndot) > PARALLEL_EPS * dn[s] && th > NEAR)) continue;
+                    const double u = (th * dot3(a1, dvec[s]) - r[10]) / r[12];
+                    const double v = (th * dot3(a2, dvec[s]) - r[11]) / r[13];
+                    if (u * u + v * v <= R2) {
+                        bt[s] = th;
+                        bid[s] = sid;
+                        bpk[s] = i;
+                    }
                 }
             }
         }
@@ -369,41 +424,61 @@ __global__ void __launch_bounds__(256) k_tile64(Tile64Args a) {
 
     // ---- pass 2: depth-gated float64 Gaussian sums (forward.py:248-381)
     double w = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, gd = 0.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
-    if ((a.mode & 2) && inside) {
-        const uint32_t beg = a.gbin.tile_off(tile), end = beg + a.gbin.cnt[tile * NSLAB + NSLAB - 1];
+    if (a.mode & 2) {
+        const uint32_t beg = a.gbin.tile_off(tile), end = beg + g_end[NSLAB - 1];
         const double px = (double)x + 0.5, py = (double)y + 0.5;
         const dv3 d = {(px - a.cg.cx) / a.cg.fx, (py - a.cg.cy) / a.cg.fy, 1.0};
         const double dn = sqrt(dot3(d, d));
-        for (uint32_t e = beg; e < end; ++e) {
-            const uint32_t j = __ldg(a.g_list + e);
-            if (a.gk == 3) {
-                const double* r = a.grec + GREC3 * (size_t)j;
-                if (r[0] == 0.0) continue;
-                const double dx = px - r[1], dy = py - r[2];
-                const double pw = -0.5 * (r[3] * dx * dx + r[5] * dy * dy) - r[4] * dx * dy;
-                const double al = r[6] * exp(pw);
-                if (al >= ALPHA_CUTOFF && r[7] < ds + r[8]) {
-                    w += al;
-                    cr += al * r[9]; cg += al * r[10]; cb += al * r[11];
-                    gd += al * r[7];
-                    n0 += al * r[12]; n1 += al * r[13]; n2 += al * r[14];
-                }
-            } else {
-                const double* r = a.grec + GREC2 * (size_t)j;
-                if (r[22] == 0.0) continue;
-                const dv3 n = {r[0], r[1], r[2]}, a1 = {r[3], r[4], r[5]}, a2 = {r[6], r[7], r[8]};
-                const double ndot = dot3(n, d);
-                const double th = r[9] / ndot;
-                const double u = (th * dot3(a1, d) - r[10]) / r[12];
-                const double v = (th * dot3(a2, d) - r[11]) / r[13];
-                const bool ok = fabs(ndot) > PARALLEL_EPS * dn && th > NEAR;
-                if (!ok) continue;
-                const double al = r[14] * exp(-0.5 * (u * u + v * v));
-                if (al >= ALPHA_CUTOFF && th < ds + r[15]) {
-                    w += al;
-                    cr += al * r[16]; cg += al * r[17]; cb += al * r[18];
-                    gd += al * th;
-                    n0 += al * r[19]; n1 += al * r[20]; n2 += al * r[21];
+        const double wdmax = warp_max64(inside ? ds : -INFINITY);
+        const int wx0 = tx * TILE, wx1 = wx0 + TILE - 1, wy0 = ty * TILE + wrow, wy1 = wy0 + 1;
+        for (uint32_t e0 = beg; e0 < end; e0 += 32) {
+            // keys (depth - eps) are binned near-to-far: the rest fail every gate of the warp
+            if ((double)a.slabs.lower(slab_of_pos(g_end, e0 - beg, lane)) > wdmax) break;
+            uint32_t id = 0;
+            bool live = false;
+            if (e0 + lane < end) {
+                id = __ldg(a.g_list + e0 + lane);
+                const float4 c = __ldg(a.gcull + id);
+                live = span_hits(__float_as_uint(c.z), __float_as_uint(c.w), wx0, wx1, wy0, wy1);
+            }
+            uint32_t vote = __ballot_sync(0xffffffffu, live);
+            while (vote) {
+                const int jl = __ffs(vote) - 1;
+                vote &= vote - 1;
+                const uint32_t j = __shfl_sync(0xffffffffu, id, jl);
+                if (!inside) continue;
+                if (a.gk == 3) {
+                    const double* r = a.grec + GREC3 * (size_t)j;
+                    if (r[0] == 0.0 || !(r[7] < ds + r[8])) continue;   // invalid, or fails the gate
+                    const double dx = px - r[1], dy = py - r[2];
+                    const double pw = -0.5 * (r[3] * dx * dx + r[5] * dy * dy) - r[4] * dx * dy;
+                    if (pw < r[15]) continue;   // far below the 1/255 cutoff: no exp needed
+                    const double al = r[6] * exp(pw);
+                    if (al >= ALPHA_CUTOFF) {
+                        w += al;
+                        cr += al * r[9]; cg += al * r[10]; cb += al * r[11];
+                        gd += al * r[7];
+                        n0 += al * r[12]; n1 += al * r[13]; n2 += al * r[14];
+                    }
+                } else {
+                    const double* r = a.grec + GREC2 * (size_t)j;
+                    if (r[22] == 0.0) continue;
+                    const dv3 n = {r[0], r[1], r[2]}, a1 = {r[3], r[4], r[5]}, a2 = {r[6], r[7], r[8]};
+                    const double ndot = dot3(n, d);
+                    const double th = r[9] / ndot;
+                    const bool ok = fabs(ndot) > PARALLEL_EPS * dn && th > NEAR;
+                    if (!ok || !(th < ds + r[15])) continue;
+                    const double u = (th * dot3(a1, d) - r[10]) / r[12];
+                    const double v = (th * dot3(a2, d) - r[11]) / r[13];
+                    const double q2 = u * u + v * v;
+                    if (q2 > r[23]) continue;   // far outside the 1/255 support: no exp needed
+                    const double al = r[14] * exp(-0.5 * q2);
+                    if (al >= ALPHA_CUTOFF) {
+                        w += al;
+                        cr += al * r[16]; cg += al * r[17]; cb += al * r[18];
+                        gd += al * th;
+                        n0 += al * r[19]; n1 += al * r[20]; n2 += al * r[21];
+                    }
                 }
             }
         }
@@ -482,7 +557,8 @@ cudaError_t launch_f64(const F64Launch& L, cudaStream_t s) {
     a.W = L.W; a.H = L.H; a.ntx = L.ntx; a.grid = L.grid; a.mode = L.mode; a.layers = L.layers;
     a.gk = L.gdim; a.geom = L.geom; a.deg = L.deg;
     for (int i = 0; i < 3; ++i) a.bg[i] = L.bg[i];
-    a.cs = L.cs; a.cg = L.cg;
+    a.cs = L.cs; a.cg = L.cg; a.slabs = L.slabs;
+    a.gcull = L.gcull;
     a.srec = srec; a.scull = L.scull; a.s_list = L.s_list; a.sbin = L.sbin; a.s_id = L.s_id; a.src = L.src;
     a.grec = grec; a.g_list = L.g_list; a.gbin = L.gbin;
     a.ds_in = L.ds_in;

@@ -110,9 +110,10 @@ struct F64Launch {
     double bg[3];
     int W, H, ntx, ntiles, grid;
     CamK cs, cg;
-    const float4* scull;
+    const float4 *scull, *gcull;
     const uint32_t *s_list, *g_list;
     BinPass sbin, gbin;
+    SlabMap slabs;
     const double* ds_in;
     ges_outputs_f64_t out;
     void* records;                // f64_record_bytes(ns, ng, gdim)
