@@ -53,11 +53,8 @@ __device__ unsigned long long g_stats[20];
 #ifndef GES_TILE_WPC1
 #define GES_TILE_WPC1 2  // 16x16-pixel tiles (40 registers: 24 two-warp CTAs per SM)
 #endif
-#ifndef GES_P1_PACK
-#define GES_P1_PACK 0    // pass 1 packs survivors x lane blocks 32 per step (shared z-buffer)
-#endif
 
-template <int WPC, int ZNS>   // ZNS: samples per thread in pass 1 (the packed z-buffer)
+template <int WPC>
 struct __align__(16) TileSmem {
     float4 st[4][32 * WPC];     // per-warp slots (32 each): pass-1 surfel coefficients, pass-2
                                 // Gaussian records, then the colour tasks
@@ -67,11 +64,6 @@ struct __align__(16) TileSmem {
                                 // 2 x 2 lanes (pass-1 culling)
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
     uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
-#if GES_P1_PACK
-    unsigned long long zb[32 * WPC][ZNS];   // per lane block: packed (depth bits, source id) per sample
-    float peb[32 * WPC];        // per lane block: its near-parallel threshold
-    uint8_t sv[32 * WPC];       // per warp: lane of the r-th survivor of the chunk
-#endif
 };
 
 // Lower depth bound of the slab holding relative list position `rel` (slab
@@ -294,7 +286,7 @@ template <int SS, int PX, int MODE, int GK, bool GEOM>
 __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, PX>()) k_tile(TileArgs a) {
     constexpr int G = SS * PX, NS = G * G, NP = PX * PX, TP = TILE * PX;
     constexpr int WPC = tile_wpc<SS, PX>(), TPB = 32 * WPC;
-    __shared__ TileSmem<WPC, NS> sm;
+    __shared__ TileSmem<WPC> sm;
     pdl_wait();   // (launched as a dependent of the fill: lists, offsets, status)
     if (a.status->overflow) return;   // pair lists incomplete: host re-renders
 #ifdef GES_TIMING   // warp lifetimes (tuning builds only, see read_stats / tools/tile_stats.py --timing)
@@ -364,15 +356,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 bt[gy * G + gx] = in ? INFINITY : 0.f;
             }
         pe = PARALLEL_EPS_F * sqrtf(pe + 1.0f);   // max over the samples of 1e-8 |d|
-#if GES_P1_PACK
-        // the z-buffer lives in shared memory while the survivors are packed
-        // across lanes: packed (depth bits << 32 | source id), min = argmin with
-        // lowest-id ties (positive depths order like their bits)
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-            sm.zb[threadIdx.x][s] = ((unsigned long long)__float_as_uint(bt[s]) << 32) | 0xffffffffull;
-        sm.peb[threadIdx.x] = pe;
-#endif
         // Depth culling bounds, refreshed after every chunk: the max over each
         // region of 2 x 2 lanes (one entry of sm.rmax) and over the whole
         // patch (wmx).  A single uncovered sample keeps its bound at +inf, so
@@ -418,9 +401,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             const uint32_t id = nid;   // this chunk's ids were loaded one chunk ahead
             if (e + 32 < end) nid = a.s_list[e + 32];
             bool live = false;
-#if GES_P1_PACK
-            int pk_w = 1, pk_c = 0, pk_o = 0;   // survivor: block-rect width, block count, first block
-#endif
             if (e < end) {
                 const float4 r3 = __ldg(a.scull + id);
                 const uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
@@ -446,14 +426,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                     sm.st[0][slot] = make_float4(d0, dx_, dy_, nq);
                     sm.st[1][slot] = make_float4(u0 * IR, r1.y * IR, r1.z * IR, v0 * IR);
                     sm.st[2][slot] = make_float4(r2.y * IR, r2.z * IR, r3.w, r3.x);   // r3.w: source id
-#if GES_P1_PACK
-                    // the lane blocks of the patch its pixel range covers
-                    const int cx0 = max(span_lo(sxr) - wx0, 0) / G, cx1 = min(span_hi(sxr) - wx0, PW - 1) / G;
-                    const int cy0 = max(span_lo(syr) - wy0, 0) / G, cy1 = min(span_hi(syr) - wy0, PH - 1) / G;
-                    pk_w = cx1 - cx0 + 1;
-                    pk_c = pk_w * (cy1 - cy0 + 1);
-                    pk_o = cx0 + 8 * cy0;
-#endif
                 }
             }
             uint32_t vote = __ballot_sync(0xffffffffu, live);
@@ -462,68 +434,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             if (lane == 0) { GES_STAT(0, 1); GES_STAT(1, min(32u, end - base)); GES_STAT(2, __popc(vote)); }
 #endif
             if (!vote) continue;     // nothing tested: the patch depth is unchanged
-#if GES_P1_PACK
-            {
-                // (survivor, lane block) pairs in survivor order, 32 per step: each
-                // lane tests the G x G samples of one block against one survivor
-                int incl = pk_c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                const int total = __shfl_sync(0xffffffffu, incl, 31), start = incl - pk_c;
-                if (live) sm.sv[wl * 32 + __popc(vote & ((1u << lane) - 1u))] = (uint8_t)lane;
-                // per survivor lane: first pair, block-rect origin and width, 1/width
-                const int info = pk_o | (pk_w << 8);
-                __syncwarp();
-                for (int P = 0; P < total; P += 32) {
-                    const int k = P + lane;
-                    const bool hs = live && start >= P && start < P + 32;
-                    const unsigned H = __reduce_or_sync(0xffffffffu, hs ? 1u << (start - P) : 0u);
-                    const int nb = __popc(__ballot_sync(0xffffffffu, live && start < P));
-                    const int r = nb + __popc(H & ((2u << lane) - 1u)) - 1;   // survivor rank of pair k
-                    const int ol = sm.sv[wl * 32 + min(max(r, 0), 31)];
-                    const int so = __shfl_sync(0xffffffffu, start, ol), io = __shfl_sync(0xffffffffu, info, ol);
-                    if (k >= total) continue;
-                    const int wo = io >> 8, b = k - so;
-                    const int byy = (int)(((float)b + 0.5f) * __frcp_rn((float)wo)), bxx = b - byy * wo;
-                    const int blk = (io & 0xff) + bxx + 8 * byy;   // lane index of the block in the patch
-                    const int j = wl * 32 + ol;
-                    const float4 A = sm.st[0][j], B = sm.st[1][j], C = sm.st[2][j];
-                    const float Awf = A.w * 0.99999f;
-                    const float bxl = (float)(G * ((warp & 1) * 8 + (blk & 7))), byl = (float)(G * ((warp >> 1) * 4 + (blk >> 3)));
-                    const float den0 = fmaf(A.z, byl, fmaf(A.y, bxl, A.x));
-                    const float U0 = fmaf(B.z, byl, fmaf(B.y, bxl, B.x));
-                    const float V0 = fmaf(C.y, byl, fmaf(C.x, bxl, B.w));
-                    const float peo = sm.peb[wl * 32 + blk];
-                    unsigned long long* zp = sm.zb[wl * 32 + blk];
-                    const uint32_t sid = __float_as_uint(C.z);
-#pragma unroll
-                    for (int gy = 0; gy < G; ++gy)
-#pragma unroll
-                        for (int gx = 0; gx < G; ++gx) {
-                            const int s = gy * G + gx;
-                            float den = den0, U = U0, V = V0;
-                            if (gx) { den = fmaf(A.y, (float)gx, den); U = fmaf(B.y, (float)gx, U); V = fmaf(C.x, (float)gx, V); }
-                            if (gy) { den = fmaf(A.z, (float)gy, den); U = fmaf(B.z, (float)gy, U); V = fmaf(C.y, (float)gy, V); }
-                            const float r2 = fmaf(U, U, V * V);
-                            const float bts = __uint_as_float((uint32_t)(zp[s] >> 32));
-                            if (r2 <= den * den && Awf <= bts * den) {
-                                const float t = A.w * rcp_ftz(den);   // 2 ulp: ties are flagged
-                                if (den > peo && t > NEAR_F)
-                                    atomicMin(zp + s, ((unsigned long long)__float_as_uint(t) << 32) | sid);
-                            }
-                        }
-                }
-                __syncwarp();
-#pragma unroll
-                for (int s = 0; s < NS; ++s) bt[s] = __uint_as_float((uint32_t)(sm.zb[threadIdx.x][s] >> 32));
-                wmx = patch_depth();
-                __syncwarp();   // the slots are rewritten by the next chunk
-                continue;
-            }
-#endif
             __syncwarp();
             while (vote) {
                 const int j = wl * 32 + __ffs(vote) - 1;
@@ -582,14 +492,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             wmx = patch_depth();
             __syncwarp();   // the slots are rewritten by the next chunk
         }
-#if GES_P1_PACK
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            const unsigned long long z = sm.zb[threadIdx.x][s];
-            bt[s] = __uint_as_float((uint32_t)(z >> 32));
-            bid[s] = (uint32_t)z;
-        }
-#endif
         // the winners' SH blocks are read at the end (deferred colour): find
         // their packed indices and start pulling them into L2 now, overlapping
         // the Gaussian pass
