@@ -403,7 +403,8 @@ def measure_config(cfg, dev, streams, steps=5, warmup=3):
     settings = G.RenderSettings(mip=(cfg == 4))
     ds = G.DeviceScene(scene, dev)
     rend = G.Renderer(dev)
-    vb = ViewBatchRenderer(rend, ds, cams, settings, want=() if cfg == 5 else ("image", "s_depth", "s_winner"),
+    vb = ViewBatchRenderer(rend, ds, cams, settings,
+                           want=("image_rgba8",) if cfg == 5 else ("image", "s_depth", "s_winner"),
                            streams=streams)
     for i, r in enumerate(vb.pool):
         for c, fr in list(zip(vb.cams, vb.frames))[i::len(vb.pool)]:
@@ -509,8 +510,10 @@ def run_gpu(args, rank, world, local_rank):
                       file=sys.stderr)
         else:
             gather_used = "peer"
-    want = (() if cfg == 5 else ("image", "s_depth", "s_winner")) + \
-        (("image_rgba8",) if world > 1 and sink is None else ())
+    # config 5 keeps only the RGBA8 frames (256 4K views); the others the float
+    # outputs (plus the RGBA8 send buffer of the NCCL gather at N > 1)
+    want = (("image_rgba8",) if cfg == 5 else ("image", "s_depth", "s_winner")) + \
+        (("image_rgba8",) if world > 1 and sink is None and cfg != 5 else ())
     rgba_out = sink.slots if sink is not None else None
     strip_pad = None
     if strips is not None and sink is None and world > 1:
@@ -664,8 +667,12 @@ def run_gpu(args, rank, world, local_rank):
             else:
                 # fp32 Gaussian sums may differ in the last bit between renders (atomic list
                 # order), which can move an 8-bit rounding by one step
-                dev_rgba = (vb.rgba[0] if torch.is_tensor(vb.rgba[0]) else
-                            sink.frames[0] if sink is not None and sink.frames is not None else None)
+                if vb.rgba is None:   # (N = 1: the step writes float frames only)
+                    dev_rgba = (vb.frames[0].image * 255.0 + 0.5).clamp(0, 255).to(torch.uint8)
+                    dev_rgba = torch.cat([dev_rgba, torch.full_like(dev_rgba[..., :1], 255)], dim=-1)
+                else:
+                    dev_rgba = (vb.rgba[0] if torch.is_tensor(vb.rgba[0]) else
+                                sink.frames[0] if sink is not None and sink.frames is not None else None)
                 if dev_rgba is not None:   # (ranks > 0 of the peer gather hold no local frame copy)
                     dif = (host[0].int() - dev_rgba.cpu().int()).abs().max().item()
                     assert dif <= 1, f"e2e RGBA8 frame differs from device render by {dif}"

@@ -242,9 +242,9 @@ int ges_peer_free(void *dev_ptr);
 int ges_peer_open(const void *ipc_handle, int32_t device, void **dev_ptr);
 int ges_peer_close(void *dev_ptr);
 
-/* Tile-kernel work counters (20 x u64), then reset.  All zero unless the
+/* Tile-kernel work counters (24 x u64), then reset.  All zero unless the
  * library was built with -DGES_STATS (tuning builds only; synchronous). */
-int ges_debug_stats(uint64_t *out20);
+int ges_debug_stats(uint64_t *out24);
 
 /* ------------------------------------------------------------------ training
  * Joint-stage training step of the reference (training.py:358-392 frozen

@@ -663,9 +663,9 @@ int ges_peer_close(void* dev_ptr) {
     return e == cudaSuccess ? GES_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
-int ges_debug_stats(uint64_t* out20) {
-    if (!out20) return fail(GES_EINVAL, "NULL argument");
-    if (read_stats(reinterpret_cast<unsigned long long*>(out20))) return fail(GES_ECUDA, "stats copy failed");
+int ges_debug_stats(uint64_t* out24) {
+    if (!out24) return fail(GES_EINVAL, "NULL argument");
+    if (read_stats(reinterpret_cast<unsigned long long*>(out24))) return fail(GES_ECUDA, "stats copy failed");
     return GES_OK;
 }
 

@@ -214,8 +214,11 @@ __device__ __forceinline__ void fill_one(bool live, uint32_t id, uint32_t sx, ui
                 toff_r[r] = p.tile_off(tile);
                 if (lane == (unsigned)(__ffs(peers) - 1))
                     base_r[r] = atomicAdd(p.cnt + key, (uint32_t)__popc(peers));
-                if (++tx > tx1) { tx = tx0; if (++ty > ty1) more = false; }
             }
+            const bool wrap = tx >= tx1;   // next tile, row-major over the range (branch-free)
+            tx = wrap ? tx0 : tx + 1;
+            ty += wrap;
+            more = more && !(wrap && ty > ty1);
         }
     }
 #pragma unroll

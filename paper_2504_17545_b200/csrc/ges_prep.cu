@@ -80,7 +80,7 @@ __device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1,
         x0 = 0; x1 = c.W - 1; y0 = 0; y1 = c.H - 1;
         return c.W > 0 && c.H > 0;
     }
-    const float iA = 1.0f / A, iz = 1.0f / qz;
+    const float iA = rcp_ftz(A), iz = rcp_ftz(qz);   // (1 ulp: inside the padding)
     float lo[2], hi[2];
 #pragma unroll
     for (int ax = 0; ax < 2; ++ax) {
@@ -126,9 +126,10 @@ __device__ __forceinline__ void count_tiles(uint32_t* cnt, const Grid& g, bool l
         int key = more ? (ty * g.ntx + tx) * NSLAB + slab : -1;
         unsigned peers = __match_any_sync(0xffffffffu, key);
         if (more && lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(cnt + key, (uint32_t)__popc(peers));
-        if (more) {
-            if (++tx > tx1) { tx = tx0; if (++ty > ty1) more = false; }
-        }
+        const bool wrap = tx >= tx1;   // next tile, row-major over the range (branch-free)
+        tx = wrap ? tx0 : tx + 1;
+        ty += wrap;
+        more = more && !(wrap && ty > ty1);
     }
 }
 
@@ -140,18 +141,28 @@ __device__ __forceinline__ float4 affine_of(d3 v, const CamK& c, int xr, int yr,
     return make_float4((float)c0, (float)cx, (float)cy, last);
 }
 
+// 1/x of a positive normal x to float64 accuracy without the IEEE division's
+// slow path: the float32 estimate (rel. error < 2^-22) refined by two Newton
+// steps (error squared each), a few float64 ulp.
+__device__ __forceinline__ double rcp_pos(double x) {
+    double r = (double)rcp_ftz((float)x);
+    r = fma(r, fma(-x, r, 1.0), r);
+    return fma(r, fma(-x, r, 1.0), r);
+}
+
 __device__ __forceinline__ void planar_coeffs(d3 q, d3 a1, d3 a2, d3 n, double s1, double s2,
                                               const CamK& c, int x0, int x1, int y0, int y1,
                                               float4& r0, float4& r1, float4& r2) {
     double nq = dot(n, q);
-    d3 cu = scl(sub(scl(a1, nq), scl(n, dot(a1, q))), 1.0 / s1);
-    d3 cv = scl(sub(scl(a2, nq), scl(n, dot(a2, q))), 1.0 / s2);
+    d3 cu = scl(sub(scl(a1, nq), scl(n, dot(a1, q))), rcp_pos(s1));
+    d3 cv = scl(sub(scl(a2, nq), scl(n, dot(a2, q))), rcp_pos(s2));
     int xr = x0, yr = y0;
-    if (q.z > 0.0) {
-        const double iz = 1.0 / q.z;   // reference pixel of the coefficients: any pixel works
-        double mx = c.fx * q.x * iz + c.cx, my = c.fy * q.y * iz + c.cy;
-        xr = (int)fmin(fmax(floor(mx), (double)x0), (double)x1);
-        yr = (int)fmin(fmax(floor(my), (double)y0), (double)y1);
+    if (q.z > 0.0) {   // reference pixel of the coefficients: any pixel of the range works
+        const float iz = rcp_ftz((float)q.z);
+        const float mx = fmaf((float)c.fx * (float)q.x, iz, (float)c.cx);
+        const float my = fmaf((float)c.fy * (float)q.y, iz, (float)c.cy);
+        xr = mx >= (float)x1 ? x1 : (mx > (float)x0 ? (int)mx : x0);   // clamp(floor(mx), x0, x1)
+        yr = my >= (float)y1 ? y1 : (my > (float)y0 ? (int)my : y0);
     }
     r0 = affine_of(n, c, xr, yr, (float)nq);
     r1 = affine_of(cu, c, xr, yr, (float)xr);
@@ -245,7 +256,9 @@ __global__ void __launch_bounds__(256, GES_PREP_MINB) k_surfel_prep(ges_scene_t 
     if (alive) alive = disc_ranges(q, scl(a1, s1 * R_OPAQUE), scl(a2, s2 * R_OPAQUE), cam, x0, x1, y0, y1);
     // nearest camera depth of the disc, made conservative against the float32
     // evaluation of the per-pixel hit depth (culling and slab key only)
-    double zmin = q.z - R_OPAQUE * sqrt(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z);
+    // (float32 radius, rounded up by 1e-6 relative: the bound stays conservative)
+    const float rz = sqrtf((float)(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z)) * (float)(R_OPAQUE * (1.0 + 1e-6));
+    double zmin = q.z - (double)rz;
     zmin -= 1e-5 * fabs(zmin) + 1e-6;
     const float zkey = (float)zmin;
     count_tiles(o.bin_count, g, alive, x0, x1, y0, y1, zkey);

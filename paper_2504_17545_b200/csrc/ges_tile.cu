@@ -36,7 +36,7 @@ namespace ges {
 // a live warp mask, 3 surfel warp tests, 4 candidate lanes, 5 Gaussian
 // batches, 6 Gaussian entries staged, 7 staged with a live mask, 8 Gaussian
 // warp tests, 9 contributing lanes, 10 tiles, 11 tiles with uncovered pixels.
-__device__ unsigned long long g_stats[20];
+__device__ unsigned long long g_stats[24];
 #ifdef GES_STATS
 #define GES_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 #else
@@ -116,7 +116,7 @@ __device__ __forceinline__ float3 im_of(const TileArgs& a, float3 cs, float w, f
         }
         return make_float3(a.bg[0], a.bg[1], a.bg[2]);
     }
-    const float r = __frcp_rn(1.0f + w);
+    const float r = rcp_ftz(1.0f + w);   // (1 + w >= 1: the approximate reciprocal is within 1 ulp)
     return make_float3((cs.x + cr) * r, (cs.y + cg) * r, (cs.z + cb) * r);
 }
 
@@ -303,7 +303,11 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
     const int cta = blockIdx.y * gridDim.x + blockIdx.x;
     const int warp = (cta % (NWARP / WPC)) * WPC + wl;
     const int tile = a.order ? (int)__ldg(a.order + cta / (NWARP / WPC)) : cta / (NWARP / WPC);
-    const int tx = tile % a.ntx, ty = tile / a.ntx;
+    // tile / ntx without the integer division: (tile + 0.5) / ntx is >= 0.5 / ntx
+    // away from an integer, beyond the float quotient's error (2 ulp of <= nty)
+    // while ntx * nty < 2^21 tiles
+    const int ty = a.ntx * a.nty < (1 << 21) ? (int)__fdividef((float)tile + 0.5f, (float)a.ntx) : tile / a.ntx;
+    const int tx = tile - ty * a.ntx;
     const int plx = (warp & 1) * 8 + (lane & 7), ply = (warp >> 1) * 4 + (lane >> 3);
     const int bx = tx * TP + PX * plx, by = ty * TP + PX * ply;   // first base pixel of the thread
 
@@ -406,6 +410,10 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 const uint32_t sxr = __float_as_uint(r3.y), syr = __float_as_uint(r3.z);
                 live = span_lo(sxr) < wx0 + PW && span_hi(sxr) >= wx0 && span_lo(syr) < wy0 + PH &&
                        span_hi(syr) >= wy0 && !(r3.x > wmx);
+#ifdef GES_STATS
+                if (span_lo(sxr) < wx0 + PW && span_hi(sxr) >= wx0 && span_lo(syr) < wy0 + PH && span_hi(syr) >= wy0)
+                    GES_STAT(17, 1);
+#endif
                 // nearest disc depth vs the regions its pixel range overlaps
                 if (live) live = !(r3.x > region_max<2 * G>(sm.rmax[wl], span_lo(sxr) - wx0, span_hi(sxr) - wx0,
                                                             span_lo(syr) - wy0, span_hi(syr) - wy0));
@@ -426,6 +434,9 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                     sm.st[0][slot] = make_float4(d0, dx_, dy_, nq);
                     sm.st[1][slot] = make_float4(u0 * IR, r1.y * IR, r1.z * IR, v0 * IR);
                     sm.st[2][slot] = make_float4(r2.y * IR, r2.z * IR, r3.w, r3.x);   // r3.w: source id
+#ifdef GES_STATS
+                    sm.st[3][slot] = make_float4(r3.y, r3.z, 0.f, 0.f);   // spans (work counters only)
+#endif
                 }
             }
             uint32_t vote = __ballot_sync(0xffffffffu, live);
@@ -442,6 +453,16 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
                 if (lane == 0) GES_STAT(3, 1);
                 if (lane == 0) GES_STAT(12, wmx == INFINITY);
+#ifdef GES_STATS
+                if (lane == 0) {   // survivor's pixel range within one x half / y half / quadrant of the patch
+                    const float4 S = sm.st[3][j];
+                    const uint32_t sxr = __float_as_uint(S.x), syr = __float_as_uint(S.y);
+                    const int ax0 = max(span_lo(sxr) - wx0, 0), ax1 = min(span_hi(sxr) - wx0, PW - 1);
+                    const int ay0 = max(span_lo(syr) - wy0, 0), ay1 = min(span_hi(syr) - wy0, PH - 1);
+                    const bool xh = (ax0 / (PW / 2)) == (ax1 / (PW / 2)), yh = (ay0 / (PH / 2)) == (ay1 / (PH / 2));
+                    GES_STAT(20, xh); GES_STAT(21, yh); GES_STAT(22, xh && yh);
+                }
+#endif
                 GES_TM(++tm_t1);
                 const float4 A = sm.st[0][j], B = sm.st[1][j];
                 const float Awf = A.w * 0.99999f;   // candidate filter t <= 1.00001 bt (margin vs rounding)
@@ -603,6 +624,11 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                     live = span_lo(sxr) - ox <= px0 + 8 * PX - 1 && span_hi(sxr) - ox >= px0 &&
                            span_lo(syr) - oy <= py0 + 4 * PX - 1 && span_hi(syr) - oy >= py0 &&
                            c.x < wdmax + c.y;
+#ifdef GES_STATS
+                    if (span_lo(sxr) - ox <= px0 + 8 * PX - 1 && span_hi(sxr) - ox >= px0 &&
+                        span_lo(syr) - oy <= py0 + 4 * PX - 1 && span_hi(syr) - oy >= py0)
+                        GES_STAT(18, 1);
+#endif
                     if (live) {
                         const float4 r0 = __ldg(&r->r0), r1 = __ldg(&r->r1), r2 = __ldg(&r->r2);
                         v[0] = (r0.x - (float)ox) + (r0.y - 0.5f);   // mean relative to the tile
@@ -644,7 +670,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             uint32_t vote = __ballot_sync(0xffffffffu, live);
             GES_TM(++tm_b2);
             GES_TM(tm_t2 += __popc(vote));
-            if (lane == 0) { GES_STAT(6, min(32u, gend - base)); GES_STAT(7, __popc(vote)); }
+            if (lane == 0) { GES_STAT(6, min(32u, gend - base)); GES_STAT(7, __popc(vote)); GES_STAT(19, 1); }
             __syncwarp();
             while (vote) {
                 const int j = __ffs(vote) - 1;
@@ -889,7 +915,7 @@ __global__ void k_smooth(const float* __restrict__ sd, const float* __restrict__
 
 int read_stats(unsigned long long* out) {
     if (cudaMemcpyFromSymbol(out, g_stats, sizeof(g_stats)) != cudaSuccess) return 1;
-    unsigned long long z[20] = {};
+    unsigned long long z[24] = {};
     return cudaMemcpyToSymbol(g_stats, z, sizeof(z)) == cudaSuccess ? 0 : 1;
 }
 

@@ -251,7 +251,12 @@ class ViewBatchRenderer:
         shapes = {(int(c.height), int(c.width)) for c in self.cams}
         dev = renderer.device
         self.frames = []
-        if rgba_out is not None:
+        # RGBA8 frames only when asked for (or given a destination): the
+        # float outputs alone are the reference's RenderResult
+        if rgba_out is None and "image_rgba8" not in want:
+            bufs = [None] * len(self.cams)
+            self.rgba = None
+        elif rgba_out is not None:
             if len(rgba_out) != len(self.cams):
                 raise ValueError("one RGBA8 destination per view")
             self.rgba = bufs = list(rgba_out)

@@ -20,7 +20,9 @@ NAMES = ["surfel batches", "surfel entries staged", "  with live mask", "surfel 
          "candidate lanes", "gauss batches", "gauss entries walked (x warps)", "  surviving the warp cull",
          "gauss warp tests", "contributing lanes", "tiles", "tiles with uncovered px",
          "surfel warp tests at wmx=inf", "sample tests: not covered", "sample tests: covered",
-         "  covered, sample still empty", "surfel warp tests covering no sample", "-", "-", "-"]
+         "  covered, sample still empty", "surfel warp tests covering no sample", "surfel entries in the warp patch (range)",
+         "gauss entries in the warp patch (range)", "gauss batches (chunk iterations)",
+         "surfel tests: range in one x half", "surfel tests: range in one y half", "surfel tests: range in one quadrant", "-"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
@@ -33,7 +35,7 @@ ds = G.DeviceScene(sc)
 r = G.Renderer()
 st = G.RenderSettings(supersample=a.ss)
 fr = r.render(ds, cam, st, check=True)
-buf = (C.c_uint64 * 20)()
+buf = (C.c_uint64 * 24)()
 _lib.lib().ges_debug_stats(buf)            # reset after the sizing render
 fr = r.render(ds, cam, st, check=True)
 torch.cuda.synchronize()
