@@ -37,6 +37,14 @@ __device__ __forceinline__ float rcp_ftz(float x) {
     return y;
 }
 
+// sqrt on the SFU (approximate, relative error ~2^-22, sqrt(0) = 0); for
+// bounds and thresholds that carry their own margins
+__device__ __forceinline__ float sqrt_ftz(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Camera in the form the kernels use (double for per-primitive math).
 struct CamK {
     double fx, fy, cx, cy;

@@ -88,7 +88,7 @@ __device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1,
         const float s0 = (float)(ax ? q.y : q.x) * iz;
         const float w1 = fmaf(-s0, m1z, (float)(ax ? m1.y : m1.x)), w2 = fmaf(-s0, m2z, (float)(ax ? m2.y : m2.x));
         const float B = fmaf(w1, m1z, w2 * m2z), Cw = fmaf(w1, w1, w2 * w2);
-        const float root = sqrtf(fmaxf(fmaf(B, B, A * Cw), 0.f));
+        const float root = sqrt_ftz(fmaxf(fmaf(B, B, A * Cw), 0.f));
         const float dlo = (-B - root) * iA, dhi = (-B + root) * iA;
         const float clo = fmaf(f, s0 + dlo, cc), chi = fmaf(f, s0 + dhi, cc);
         const float pad = PAD_PX + 1e-6f * (fabsf(clo) + fabsf(chi));
@@ -256,8 +256,8 @@ __global__ void __launch_bounds__(256, GES_PREP_MINB) k_surfel_prep(ges_scene_t 
     if (alive) alive = disc_ranges(q, scl(a1, s1 * R_OPAQUE), scl(a2, s2 * R_OPAQUE), cam, x0, x1, y0, y1);
     // nearest camera depth of the disc, made conservative against the float32
     // evaluation of the per-pixel hit depth (culling and slab key only)
-    // (float32 radius, rounded up by 1e-6 relative: the bound stays conservative)
-    const float rz = sqrtf((float)(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z)) * (float)(R_OPAQUE * (1.0 + 1e-6));
+    // (float32 radius, rounded up by 2e-6 relative: the bound stays conservative)
+    const float rz = sqrt_ftz((float)(s1 * s1 * a1.z * a1.z + s2 * s2 * a2.z * a2.z)) * (float)(R_OPAQUE * (1.0 + 2e-6));
     double zmin = q.z - (double)rz;
     zmin -= 1e-5 * fabs(zmin) + 1e-6;
     const float zkey = (float)zmin;
@@ -326,7 +326,7 @@ __device__ __forceinline__ float3 gauss_view_colour(const ges_scene_t& sc, const
                                                     GaussShSmem<DEG>& sm) {
     // (the colour is evaluated in float32: the direction is too)
     const float dx = (float)(cam.pos[0] - p.x), dy = (float)(cam.pos[1] - p.y), dz = (float)(cam.pos[2] - p.z);
-    const float inv = 1.0f / fmaxf(sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))), 1e-12f);
+    const float inv = rsqrtf(fmaxf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), 1e-24f));   // (2 ulp)
     const int w = threadIdx.x >> 5;
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31u);
     if constexpr (sh_bulk_ok<DEG>()) {
@@ -379,9 +379,10 @@ __global__ void __launch_bounds__(GPREP_T, GES_GPREP_MINB) k_gauss3_prep(ges_sce
     // m2max = 2 ln(max(255 sig, 1e-12)) > 0  <=>  255 sig > 1 (exactly, ln is monotone with
     // ln 1 = 0); the support box only culls, so its radius is evaluated in float32 and widened
     valid = valid && 255.0 * sig > 1.0;
-    const float m2 = fmaxf(2.0f * logf((float)(255.0 * sig)), 0.f) * 1.0001f + 1e-6f;
-    const double rx = (double)(sqrtf(m2 * (float)c00) * 1.0001f) + 1e-3;
-    const double ry = (double)(sqrtf(m2 * (float)c11) * 1.0001f) + 1e-3;
+    // (__logf: absolute error < 4e-7 near 1, relative 2^-21 elsewhere; inside the widening)
+    const float m2 = fmaxf(2.0f * __logf((float)(255.0 * sig)), 0.f) * 1.0001f + 4e-6f;
+    const double rx = (double)(sqrt_ftz(m2 * (float)c00) * 1.0001f) + 1e-3;
+    const double ry = (double)(sqrt_ftz(m2 * (float)c11) * 1.0001f) + 1e-3;
     double mx = cam.fx * ts.x * iz + cam.cx, my = cam.fy * ts.y * iz + cam.cy;
     GaussRec rec;
     int x0 = 0, x1 = -1, y0 = 0, y1 = -1;

@@ -111,8 +111,8 @@ __device__ __forceinline__ float warp_max(float v) {
 __device__ __forceinline__ float3 im_of(const TileArgs& a, float3 cs, float w, float cr, float cg, float cb) {
     if (a.layers == GES_LAYERS_GAUSSIANS_ONLY) {
         if (w > 0.f) {
-            float dn = fmaxf(w, 1e-12f);
-            return make_float3(cr / dn, cg / dn, cb / dn);
+            const float r = rcp_ftz(fmaxf(w, 1e-12f));   // (1 ulp)
+            return make_float3(cr * r, cg * r, cb * r);
         }
         return make_float3(a.bg[0], a.bg[1], a.bg[2]);
     }
@@ -184,7 +184,7 @@ static __device__ __noinline__ float3 surfel_color_eval(const float* __restrict_
                                                         int deg, float cx, float cy, float cz, uint32_t pidx) {
     const float4 p = __ldg(pos + pidx);
     const float dx = cx - p.x, dy = cy - p.y, dz = cz - p.z;   // |d| ~ scene distance: fp32 is ample
-    const float inv = 1.0f / fmaxf(sqrtf(dx * dx + dy * dy + dz * dz), 1e-12f);
+    const float inv = rsqrtf(fmaxf(dx * dx + dy * dy + dz * dz, 1e-24f));   // (2 ulp)
     const int K3 = (deg + 1) * (deg + 1) * 3;
     return sh_color_dyn(deg, sh + (size_t)pidx * K3, dx * inv, dy * inv, dz * inv);
 }
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 const bool in = bx + gx / SS < a.W && by + gy / SS < a.H;
                 bt[gy * G + gx] = in ? INFINITY : 0.f;
             }
-        pe = PARALLEL_EPS_F * sqrtf(pe + 1.0f);   // max over the samples of 1e-8 |d|
+        pe = PARALLEL_EPS_F * sqrt_ftz(pe + 1.0f);   // max over the samples of 1e-8 |d|
         // Depth culling bounds, refreshed after every chunk: the max over each
         // region of 2 x 2 lanes (one entry of sm.rmax) and over the whole
         // patch (wmx).  A single uncovered sample keeps its bound at +inf, so
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             if constexpr (GK == 2) {
                 const float dxn = ((float)(bx + p % PX) + 0.5f - a.gcx) * a.gifx;
                 const float dyn = ((float)(by + p / PX) + 0.5f - a.gcy) * a.gify;
-                pe[p] = PARALLEL_EPS_F * sqrtf(dxn * dxn + dyn * dyn + 1.0f);
+                pe[p] = PARALLEL_EPS_F * sqrt_ftz(dxn * dxn + dyn * dyn + 1.0f);
             }
         }
         const int ox = tx * TP, oy = ty * TP;
