@@ -10,10 +10,10 @@
 #include "ges_sh.cuh"
 
 #ifndef GES_PREP_MINB
-#define GES_PREP_MINB 3   // resident 256-thread blocks per SM of the surfel preprocess
+#define GES_PREP_MINB 5   // resident 256-thread blocks per SM of the surfel preprocess (48 registers)
 #endif
 #ifndef GES_GPREP_MINB
-#define GES_GPREP_MINB (2 * GES_PREP_MINB)   // resident 128-thread blocks per SM, Gaussian preprocess
+#define GES_GPREP_MINB 6   // resident 128-thread blocks per SM, Gaussian preprocess
 #endif
 
 namespace ges {
