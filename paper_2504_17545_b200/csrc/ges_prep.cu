@@ -13,7 +13,7 @@
 #define GES_PREP_MINB 5   // resident 256-thread blocks per SM of the surfel preprocess (48 registers)
 #endif
 #ifndef GES_GPREP_MINB
-#define GES_GPREP_MINB 6   // resident 128-thread blocks per SM, Gaussian preprocess
+#define GES_GPREP_MINB 7   // resident 128-thread blocks per SM, Gaussian preprocess (72 registers)
 #endif
 
 namespace ges {
