@@ -230,10 +230,12 @@ class PeerFrameGather:
 
 class ViewBatchRenderer:
     """Renders a batch of views of one packed scene, asynchronously on the
-    current stream, into preallocated outputs: a (V, H, W, 4) RGBA8 send
-    buffer when all views share one resolution (a list of (H, W, 4) buffers
-    otherwise, e.g. the multi-scale Mip views), plus any other requested
-    buffers (fp32 image, depth, winner ...)."""
+    current stream, into preallocated outputs: the requested buffers (fp32
+    image, depth, winner ...) and, when ``"image_rgba8"`` is requested or
+    ``rgba_out`` is given, a (V, H, W, 4) RGBA8 send buffer when all views
+    share one resolution (a list of (H, W, 4) buffers otherwise, e.g. the
+    multi-scale Mip views); without either, ``rgba`` is None and no RGBA8
+    frame is written."""
 
     def __init__(self, renderer, scene, cams, settings, *, want=("image_rgba8",), streams: int = 1,
                  rgba_out=None):
