@@ -456,8 +456,9 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
             while (vote) {
                 const int j = wl * 32 + __ffs(vote) - 1;
                 vote &= vote - 1;
+                // (no depth re-check here: wmx only changes between chunks, and the
+                // staging already required the disc's nearest depth <= wmx)
                 const float4 C = sm.st[2][j];
-                if (C.w > wmx) continue;   // disc entirely behind every hit of the patch
                 if (lane == 0) GES_STAT(3, 1);
                 if (lane == 0) GES_STAT(12, wmx == INFINITY);
 #ifdef GES_STATS
