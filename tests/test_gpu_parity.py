@@ -363,6 +363,33 @@ def test_view_batch_streams_and_graph_match_single_renders():
         assert np.abs(rgba[..., :3].cpu().numpy().astype(np.int32) - q).max() <= 1
 
 
+def test_view_batch_float_outputs_only():
+    """Without "image_rgba8" (the N = 1 bench batch) no RGBA8 frame exists and
+    the float outputs are those of single renders."""
+    from paper_2504_17545_b200.multiview import ViewBatchRenderer
+    from paper_2504_17545_b200.renderer import DeviceScene, Renderer
+    sc = S.random_scene(np.random.default_rng(11), 2000, 800, degree=3)
+    cams = S.orbit_views(4, 128, 96)
+    ds = DeviceScene(sc)
+    st = G.RenderSettings()
+    vb = ViewBatchRenderer(Renderer(), ds, cams, st, want=("image", "s_depth", "s_winner"), streams=2)
+    assert vb.rgba is None and all(fr.image_rgba8 is None for fr in vb.frames)
+    for rr in vb.pool:
+        for c, fr in zip(vb.cams, vb.frames):
+            rr.render(ds, c, st, frame=fr, check=True)
+    assert vb.capture()
+    assert vb.render() is None
+    torch.cuda.synchronize()
+    assert not vb.overflowed()
+    for c, fr in zip(cams, vb.frames):
+        ref = G.render(sc, c)
+        assert np.array_equal(fr.s_winner.cpu().numpy(), ref.surfels.winner)
+        assert np.max(np.abs(fr.image.cpu().numpy() - ref.image)) <= 1e-6
+        d, rd = fr.s_depth.cpu().numpy(), ref.surfels.depth
+        assert np.array_equal(np.isinf(d), np.isinf(rd))
+        assert np.max(np.abs(d - rd)[np.isfinite(rd)]) <= 1e-6 * max(1.0, np.abs(rd[np.isfinite(rd)]).max())
+
+
 def _tile_region(cam, tiles):
     region = np.zeros((cam.height, cam.width), bool)
     for ti in tiles:
