@@ -93,7 +93,7 @@ typedef struct ges_scene {
     float *g_pos_op;      /* n_gaussians x 4: pos.xyz, eff_opacity             */
     float *g_quat;        /* n_gaussians x 4                                   */
     float *g_scale_eps;   /* n_gaussians x 4: eff_scale (s2=0 for 2D), epsilon */
-    float *g_sh;          /* n_gaussians x K x 3                               */
+    float *g_sh;          /* n_gaussians rows of 3K floats padded to 4, 12, 28, 52 floats (deg 0-3) */
     double bounds[7];     /* copied from ges_scene_src_t::bounds               */
 } ges_scene_t;
 

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "ges_launch.h"
+#include "ges_sh.cuh"
 
 using namespace ges;
 
@@ -349,7 +350,7 @@ size_t ges_scene_bytes(int64_t ns, int64_t ng, int32_t deg) {
     if (deg < 0 || deg > 3 || ns < 0 || ng < 0) return 0;
     size_t K = (size_t)(deg + 1) * (deg + 1);
     return al(ns * 16) + al(ns * 16) + al(ns * 4) + al(ns * K * 12) + al(ns * 4) * 2 + al(ng * 16) * 3 +
-           al(ng * K * 12);
+           al(ng * gsh_stride(deg) * 4);
 }
 
 int ges_scene_pack(const ges_scene_src_t* src, void* blob, size_t blob_bytes, ges_scene_t* out, void* stream) {
@@ -374,7 +375,7 @@ int ges_scene_pack(const ges_scene_src_t* src, void* blob, size_t blob_bytes, ge
     sc.g_pos_op = c.take<float>(ng * 4);
     sc.g_quat = c.take<float>(ng * 4);
     sc.g_scale_eps = c.take<float>(ng * 4);
-    sc.g_sh = c.take<float>(ng * K * 3);
+    sc.g_sh = c.take<float>(ng * gsh_stride(src->sh_degree));   // rows padded (ges_sh.cuh gsh_stride)
     cudaError_t e = launch_pack(*src, sc, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "scene pack");
     *out = sc;

@@ -211,14 +211,15 @@ __global__ void k_pack_prims(ges_scene_src_t src, ges_scene_t dst) {
     }
 }
 
-// Row-permuted float64 -> float32 copy of the (N, K*3) SH blocks.
-__global__ void k_pack_sh(const double* __restrict__ a, float* __restrict__ b, int64_t n, int row,
+// Row-permuted float64 -> float32 copy of the (N, K*3) SH blocks into rows of
+// `stride` floats (zero padding after the K*3 coefficients).
+__global__ void k_pack_sh(const double* __restrict__ a, float* __restrict__ b, int64_t n, int row, int stride,
                           const int32_t* __restrict__ order) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t r = i / row, c = i - r * row;
+        int64_t r = i / stride, c = i - r * stride;
         int64_t src = order ? (int64_t)order[r] : r;
-        b[i] = (float)a[src * row + c];
+        b[i] = c < row ? (float)a[src * row + c] : 0.f;
     }
 }
 
@@ -226,10 +227,11 @@ cudaError_t launch_pack(const ges_scene_src_t& src, const ges_scene_t& dst, cuda
     int64_t n = src.n_surfels > src.n_gaussians ? src.n_surfels : src.n_gaussians;
     if (n > 0) k_pack_prims<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, dst);
     int K = (src.sh_degree + 1) * (src.sh_degree + 1);
+    const int gs = gsh_stride(src.sh_degree);   // Gaussian rows padded for the preprocess's bulk copies
     if (src.n_surfels)
-        k_pack_sh<<<1184, 256, 0, s>>>(src.s_sh, dst.s_sh, src.n_surfels * K * 3, K * 3, src.s_order);
+        k_pack_sh<<<1184, 256, 0, s>>>(src.s_sh, dst.s_sh, src.n_surfels * K * 3, K * 3, K * 3, src.s_order);
     if (src.n_gaussians)
-        k_pack_sh<<<1184, 256, 0, s>>>(src.g_sh, dst.g_sh, src.n_gaussians * K * 3, K * 3, src.g_order);
+        k_pack_sh<<<1184, 256, 0, s>>>(src.g_sh, dst.g_sh, src.n_gaussians * gs, K * 3, gs, src.g_order);
     return cudaGetLastError();
 }
 
@@ -296,31 +298,27 @@ struct GaussCfg {
     float eps_value;
 };
 
-// Gaussian preprocess blocks: 128 threads (4 warps) so the warps' shared
-// coefficient slices of sh_color_warp fit the static shared-memory limit.
+// Gaussian preprocess blocks: 128 threads (4 warps).
 constexpr int GPREP_T = 128;
 
-// View colour of this lane's Gaussian (forward.py:99-109) with the warp's
-// coefficient blocks loaded coalesced (sh_color_warp); all lanes call it.
-// Shared state of the warp's SH fetch: TMA rows + mbarrier (degrees 1, 3) or
-// the coalesced-load slice of sh_color_warp (degrees 0, 2).
+// Shared state of the warp's SH fetch: its 32 coefficient rows (one TMA bulk
+// copy of the packed, row-padded blocks, sh_bulk_issue) + the mbarrier.
 template <int DEG>
 struct GaussShSmem {
-    static constexpr int FLOATS = sh_bulk_ok<DEG>() ? 32 * sh_bulk_stride<DEG>() : sh_warp_floats<DEG>();
-    alignas(16) float rows[GPREP_T / 32][FLOATS];
+    alignas(16) float rows[GPREP_T / 32][32 * sh_bulk_stride<DEG>()];
     uint64_t bar[GPREP_T / 32];
 };
 
-// Start the warp's coefficient fetch (TMA bulk copies) at kernel entry.
+// Start the warp's coefficient fetch at kernel entry.
 template <int DEG>
 __device__ __forceinline__ void gauss_sh_prefetch(const ges_scene_t& sc, GaussShSmem<DEG>& sm) {
-    if constexpr (sh_bulk_ok<DEG>()) {
-        const int w = threadIdx.x >> 5;
-        const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31u);
-        sh_bulk_issue<DEG>(sc.g_sh, i0, sc.n_gaussians, sm.rows[w], &sm.bar[w]);
-    }
+    const int w = threadIdx.x >> 5;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31u);
+    sh_bulk_issue<DEG>(sc.g_sh, i0, sc.n_gaussians, sm.rows[w], &sm.bar[w]);
 }
 
+// View colour of this lane's Gaussian (forward.py:99-109) from the warp's
+// fetched rows; all lanes call it.
 template <int DEG>
 __device__ __forceinline__ float3 gauss_view_colour(const ges_scene_t& sc, const CamK& cam, d3 p,
                                                     GaussShSmem<DEG>& sm) {
@@ -329,11 +327,7 @@ __device__ __forceinline__ float3 gauss_view_colour(const ges_scene_t& sc, const
     const float inv = rsqrtf(fmaxf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), 1e-24f));   // (2 ulp)
     const int w = threadIdx.x >> 5;
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31u);
-    if constexpr (sh_bulk_ok<DEG>()) {
-        return sh_color_bulk<DEG>(sm.rows[w], &sm.bar[w], i0, sc.n_gaussians, dx * inv, dy * inv, dz * inv);
-    } else {
-        return sh_color_warp<DEG>(sc.g_sh, i0, sc.n_gaussians, sm.rows[w], dx * inv, dy * inv, dz * inv);
-    }
+    return sh_color_bulk<DEG>(sm.rows[w], &sm.bar[w], i0, sc.n_gaussians, dx * inv, dy * inv, dz * inv);
 }
 
 // 3D EWA: geometry.py:114-132 + forward.py:252-290.

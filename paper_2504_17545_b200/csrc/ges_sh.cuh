@@ -63,48 +63,6 @@ __device__ __forceinline__ float3 sh_color(const float* __restrict__ sh, float x
     return sh_color_regs<DEG>(c, x, y, z);
 }
 
-// Shared floats per warp for sh_color_warp<DEG>.
-template <int DEG>
-__host__ __device__ constexpr int sh_warp_floats() { return 32 * ((3 * (DEG + 1) * (DEG + 1)) | 1); }
-
-// Warp-cooperative sh_color for the warp's 32 consecutive primitives
-// i0 .. i0+31 (< n): their coefficient blocks are contiguous, so the warp
-// loads them coalesced into its shared slice smw (row stride K*3 | 1 floats:
-// conflict-free column reads), then every lane evaluates its own primitive.
-// Must be called by all 32 lanes.
-template <int DEG>
-__device__ __forceinline__ float3 sh_color_warp(const float* __restrict__ sh, int64_t i0, int64_t n, float* smw,
-                                                float x, float y, float z) {
-    constexpr int K3 = 3 * (DEG + 1) * (DEG + 1), STR = K3 | 1;
-    const int lane = threadIdx.x & 31;
-    const int cnt = n - i0 < 32 ? (int)(n - i0) : 32;
-    const float* base = sh + i0 * K3;
-    if constexpr (K3 % 4 == 0) {   // float4 loads never straddle two primitives
-        const float4* b4 = reinterpret_cast<const float4*>(base);
-#pragma unroll
-        for (int t = lane; t < 8 * K3; t += 32) {
-            const int g = (4 * t) / K3, f = 4 * t - g * K3;
-            if (g < cnt) {
-                const float4 v = __ldg(b4 + t);
-                float* d = smw + g * STR + f;
-                d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-            }
-        }
-    } else {
-#pragma unroll
-        for (int t = lane; t < 32 * K3; t += 32) {
-            const int g = t / K3;
-            if (g < cnt) smw[g * STR + t - g * K3] = __ldg(base + t);
-        }
-    }
-    __syncwarp();
-    float c[K3];
-#pragma unroll
-    for (int j = 0; j < K3; ++j) c[j] = smw[lane * STR + j];
-    __syncwarp();
-    return sh_color_regs<DEG>(c, x, y, z);
-}
-
 // ---- TMA form of the warp's coefficient fetch (degrees 1 and 3: 48 / 192-byte
 // blocks, multiples of 16 B).  sh_bulk_issue: every lane starts a bulk copy
 // (cp.async.bulk, the Blackwell/Hopper TMA engine) of its primitive's block
@@ -114,30 +72,35 @@ __device__ __forceinline__ float3 sh_color_warp(const float* __restrict__ sh, in
 // does its float64 geometry; sh_color_bulk waits on the barrier and evaluates
 // from the row with 16-byte shared loads (no per-lane global loads or
 // shared stores).  Both must be called by all 32 lanes.
+// Row stride (floats) of the packed Gaussian SH blocks, in global memory AND
+// in the preprocess's shared rows: K*3 rounded up to 16 bytes, plus 16 bytes
+// when that is an even number of 16-byte units (4, 12, 28, 52 floats for
+// degrees 0-3), so the rows' 16-byte reads by 8 lanes hit distinct bank
+// groups and a warp's 32 consecutive rows arrive with ONE bulk copy.
+__host__ __device__ constexpr int gsh_stride(int deg) {
+    return (((3 * (deg + 1) * (deg + 1) + 3) & ~3) / 4) % 2 == 0 ? ((3 * (deg + 1) * (deg + 1) + 3) & ~3) + 4
+                                                                  : ((3 * (deg + 1) * (deg + 1) + 3) & ~3);
+}
 template <int DEG>
-__host__ __device__ constexpr int sh_bulk_stride() { return ((3 * (DEG + 1) * (DEG + 1) + 3) & ~3) + 4; }
-template <int DEG>
-__host__ __device__ constexpr bool sh_bulk_ok() { return (3 * (DEG + 1) * (DEG + 1)) % 4 == 0; }
+__host__ __device__ constexpr int sh_bulk_stride() { return gsh_stride(DEG); }
 
+// One bulk copy (cp.async.bulk, the TMA engine) of the warp's rows i0 ..
+// i0+31 (< n) into its shared slice, completing on the warp's mbarrier.
 template <int DEG>
 __device__ __forceinline__ void sh_bulk_issue(const float* __restrict__ sh, int64_t i0, int64_t n, float* smw,
                                               uint64_t* bar) {
-    constexpr int K3 = 3 * (DEG + 1) * (DEG + 1), STR = sh_bulk_stride<DEG>();
+    constexpr int STR = sh_bulk_stride<DEG>();
     const int lane = threadIdx.x & 31;
     const int cnt = n - i0 < 32 ? (int)(n - i0) : 32;
     if (cnt <= 0) return;   // a warp past the end has nothing to fetch (and never waits)
-    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
     if (lane == 0) {
+        const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(cnt * K3 * 4) : "memory");
-    }
-    __syncwarp();
-    if (lane < cnt) {
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smw + lane * STR);
-        const float* src = sh + (i0 + lane) * K3;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(cnt * STR * 4) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(dst), "l"(src), "r"(K3 * 4), "r"(b) : "memory");
+                     ::"r"((uint32_t)__cvta_generic_to_shared(smw)), "l"(sh + i0 * STR), "r"(cnt * STR * 4), "r"(b)
+                     : "memory");
     }
 }
 
@@ -153,9 +116,9 @@ __device__ __forceinline__ float3 sh_color_bulk(const float* smw, uint64_t* bar,
                      : "=r"(done) : "r"(b) : "memory");
     }
     const float4* row = reinterpret_cast<const float4*>(smw + (threadIdx.x & 31) * STR);
-    float c[K3];
+    float c[(K3 + 3) & ~3];
 #pragma unroll
-    for (int j = 0; j < K3 / 4; ++j) {
+    for (int j = 0; j < (K3 + 3) / 4; ++j) {
         const float4 v = row[j];
         c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
     }
