@@ -36,7 +36,7 @@ def parse():
     p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     p.add_argument("--views", type=int, default=None, help="views per rank per step")
     p.add_argument("--ss", type=int, default=1, choices=[1, 4])
-    p.add_argument("--streams", type=int, default=12, help="CUDA streams pipelining the views of a step")
+    p.add_argument("--streams", type=int, default=16, help="CUDA streams pipelining the views of a step")
     p.add_argument("--layers", default="full", choices=["full", "surfels_only", "gaussians_only"])
     p.add_argument("--gather", default="peer", choices=["peer", "nccl"],
                    help="N > 1: frames to rank 0 through peer memory written by the tile kernel, or NCCL gather")
