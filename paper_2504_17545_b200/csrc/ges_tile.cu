@@ -262,13 +262,6 @@ __device__ __forceinline__ void resolve_surfel_colors(const TileArgs& a, Smem& s
     }
 }
 
-#ifndef GES_P2_INCR
-#define GES_P2_INCR 1   // Gaussian power of a 2 x 2 pixel block by finite differences
-#endif
-#ifndef GES_P1_MERGED
-#define GES_P1_MERGED 1   // surfel test: one candidate branch per thread and survivor
-#endif
-
 #ifndef GES_TILE_MINB2
 #define GES_TILE_MINB2 4   // resident CTAs per SM for the 4-sample variants (64 registers)
 #endif
@@ -482,10 +475,8 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 const float den0 = fmaf(A.z, ly0, fmaf(A.y, lx0, A.x));
                 const float U0 = fmaf(B.z, ly0, fmaf(B.y, lx0, B.x));
                 const float V0 = fmaf(C.y, ly0, fmaf(C.x, lx0, B.w));
-#if GES_P1_MERGED
                 float dens[NS];
                 bool cand[NS], anyc = false;
-#endif
 #pragma unroll
                 for (int gy = 0; gy < G; ++gy)
 #pragma unroll
@@ -508,7 +499,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                         // multiplied out, den > 0 <=> t > 0: with den <= 0 the product
                         // bt*den is <= 0 or NaN and the filter fails); |n.d| > eps|d|, the
                         // exact t > 0.01 and the packed-key comparison run only for candidates
-#if GES_P1_MERGED
                         dens[s] = den;
                         cand[s] = r2 <= den * den && Awf <= bt[s] * den;
                         anyc = anyc || cand[s];
@@ -527,18 +517,6 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                         bid[s] = take ? sid : bid[s];
                     }
                 }
-#else
-                        if (r2 <= den * den && Awf <= bt[s] * den) {
-                            const float t = A.w * rcp_ftz(den);   // 2 ulp: ties are flagged
-                            const uint32_t sid = __float_as_uint(C.z);
-                            GES_STAT(4, 1);
-                            if (den > pe && t > NEAR_F && (t < bt[s] || (t == bt[s] && sid < bid[s]))) {
-                                bt[s] = t;
-                                bid[s] = sid;
-                            }
-                        }
-                    }
-#endif
 #ifdef GES_STATS
                 if (__ballot_sync(0xffffffffu, st_any) == 0u && lane == 0) GES_STAT(16, 1);
 #endif
@@ -725,7 +703,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                 // pixel (0,0) directly, its neighbours by the exact finite differences
                 // (a (2dx + 1) + b dy, c (2dy + 1) + b dx; the diagonal adds b)
                 float pwv[NP];
-                if constexpr (GK == 3 && PX == 2 && GES_P2_INCR) {
+                if constexpr (GK == 3 && PX == 2) {
                     const float dx = lxs[0] - w[0], dy = lys[0] - w[1];
                     const float bdx = w[3] * dx;
                     const float p00 = fmaf(w[2] * dx, dx, fmaf(w[4] * dy, dy, bdx * dy));
@@ -740,7 +718,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                         // forward.py:301-311; the conic is pre-scaled by log2(e), so
                         // exp is one ex2 (branch-free: most survivors' pixels pass)
                         float pw;
-                        if constexpr (PX == 2 && GES_P2_INCR) {
+                        if constexpr (PX == 2) {
                             pw = pwv[p];
                         } else {
                             const float dx = lx - w[0], dy = ly - w[1];
