@@ -54,8 +54,9 @@ __device__ __forceinline__ void quat_cols(float4 qf, d3& c0, d3& c1, d3& c2) {
 }
 
 // Screen AABB of the projected disc {q + a m1 + b m2 : a^2+b^2<=1}
-// (geometry.py:273-302) -> inclusive pixel ranges with 0.5 px padding
-// (forward.py:85-96).  Returns false if the range is empty.
+// (geometry.py:273-302) -> inclusive ranges of the pixels whose centres it
+// contains (forward.py:85-96 pads them by another half pixel).  Returns false
+// if the range is empty.
 //
 // The ranges only cull (every pixel in them still gets the exact coverage
 // test), so they need to contain the reference's, not to equal them.  The
@@ -95,8 +96,12 @@ __device__ bool disc_ranges(d3 q, d3 m1, d3 m2, const CamK& c, int& x0, int& x1,
         lo[ax] = clo - pad;
         hi[ax] = chi + pad;
     }
-    const float fx0 = ceilf(lo[0] - 0.5f - 0.5f), fx1 = floorf(hi[0] + 0.5f - 0.5f);
-    const float fy0 = ceilf(lo[1] - 0.5f - 0.5f), fy1 = floorf(hi[1] + 0.5f - 0.5f);
+    // pixels whose centre p + 0.5 lies in [lo, hi]: a covered pixel's centre is
+    // inside the projected ellipse, so inside its (padded) box -- the
+    // reference's extra half-pixel of padding (forward.py:85-96) only adds
+    // pixels that fail the exact test
+    const float fx0 = ceilf(lo[0] - 0.5f), fx1 = floorf(hi[0] - 0.5f);
+    const float fy0 = ceilf(lo[1] - 0.5f), fy1 = floorf(hi[1] - 0.5f);
     // A disc whose padded box lies entirely beyond an image edge covers no
     // pixel.  The reference's clamp turns its range into the edge row/column
     // (forward.py:85-96), so every off-screen disc is a candidate of the
@@ -386,8 +391,9 @@ __global__ void __launch_bounds__(GPREP_T, GES_GPREP_MINB) k_gauss3_prep(ges_sce
             if (v > n - 1.0) return n - 1;
             return (int)v;
         };
-        const double fx0 = ceil(mx - rx - 0.5 - 0.5), fx1 = floor(mx + rx + 0.5 - 0.5);
-        const double fy0 = ceil(my - ry - 0.5 - 0.5), fy1 = floor(my + ry + 0.5 - 0.5);
+        // pixel centres inside the (widened) support box (see disc_ranges)
+        const double fx0 = ceil(mx - rx - 0.5), fx1 = floor(mx + rx - 0.5);
+        const double fy0 = ceil(my - ry - 0.5), fy1 = floor(my + ry - 0.5);
         // off-screen support box: no pixel of the image reaches alpha >= 1/255
         // (the reference clamps it onto the edge tiles and rejects it per pixel)
         valid = !(fx0 > cam.W - 1.0 || fx1 < 0.0 || fy0 > cam.H - 1.0 || fy1 < 0.0);
