@@ -43,12 +43,6 @@ __device__ unsigned long long g_stats[24];
 #define GES_STAT(i, v) ((void)0)
 #endif
 
-// Rows of pass-1 culling regions per warp patch: 2 (regions of 2 x 2 lanes)
-// or 4 (2 x 1 lanes).
-#ifndef GES_RROWS
-#define GES_RROWS 4
-#endif
-
 // Warps per CTA.  The 8 warps of a tile never synchronise after the
 // prologue, so a tile can be split over 8 / WPC CTAs: a CTA's registers are
 // held until its slowest warp finishes, and small CTAs hand them back warp by
@@ -66,7 +60,7 @@ struct __align__(16) TileSmem {
                                 // Gaussian records, then the colour tasks
     uint32_t wpk[4][32 * WPC];  // per lane: packed indices of its samples' winners, parked
                                 // in shared memory through the Gaussian pass
-    float4 rmax[WPC][GES_RROWS];   // per warp: max best depth of each of its 4 x GES_RROWS regions of
+    float4 rmax[WPC][2];        // per warp: max best depth of each of its 4 x 2 regions of
                                 // 2 x 2 lanes (pass-1 culling)
     uint32_t slab_end[NSLAB];   // this tile's surfel slab ends (relative list positions)
     uint32_t gslab_end[NSLAB];  // this tile's Gaussian slab ends
@@ -78,14 +72,13 @@ struct __align__(16) TileSmem {
 __device__ __forceinline__ float slab_floor(const uint32_t* ends, const SlabMap& m, uint32_t rel, int lane) {
     return m.lower(slab_of_pos(ends, rel, lane));
 }
-// Max of the per-region depth bounds of a warp (4 x RR regions of 2 x (4/RR)
-// lanes, RW x RH samples) over the regions that the pixel range [x0, x1] x
-// [y0, y1] (relative to the patch origin, overlapping the patch) touches.
-template <int RW, int RH>
+// Max of the per-region depth bounds of a warp (4 x 2 regions of 2 x 2 lanes,
+// RW pixels square) over the regions that the pixel range [x0, x1] x [y0, y1]
+// (relative to the patch origin, overlapping the patch) touches.
+template <int RW>
 __device__ __forceinline__ float region_max(const float4* rmax, int x0, int x1, int y0, int y1) {
-    constexpr int RR = GES_RROWS;
     const int c0 = max(x0, 0) / RW, c1 = min(x1, 4 * RW - 1) / RW;
-    const int q0 = max(y0, 0) / RH, q1 = min(y1, RR * RH - 1) / RH;
+    const int q0 = max(y0, 0) / RW, q1 = min(y1, 2 * RW - 1) / RW;
     auto rowmax = [&](const float4& m) {
         float v = -INFINITY;
         v = (c0 <= 0) ? fmaxf(v, m.x) : v;
@@ -94,23 +87,16 @@ __device__ __forceinline__ float region_max(const float4* rmax, int x0, int x1, 
         v = (c1 >= 3) ? fmaxf(v, m.w) : v;
         return v;
     };
-    float r = -INFINITY;
-#pragma unroll
-    for (int q = 0; q < RR; ++q)
-        if (q >= q0 && q <= q1) r = fmaxf(r, rowmax(rmax[q]));
+    float r = q0 == 0 ? rowmax(rmax[0]) : -INFINITY;
+    if (q1 == 1) r = fmaxf(r, rowmax(rmax[1]));
     return r;
 }
-// Per-region maxima of v (lane = x + 8 y in the warp's 8 x 4 lane grid) into
-// rm[4 x RR]; returns the max over the warp.
+// Per-region maxima of v over 2 x 2 lanes (lane = x + 8 y in the warp's 8 x 4
+// lane grid) into rm[4 x 2]; returns the max over the warp.
 __device__ __forceinline__ float region_reduce(float m, float* rm, int lane) {
     m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-    if constexpr (GES_RROWS == 4) {   // regions of 2 x 1 lanes
-        if ((lane & 1) == 0) rm[((lane & 7) >> 1) + 4 * (lane >> 3)] = m;
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
-    } else {                          // regions of 2 x 2 lanes
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
-        if ((lane & 9) == 0) rm[((lane & 7) >> 1) + 4 * (lane >> 4)] = m;
-    }
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+    if ((lane & 9) == 0) rm[((lane & 7) >> 1) + 4 * (lane >> 4)] = m;
     m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
     m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
     return fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
@@ -429,7 +415,7 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
                     GES_STAT(17, 1);
 #endif
                 // nearest disc depth vs the regions its pixel range overlaps
-                if (live) live = !(r3.x > region_max<2 * G, 4 / GES_RROWS * G>(sm.rmax[wl], span_lo(sxr) - wx0, span_hi(sxr) - wx0,
+                if (live) live = !(r3.x > region_max<2 * G>(sm.rmax[wl], span_lo(sxr) - wx0, span_hi(sxr) - wx0,
                                                             span_lo(syr) - wy0, span_hi(syr) - wy0));
                 if (live) {
                     const SurfRec* r = a.srec + id;
