@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GES_ABI_VERSION 2
+#define GES_ABI_VERSION 3
 
 #define GES_OK 0
 #define GES_EINVAL 1

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # GES_B200_LIB overrides the library path (A/B runs of alternative builds)
 LIB_PATH = os.environ.get("GES_B200_LIB") or os.path.join(HERE, "libges_b200.so")
 
-ABI_VERSION = 2   # include/ges_b200.h GES_ABI_VERSION
+ABI_VERSION = 3   # include/ges_b200.h GES_ABI_VERSION
 GES_OK, GES_EINVAL, GES_EDEGREE, GES_EWORKSPACE, GES_ECUDA = 0, 1, 2, 3, 4
 GES_IMAGE_F32_RGB, GES_IMAGE_RGBA8 = 0, 1
 LAYERS = {"full": 0, "surfels_only": 1, "gaussians_only": 2}

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     assert set(declared) == set(_lib.EXPORTS)
     for name in declared:
         assert hasattr(L, name), name
-    assert L.ges_abi_version() == 2
+    assert L.ges_abi_version() == 3
 
 
 def test_library_is_sm100a():
