@@ -49,6 +49,19 @@ def test_scene_bytes_and_workspace_validation():
     assert L.ges_workspace_bytes(C.byref(sc), C.byref(cam), C.byref(st), 1 << 16, 1 << 16) == 0
 
 
+def test_scene_bytes_pad_gaussian_sh_rows():
+    """ABI 3: the packed Gaussian SH rows are padded to 4 / 12 / 28 / 52 floats
+    (an odd number of 16-byte units, one bulk copy per warp in the
+    preprocess); surfel SH rows stay 3K floats."""
+    L = _lib.lib()
+    n = 1 << 16   # (multiples of the 256-byte carve alignment)
+    for deg, stride in ((0, 4), (1, 12), (2, 28), (3, 52)):
+        k3 = 3 * (deg + 1) ** 2
+        g = L.ges_scene_bytes(0, n, deg)
+        assert g == n * (3 * 16 + 4 * stride)
+        assert L.ges_scene_bytes(n, 0, deg) == n * (16 + 16 + 4 + 4 * k3 + 4 + 4)
+
+
 def test_error_codes_map_to_reference_exceptions():
     L = _lib.lib()
     sc = _lib.Scene(n_surfels=0, n_gaussians=0, sh_degree=7, gaussian_dim=3)
