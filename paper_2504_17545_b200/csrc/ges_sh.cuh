@@ -63,15 +63,14 @@ __device__ __forceinline__ float3 sh_color(const float* __restrict__ sh, float x
     return sh_color_regs<DEG>(c, x, y, z);
 }
 
-// ---- TMA form of the warp's coefficient fetch (degrees 1 and 3: 48 / 192-byte
-// blocks, multiples of 16 B).  sh_bulk_issue: every lane starts a bulk copy
-// (cp.async.bulk, the Blackwell/Hopper TMA engine) of its primitive's block
-// into its own shared row, all completing on one mbarrier; the row stride
-// (K*3 rounded up to 4 floats + 4) keeps the rows' 16-byte reads
-// conflict-free.  Issued at kernel entry, so the loads fly while the caller
-// does its float64 geometry; sh_color_bulk waits on the barrier and evaluates
-// from the row with 16-byte shared loads (no per-lane global loads or
-// shared stores).  Both must be called by all 32 lanes.
+// ---- TMA form of the warp's coefficient fetch (Gaussian preprocess).
+// sh_bulk_issue: one lane starts ONE bulk copy (cp.async.bulk, the TMA
+// engine) of the warp's 32 consecutive padded rows into its shared slice,
+// completing on the warp's mbarrier.  Issued at kernel entry, so the load
+// flies while the caller does its float64 geometry; sh_color_bulk waits on
+// the barrier and evaluates from the lane's row with 16-byte shared loads
+// (no per-lane global loads or shared stores).  Both must be called by all
+// 32 lanes.
 // Row stride (floats) of the packed Gaussian SH blocks, in global memory AND
 // in the preprocess's shared rows: K*3 rounded up to 16 bytes, plus 16 bytes
 // when that is an even number of 16-byte units (4, 12, 28, 52 floats for
