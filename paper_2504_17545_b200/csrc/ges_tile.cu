@@ -510,8 +510,11 @@ __global__ void __launch_bounds__(32 * tile_wpc<SS, PX>(), tile_min_blocks<SS, P
 #pragma unroll
                     for (int s = 0; s < NS; ++s) {
                         const float t = A.w * rcp_ftz(dens[s]);   // 2 ulp: ties are flagged
-                        const bool take = cand[s] && dens[s] > pe && t > NEAR_F &&
-                                          (t < bt[s] || (t == bt[s] && sid < bid[s]));
+                        // (t, sid) < (bt, bid) lexicographically as one 64-bit compare of
+                        // (float bits, id): t > 0 and bt >= 0, so the bits order like the values
+                        const unsigned long long kt = ((unsigned long long)__float_as_uint(t) << 32) | sid;
+                        const unsigned long long kb = ((unsigned long long)__float_as_uint(bt[s]) << 32) | bid[s];
+                        const bool take = cand[s] && dens[s] > pe && t > NEAR_F && kt < kb;
                         GES_STAT(4, cand[s]);
                         bt[s] = take ? t : bt[s];
                         bid[s] = take ? sid : bid[s];
